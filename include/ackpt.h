@@ -1,0 +1,249 @@
+/*
+ * ackpt.h — C ABI of the B200-native asynchronous multistage checkpointing
+ * hot path (arXiv 1806.01117).  Every entry point returns an int status
+ * (ACKPT_OK == 0) and never throws across the boundary; the message of the
+ * last failure on the calling thread is ackpt_last_error().
+ *
+ * Reference interfaces replaced (paths relative to the reference package
+ * root pkg/src/asyncckpt/):
+ *   status codes            errors.py:4-37  (one code per exception class)
+ *   ackpt_forward_cost      schedule.py:161-169   forward_cost(n, s)
+ *   ackpt_revolve_schedule  schedule.py:188-235   revolve_schedule(ScheduleParams)
+ *   ackpt_taped_schedule    schedule.py:279-285   taped_schedule(length)
+ *   ackpt_best_split        schedule.py:177-181   _best_split(length, slots, table)
+ *   ackpt_interval_length   perfmodel.py:56-64    interval_length(t_t, t_a)
+ *   ackpt_lstm_*            lstm.py:110-163       _gates / lstm_forward_step /
+ *                                                 lstm_backward_step / loss /
+ *                                                 loss_gradient_seed
+ *   ackpt_tier_*            storage.py:181-278    TransferTicket + Level2Backend
+ *                                                 (begin_store/begin_fetch/wait/poll/contains/close)
+ *   ackpt_engine_*          runtime.py:162-381    _Execution / execute / calibrate
+ *   ackpt_crc32c            storage.py:49-68      crc32c(data, crc)
+ *
+ * Memory ownership: device buffers passed in are owned by the caller (torch);
+ * the engine owns its checkpoint buffer pool (HBM), the tier owns its pinned
+ * host slab.  Streams are plain cudaStream_t handles passed as void*.
+ */
+#ifndef ACKPT_H_
+#define ACKPT_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#if defined(__GNUC__)
+#define ACKPT_API __attribute__((visibility("default")))
+#else
+#define ACKPT_API
+#endif
+
+/* ---- status codes: 1..8 mirror errors.py:8-37 in declaration order ---- */
+enum {
+  ACKPT_OK = 0,
+  ACKPT_INFEASIBLE_SCHEDULE = 1, /* errors.py:8  InfeasibleSchedule */
+  ACKPT_SIZE_MISMATCH = 2,       /* errors.py:12 SizeMismatch */
+  ACKPT_SLOT_OUT_OF_RANGE = 3,   /* errors.py:16 SlotOutOfRange */
+  ACKPT_SLOT_UNWRITTEN = 4,      /* errors.py:20 SlotUnwritten */
+  ACKPT_MISSING_KEY = 5,         /* errors.py:24 MissingKey */
+  ACKPT_CHECKSUM_MISMATCH = 6,   /* errors.py:28 ChecksumMismatch */
+  ACKPT_STORAGE_FULL = 7,        /* errors.py:32 StorageFull */
+  ACKPT_EXECUTION_ERROR = 8,     /* errors.py:36 ExecutionError */
+  ACKPT_VALUE_ERROR = 9,         /* ValueError raised by argument checks */
+  ACKPT_CUDA_ERROR = 10,         /* any cudaError_t (reported as ExecutionError) */
+  ACKPT_NOT_READY = 11           /* ackpt_tier_poll: transfer still in flight */
+};
+
+ACKPT_API const char* ackpt_last_error(void);
+ACKPT_API const char* ackpt_version(void);
+
+/* ---- schedule actions (schedule.py:70-114) ---- */
+enum {
+  ACKPT_ADVANCE = 0, /* a=from_step b=to_step   schedule.py:70  */
+  ACKPT_SAVE = 1,    /* a=step      b=slot      schedule.py:78  */
+  ACKPT_LOAD = 2,    /* a=slot                  schedule.py:86  */
+  ACKPT_TAPE = 3,    /* a=from_step b=to_step   schedule.py:93  */
+  ACKPT_REVERSE = 4, /* a=step                  schedule.py:102 */
+  ACKPT_DONE = 5     /*                         schedule.py:109 */
+};
+
+typedef struct ackpt_action {
+  int32_t op;
+  int32_t reserved;
+  int64_t a;
+  int64_t b;
+} ackpt_action;
+
+/* Host scheduler.  Tables are built once and cached per process (grow-only,
+ * like schedule.py:121-136); values and tie-breaks are bit-exact. */
+ACKPT_API int ackpt_forward_cost(int64_t n, int64_t s, int64_t* out);
+ACKPT_API int ackpt_best_split(int64_t length, int64_t slots, int64_t* out);
+/* Writes up to cap actions (Done included); *len receives the full count, so
+ * a call with cap=0 sizes the buffer.  Fails with INFEASIBLE_SCHEDULE/VALUE_ERROR
+ * exactly where ScheduleParams.__post_init__ (schedule.py:59-66) raises. */
+ACKPT_API int ackpt_revolve_schedule(int64_t n, int64_t s, ackpt_action* out, int64_t cap,
+                                     int64_t* len);
+ACKPT_API int ackpt_taped_schedule(int64_t length, ackpt_action* out, int64_t cap, int64_t* len);
+/* Exact ceil(Fraction(t_t)/Fraction(t_a)), at least 1 (perfmodel.py:56-64). */
+ACKPT_API int ackpt_interval_length(double t_t, double t_a, int64_t* out);
+/* Threads used by the cost-table build (0 = all hardware threads). */
+ACKPT_API int ackpt_set_schedule_threads(int32_t threads);
+
+/* ---- LSTM cell operator on device (lstm.py:39-173, batched) ----
+ * State layout in HBM, dtype T (f32 or f64): [h(d, B); c(d, B)] with the batch
+ * index fastest, i.e. element (part, j, b) at ((part*d + j)*B + b).  At B=1
+ * this is exactly the reference's byte image [h(d), c(d)] (lstm.py:99-107). */
+enum { ACKPT_F32 = 0, ACKPT_F64 = 1 };
+
+typedef struct ackpt_lstm ackpt_lstm;
+
+/* Weights are given in float64 exactly as LstmCell holds them
+ * (w_*: d x 2d row-major, b_*: d, xs: n x d, target: d) and are rounded to
+ * the cell dtype once; the per-step input projection W_x x_k + b is
+ * precomputed in float64 and then rounded. */
+ACKPT_API int ackpt_lstm_create(int32_t d, int64_t n_steps, int64_t batch, int32_t dtype,
+                                const double* w_f, const double* w_i, const double* w_o,
+                                const double* w_c, const double* b_f, const double* b_i,
+                                const double* b_o, const double* b_c, const double* xs,
+                                const double* target, ackpt_lstm** out);
+ACKPT_API int ackpt_lstm_destroy(ackpt_lstm* cell);
+ACKPT_API int64_t ackpt_lstm_state_bytes(const ackpt_lstm* cell);
+/* One forward step k: state_k -> state_{k+1} (lstm.py:123-129). */
+ACKPT_API int ackpt_lstm_forward(const ackpt_lstm* cell, int64_t step, const void* state_in,
+                                 void* state_out, void* stream);
+/* Fused run of steps [from, to): one launch, state kept in registers. */
+ACKPT_API int ackpt_lstm_advance(const ackpt_lstm* cell, int64_t from_step, int64_t to_step,
+                                 const void* state_in, void* state_out, void* stream);
+/* One adjoint step k (lstm.py:132-152). */
+ACKPT_API int ackpt_lstm_backward(const ackpt_lstm* cell, int64_t step, const void* state,
+                                  const void* adjoint_in, void* adjoint_out, void* stream);
+/* seed = [2(h - target), 0] (lstm.py:161-163). */
+ACKPT_API int ackpt_lstm_seed(const ackpt_lstm* cell, const void* final_state, void* adjoint_out,
+                              void* stream);
+/* Per-sequence loss sum_j (h_j - target_j)^2 (lstm.py:155-158), B values of dtype T. */
+ACKPT_API int ackpt_lstm_loss(const ackpt_lstm* cell, const void* final_state, void* loss_out,
+                              void* stream);
+
+/* ---- generic operator plugin (runtime.py:62-87 OperatorPair) ----
+ * The engine calls these on its compute stream; device pointers only. */
+typedef int (*ackpt_forward_fn)(void* ctx, int64_t step, const void* state_in, void* state_out,
+                                void* stream);
+typedef int (*ackpt_backward_fn)(void* ctx, int64_t step, const void* state,
+                                 const void* adjoint_in, void* adjoint_out, void* stream);
+typedef int (*ackpt_seed_fn)(void* ctx, const void* final_state, void* adjoint_out, void* stream);
+/* Optional: fused forward over [from, to); NULL means per-step forward. */
+typedef int (*ackpt_advance_fn)(void* ctx, int64_t from_step, int64_t to_step,
+                                const void* state_in, void* state_out, void* stream);
+
+typedef struct ackpt_operator {
+  void* ctx;
+  ackpt_forward_fn forward;
+  ackpt_backward_fn backward;
+  ackpt_seed_fn seed; /* NULL: the adjoint seed is given to ackpt_engine_run */
+  ackpt_advance_fn advance;
+  int64_t state_bytes; /* OperatorPair.state_size */
+  int64_t n_steps;     /* OperatorPair.n_steps */
+} ackpt_operator;
+
+/* Fills *out with the built-in LSTM operator bound to cell. */
+ACKPT_API int ackpt_lstm_operator(ackpt_lstm* cell, ackpt_operator* out);
+
+/* ---- Level-2 tier: HBM <-> pinned host DRAM (storage.py:181-278) ---- */
+typedef struct ackpt_tier ackpt_tier;
+typedef int64_t ackpt_ticket;
+
+/* capacity: number of keys the pinned slab can hold; slot_bytes: bytes per key.
+ * The slab is allocated here (outside any timed window). */
+ACKPT_API int ackpt_tier_create(int64_t capacity, int64_t slot_bytes, ackpt_tier** out);
+ACKPT_API int ackpt_tier_destroy(ackpt_tier* tier);
+/* Stall injection for contention tests: each transfer holds its copy stream
+ * for at least latency_us + bytes / bandwidth (bandwidth <= 0: no limit),
+ * like SimulatedBackend.transfer_seconds (storage.py:300-301). */
+ACKPT_API int ackpt_tier_set_throttle(ackpt_tier* tier, double latency_s, double bandwidth);
+/* Store bytes at device pointer src under key; the copy starts after all work
+ * already enqueued on after_stream (may be NULL). */
+ACKPT_API int ackpt_tier_begin_store(ackpt_tier* tier, int64_t key, int64_t step,
+                                     const void* src, int64_t bytes, void* after_stream,
+                                     ackpt_ticket* out);
+/* Fetch key into device pointer dst; a missing key is reported at wait
+ * (storage.py:310-311 raises inside the worker, surfaced by wait). */
+ACKPT_API int ackpt_tier_begin_fetch(ackpt_tier* tier, int64_t key, void* dst, int64_t bytes,
+                                     void* after_stream, ackpt_ticket* out);
+/* Blocks the host; idempotent.  *step_out (may be NULL) receives the stored step. */
+ACKPT_API int ackpt_tier_wait(ackpt_tier* tier, ackpt_ticket ticket, int64_t* step_out);
+/* Makes stream wait for the ticket on the device (no host block). */
+ACKPT_API int ackpt_tier_stream_wait(ackpt_tier* tier, ackpt_ticket ticket, void* stream);
+/* ACKPT_OK when complete, ACKPT_NOT_READY while in flight. */
+ACKPT_API int ackpt_tier_poll(ackpt_tier* tier, ackpt_ticket ticket);
+ACKPT_API int ackpt_tier_contains(ackpt_tier* tier, int64_t key, int32_t* out);
+/* Byte length stored under key (MISSING_KEY if absent). */
+ACKPT_API int ackpt_tier_key_bytes(ackpt_tier* tier, int64_t key, int64_t* out);
+/* Host-visible pointer of a stored key's bytes (pinned), for tests / file stage. */
+ACKPT_API int ackpt_tier_host_ptr(ackpt_tier* tier, int64_t key, void** out);
+ACKPT_API int ackpt_tier_clear(ackpt_tier* tier);
+
+/* ---- executor (runtime.py:90-381) ---- */
+enum { ACKPT_FULL_STORAGE = 0, ACKPT_REVOLVE = 1, ACKPT_MULTISTAGE = 2 };
+
+typedef struct ackpt_stats {
+  /* ExecutionStats fields, same meaning (runtime.py:90-98) */
+  int64_t forward_evals;
+  int64_t backward_evals;
+  int64_t stores_issued;
+  int64_t prefetches_issued;
+  double stall_seconds;
+  int64_t peak_l1_bytes;
+  double wall_seconds;
+  /* B200 extras */
+  double gpu_seconds;       /* compute-stream event time, first to last action */
+  int64_t kernel_launches;  /* kernels this run enqueued */
+  int64_t interval;         /* multistage I actually used (0 otherwise) */
+  int64_t fallback;         /* 1 if multistage fell back to plain revolve */
+  int64_t device_buffers;   /* HBM state buffers held by the pool */
+  int64_t link_bytes;       /* bytes moved over the host link */
+  int64_t fused_advances;   /* Advance actions run as one fused launch */
+} ackpt_stats;
+
+typedef struct ackpt_engine ackpt_engine;
+
+ACKPT_API int ackpt_engine_create(const ackpt_operator* op, ackpt_engine** out);
+ACKPT_API int ackpt_engine_destroy(ackpt_engine* engine);
+/* Plans the strategy (and sizes/allocates the HBM buffer pool) outside the
+ * timed window, like execute() does before t0 (runtime.py:355-362).
+ * MULTISTAGE needs interval >= 1: run ackpt_engine_calibrate + ackpt_interval_length
+ * first for the reference's interval=None (runtime.py:325-336). */
+ACKPT_API int ackpt_engine_prepare(ackpt_engine* engine, int32_t strategy, int64_t slots,
+                                   int64_t interval, ackpt_tier* tier);
+/* 0 (default): the reference's per-step operator contract, one launch per
+ * forward step.  1: run whole Advance actions as one fused launch when the
+ * operator provides advance(); counters are unchanged. */
+ACKPT_API int ackpt_engine_set_fusion(ackpt_engine* engine, int32_t fuse_advance);
+/* Mirrors CKPT_DISABLE_PREFETCH=1 (runtime.py:302): -1 read the env var at run. */
+ACKPT_API int ackpt_engine_set_prefetch(ackpt_engine* engine, int32_t prefetch);
+/* One forward/backward pass (runtime.py:339-381).  seed may be NULL when the
+ * operator has a seed function.  Blocks until the adjoint is ready. */
+ACKPT_API int ackpt_engine_run(ackpt_engine* engine, const void* initial_state,
+                               const void* seed, void* adjoint_out, ackpt_stats* stats,
+                               void* stream);
+/* Multistage sweeps over an already prepared, non-fallback plan
+ * (runtime.py:384-417).  The forward sweep writes the final state. */
+ACKPT_API int ackpt_engine_forward_sweep(ackpt_engine* engine, const void* initial_state,
+                                         void* final_state, ackpt_stats* stats, void* stream);
+ACKPT_API int ackpt_engine_backward_sweep(ackpt_engine* engine, const void* seed,
+                                          void* adjoint_out, ackpt_stats* stats, void* stream);
+/* Median per-op times (t_a, t_b, t_t) over trial_steps (runtime.py:420-466);
+ * stores overwrite keys 0..trial_steps-1 of the tier. */
+ACKPT_API int ackpt_engine_calibrate(ackpt_engine* engine, ackpt_tier* tier, int64_t trial_steps,
+                                     const void* initial_state, double* t_a, double* t_b,
+                                     double* t_t);
+/* Interval the last prepare chose. */
+ACKPT_API int64_t ackpt_engine_interval(const ackpt_engine* engine);
+
+/* ---- CRC32C (storage.py:49-68), hardware crc32 instruction when present ---- */
+ACKPT_API uint32_t ackpt_crc32c(const void* data, int64_t len, uint32_t crc);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ACKPT_H_ */

@@ -1,0 +1,67 @@
+// Internal helpers shared by the native translation units of libackpt.
+#pragma once
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/ackpt.h"
+
+namespace ackpt {
+
+// Typed failure carrying one of the ACKPT_* status codes.  Thrown inside the
+// library and converted to a status at every extern "C" boundary.
+struct Error : std::runtime_error {
+  int code;
+  Error(int c, const std::string& msg) : std::runtime_error(msg), code(c) {}
+};
+
+void set_last_error(const std::string& msg);
+
+[[noreturn]] inline void fail(int code, const std::string& msg) { throw Error(code, msg); }
+
+// Runs fn and converts any exception into a status code + last-error string.
+template <class F>
+int guard(F&& fn) {
+  try {
+    fn();
+    return ACKPT_OK;
+  } catch (const Error& e) {
+    set_last_error(e.what());
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    set_last_error("out of host memory");
+    return ACKPT_STORAGE_FULL;
+  } catch (const std::exception& e) {
+    set_last_error(e.what());
+    return ACKPT_EXECUTION_ERROR;
+  } catch (...) {
+    set_last_error("unknown native failure");
+    return ACKPT_EXECUTION_ERROR;
+  }
+}
+
+// Scheduler internals used by the executor (schedule.cpp).
+struct Action {
+  int32_t op;
+  int64_t a;
+  int64_t b;
+};
+
+void revolve_actions(int64_t n, int64_t s, std::vector<Action>& out);
+void taped_actions(int64_t length, std::vector<Action>& out);
+int64_t forward_cost_exact(int64_t n, int64_t s);
+int64_t interval_length_exact(double t_t, double t_a);
+// slot_read_liveness (schedule.py:347-362): for each action index holding a
+// Save, the index of the last Load reading that write, or -1.
+void slot_read_liveness(const std::vector<Action>& actions, std::vector<int64_t>& last_read);
+
+}  // namespace ackpt
+
+#define ACKPT_CUDA_CHECK(expr)                                                        \
+  do {                                                                                \
+    cudaError_t _e = (expr);                                                          \
+    if (_e != cudaSuccess)                                                            \
+      ::ackpt::fail(ACKPT_CUDA_ERROR, std::string(#expr) + ": " + cudaGetErrorString(_e)); \
+  } while (0)

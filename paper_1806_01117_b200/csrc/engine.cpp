@@ -1,0 +1,758 @@
+// Executor: runs a reversal schedule of an operator pair on the GPU.
+//
+// B200-native restatement of the reference runtime (pkg/src/asyncckpt/runtime.py):
+//   _ByteLedger            runtime.py:123-159  -> Ledger (identical byte accounting)
+//   _Execution.forward     runtime.py:174-180  -> Run::forward (seed at first arrival at n)
+//   _Execution.backward    runtime.py:186-190  -> Run::backward
+//   wait_transfer          runtime.py:192-199  -> Run::wait_transfer (device-side wait;
+//                                                  stall = compute-stream idle time, CUDA events)
+//   run_schedule           runtime.py:201-252  -> Run::run_schedule
+//   _multistage_forward    runtime.py:269-294  -> Run::multistage_forward
+//   _multistage_backward   runtime.py:297-322  -> Run::multistage_backward
+//   execute                runtime.py:339-381  -> ackpt_engine_run
+//   calibrate              runtime.py:420-466  -> ackpt_engine_calibrate
+//
+// States live in a pool of HBM buffers.  Save/Load/Tape do not copy: a slot
+// or tape entry holds a reference-counted buffer id, the reference's
+// "bytes are immutable, keep a reference" semantics (runtime.py:221-233)
+// without any device-to-device traffic.  A buffer returns to the free list
+// when its last reference drops; all compute runs on one stream, so reuse is
+// stream-ordered.  Buffers handed to the copy engines are covered by event
+// waits: a store's source is released only after the compute stream waited for
+// the store (the reference's own "one store in flight" rule), and a fetch's
+// destination is written only after the copy stream waited for the compute
+// stream's position at issue time.
+//
+// The host interpreter never blocks inside the timed window: every wait is a
+// cudaStreamWaitEvent.  It runs once "dry" at prepare time to size the pool
+// and the timing-event pool exactly; the real run replays identical decisions.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cstdlib>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "common.h"
+
+namespace ackpt {
+// tier.cpp
+void tier_reserve_keys(ackpt_tier* t, const std::vector<int64_t>& keys);
+cudaEvent_t tier_ticket_event(ackpt_tier* t, ackpt_ticket id);
+int tier_ticket_status(ackpt_tier* t, ackpt_ticket id, std::string* msg);
+void tier_retire(ackpt_tier* t, ackpt_ticket id);
+int64_t tier_slot_bytes(const ackpt_tier* t);
+cudaStream_t tier_d2h(const ackpt_tier* t);
+}  // namespace ackpt
+
+namespace {
+
+struct SegPlan {
+  std::vector<ackpt::Action> actions;
+  std::vector<int64_t> last_read;  // slot_read_liveness
+};
+
+}  // namespace
+
+struct ackpt_engine {
+  ackpt_operator op{};
+  int64_t S = 0, n = 0;
+  // plan
+  bool prepared = false;
+  int strategy = -1;
+  int64_t slots = 0, interval = 0;
+  bool fallback = false;
+  ackpt_tier* tier = nullptr;
+  SegPlan plain;
+  std::vector<int64_t> boundaries;
+  std::map<int64_t, SegPlan> seg_by_len;
+  // resources
+  std::vector<void*> slabs;
+  std::vector<void*> bufs;
+  void* adj_internal = nullptr;
+  std::vector<cudaEvent_t> timing;  // pool of timing events
+  cudaEvent_t ev_start = nullptr, ev_end = nullptr, ev_sync = nullptr;
+  cudaStream_t compute = nullptr;
+  int fuse = 0;
+  int prefetch = -1;
+};
+
+namespace ackpt {
+namespace {
+
+struct Ledger {  // runtime.py:123-159
+  int64_t slot_bytes = 0, tape_bytes = 0, transfer_bytes = 0, peak = 0;
+  void bump() { peak = std::max(peak, slot_bytes + tape_bytes + transfer_bytes); }
+  void set_slots(int64_t b) {
+    slot_bytes = b;
+    bump();
+  }
+  void add_tape(int64_t b) {
+    tape_bytes += b;
+    bump();
+  }
+  void drop_tape(int64_t b) { tape_bytes -= b; }
+  void add_transfer(int64_t b) {
+    transfer_bytes += b;
+    bump();
+  }
+  void drop_transfer(int64_t b) { transfer_bytes -= b; }
+};
+
+constexpr int kExt = -1;  // the caller's initial state (read-only, never pooled)
+
+void check_op(int rc) {
+  if (rc != ACKPT_OK) fail(rc, std::string("operator: ") + ackpt_last_error());
+}
+
+bool env_prefetch() {
+  const char* v = std::getenv("CKPT_DISABLE_PREFETCH");  // runtime.py:302
+  return !(v && std::string(v) == "1");
+}
+
+struct Run {
+  ackpt_engine* E;
+  bool dry;
+  cudaStream_t s;
+  ackpt_stats st{};
+  Ledger ledger;
+  // buffer pool
+  std::vector<int> refs;
+  std::vector<int> free_list;
+  int in_use = 0, peak_in_use = 0;
+  const void* ext = nullptr;
+  // adjoint
+  void* adj[2] = {nullptr, nullptr};
+  int a = 0;
+  bool seeded = false;
+  const void* seed_bytes = nullptr;
+  // timing events
+  size_t next_ev = 0;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> stall_pairs;
+
+  Run(ackpt_engine* e, bool d, cudaStream_t str) : E(e), dry(d), s(str) {
+    if (!dry) {
+      refs.assign(E->bufs.size(), 0);
+      for (int i = int(E->bufs.size()) - 1; i >= 0; --i) free_list.push_back(i);
+    }
+  }
+
+  // -- buffers --------------------------------------------------------------
+  int acquire() {
+    if (free_list.empty()) {
+      if (!dry) fail(ACKPT_EXECUTION_ERROR, "HBM buffer pool exhausted (plan/dry-run mismatch)");
+      refs.push_back(0);
+      free_list.push_back(int(refs.size()) - 1);
+    }
+    int id = free_list.back();
+    free_list.pop_back();
+    refs[size_t(id)] = 1;
+    peak_in_use = std::max(peak_in_use, ++in_use);
+    return id;
+  }
+  void retain(int id) {
+    if (id >= 0) ++refs[size_t(id)];
+  }
+  void release(int id) {
+    if (id < 0) return;
+    if (--refs[size_t(id)] == 0) {
+      free_list.push_back(id);
+      --in_use;
+    }
+  }
+  const void* ptr(int id) const { return id == kExt ? ext : E->bufs[size_t(id)]; }
+  void* wptr(int id) const { return E->bufs[size_t(id)]; }
+
+  cudaEvent_t timing_event() {
+    if (dry) {
+      ++next_ev;
+      return nullptr;
+    }
+    if (next_ev >= E->timing.size()) fail(ACKPT_EXECUTION_ERROR, "timing-event pool exhausted");
+    return E->timing[next_ev++];
+  }
+
+  // -- operator calls (runtime.py:174-190) ------------------------------------
+  void do_seed(int state) {
+    // Seed the adjoint register so that after all n backward steps the result
+    // lands in adj[0] (the caller's output buffer).
+    a = (E->n % 2 == 0) ? 0 : 1;
+    if (!dry) {
+      if (seed_bytes) {
+        ACKPT_CUDA_CHECK(cudaMemcpyAsync(adj[a], seed_bytes, size_t(E->S), cudaMemcpyDeviceToDevice, s));
+      } else {
+        if (!E->op.seed) fail(ACKPT_EXECUTION_ERROR, "no adjoint seed: operator has no seed function");
+        check_op(E->op.seed(E->op.ctx, ptr(state), adj[a], s));
+        ++st.kernel_launches;
+      }
+    }
+    seeded = true;
+  }
+
+  int forward(int64_t step, int cur) {
+    int out = acquire();
+    if (!dry) {
+      check_op(E->op.forward(E->op.ctx, step, ptr(cur), wptr(out), s));
+      ++st.kernel_launches;
+    }
+    release(cur);
+    ++st.forward_evals;
+    if (step + 1 == E->n && !seeded) do_seed(out);
+    return out;
+  }
+
+  int advance(int64_t from, int64_t to, int cur) {
+    // Advance(from, to): per-step contract by default; one fused launch when
+    // the operator provides advance() and fusion is enabled.
+    if (to - from >= 2 && E->fuse && E->op.advance) {
+      int out = acquire();
+      if (!dry) {
+        check_op(E->op.advance(E->op.ctx, from, to, ptr(cur), wptr(out), s));
+        ++st.kernel_launches;
+      }
+      release(cur);
+      st.forward_evals += to - from;
+      ++st.fused_advances;
+      if (to == E->n && !seeded) do_seed(out);
+      return out;
+    }
+    for (int64_t k = from; k < to; ++k) cur = forward(k, cur);
+    return cur;
+  }
+
+  void backward(int64_t step, int state) {
+    if (!seeded)
+      fail(ACKPT_EXECUTION_ERROR, "Reverse " + std::to_string(step) + " before the adjoint was seeded");
+    if (!dry) {
+      check_op(E->op.backward(E->op.ctx, step, ptr(state), adj[a], adj[1 - a], s));
+      ++st.kernel_launches;
+    }
+    a = 1 - a;
+    ++st.backward_evals;
+  }
+
+  // -- transfers ------------------------------------------------------------
+  void wait_transfer(ackpt_ticket t) {
+    // runtime.py:192-199.  Errors captured by the transfer surface here.
+    if (dry) {
+      next_ev += 2;
+      return;
+    }
+    std::string msg;
+    int rc = tier_ticket_status(E->tier, t, &msg);
+    if (rc != ACKPT_OK) fail(rc, msg);
+    cudaEvent_t done = tier_ticket_event(E->tier, t);
+    cudaEvent_t before = timing_event(), after = timing_event();
+    ACKPT_CUDA_CHECK(cudaEventRecord(before, s));
+    if (done) ACKPT_CUDA_CHECK(cudaStreamWaitEvent(s, done, 0));
+    ACKPT_CUDA_CHECK(cudaEventRecord(after, s));
+    stall_pairs.emplace_back(before, after);
+  }
+
+  ackpt_ticket begin_store(int64_t key, int state) {
+    ackpt_ticket t = -1;
+    if (!dry) check_op(ackpt_tier_begin_store(E->tier, key, key, ptr(state), E->S, s, &t));
+    ++st.stores_issued;
+    st.link_bytes += E->S;
+    return t;
+  }
+
+  ackpt_ticket begin_fetch(int64_t key, int dst) {
+    ackpt_ticket t = -1;
+    if (!dry) {
+      int rc = ackpt_tier_begin_fetch(E->tier, key, wptr(dst), E->S, s, &t);
+      if (rc != ACKPT_OK) fail(rc, ackpt_last_error());
+    }
+    ++st.prefetches_issued;
+    st.link_bytes += E->S;
+    return t;
+  }
+
+  // -- interpreter (runtime.py:201-252) ---------------------------------------
+  int run_schedule(const SegPlan& plan, int64_t offset, int state) {
+    const int64_t cap = E->slots;
+    std::vector<int> slot_buf(size_t(std::max<int64_t>(cap, 0)), -2);
+    std::vector<int64_t> slot_step(slot_buf.size(), 0);
+    std::vector<int64_t> write_idx(slot_buf.size(), -1);
+    int64_t occupied = 0;
+    std::vector<std::pair<int64_t, int>> tape;
+    int64_t current = 0;
+    auto free_slot = [&](int64_t slot) {
+      if (slot_buf[size_t(slot)] != -2) {
+        release(slot_buf[size_t(slot)]);
+        slot_buf[size_t(slot)] = -2;
+        --occupied;
+      }
+    };
+    const auto& acts = plan.actions;
+    for (size_t idx = 0; idx < acts.size(); ++idx) {
+      const Action& act = acts[idx];
+      if (act.op == ACKPT_ADVANCE || act.op == ACKPT_TAPE) {
+        if (act.a != current)
+          fail(ACKPT_EXECUTION_ERROR, "action " + std::to_string(idx) + " starts at " +
+                                          std::to_string(act.a) + ", state is at " +
+                                          std::to_string(current));
+        if (act.op == ACKPT_TAPE) {
+          for (int64_t rel = act.a; rel < act.b; ++rel) {
+            retain(state);
+            tape.emplace_back(rel, state);  // the INPUT state of step rel
+            ledger.add_tape(E->S);
+            state = forward(offset + rel, state);
+          }
+        } else if (act.b > act.a) {
+          state = advance(offset + act.a, offset + act.b, state);
+        }
+        current = act.b;
+      } else if (act.op == ACKPT_SAVE) {
+        if (act.b < 0 || act.b >= cap)
+          fail(ACKPT_SLOT_OUT_OF_RANGE,
+               "slot " + std::to_string(act.b) + " outside capacity " + std::to_string(cap));
+        free_slot(act.b);
+        retain(state);
+        slot_buf[size_t(act.b)] = state;
+        slot_step[size_t(act.b)] = offset + current;
+        ++occupied;
+        write_idx[size_t(act.b)] = int64_t(idx);
+        ledger.set_slots(occupied * E->S);
+      } else if (act.op == ACKPT_LOAD) {
+        if (act.a < 0 || act.a >= cap)
+          fail(ACKPT_SLOT_OUT_OF_RANGE,
+               "slot " + std::to_string(act.a) + " outside capacity " + std::to_string(cap));
+        int held = slot_buf[size_t(act.a)];
+        if (held == -2) fail(ACKPT_SLOT_UNWRITTEN, "slot " + std::to_string(act.a) + " read before write");
+        retain(held);
+        release(state);
+        state = held;
+        current = slot_step[size_t(act.a)] - offset;
+        const int64_t w = write_idx[size_t(act.a)];
+        if (w >= 0 && plan.last_read[size_t(w)] == int64_t(idx)) {  // final read: free
+          free_slot(act.a);
+          ledger.set_slots(occupied * E->S);
+        }
+      } else if (act.op == ACKPT_REVERSE) {
+        if (tape.empty() || tape.back().first != act.a)
+          fail(ACKPT_EXECUTION_ERROR, "Reverse " + std::to_string(act.a) + " without taped state");
+        int taped = tape.back().second;
+        tape.pop_back();
+        ledger.drop_tape(E->S);
+        backward(offset + act.a, taped);
+        release(taped);
+      } else if (act.op == ACKPT_DONE) {
+        break;
+      } else {
+        fail(ACKPT_EXECUTION_ERROR, "unknown action op " + std::to_string(act.op));
+      }
+    }
+    for (int64_t sl = 0; sl < cap; ++sl) free_slot(sl);  // pool.clear()
+    for (auto& te : tape) release(te.second);
+    ledger.set_slots(0);
+    return state;
+  }
+
+  // -- multistage (runtime.py:269-322) ----------------------------------------
+  int multistage_forward(int state) {
+    const auto& bs = E->boundaries;
+    ackpt_ticket ticket = -1;
+    int store_src = -2;
+    bool have = false;
+    for (size_t idx = 0; idx < bs.size(); ++idx) {
+      const int64_t b = bs[idx];
+      if (have) {
+        wait_transfer(ticket);
+        ledger.drop_transfer(E->S);
+        release(store_src);
+      }
+      ticket = begin_store(b, state);
+      retain(state);
+      store_src = state;
+      have = true;
+      ledger.add_transfer(E->S);
+      const int64_t end = idx + 1 < bs.size() ? bs[idx + 1] : E->n;
+      state = advance(b, end, state);
+    }
+    if (have) {
+      wait_transfer(ticket);
+      ledger.drop_transfer(E->S);
+      release(store_src);
+    }
+    return state;
+  }
+
+  void multistage_backward() {
+    const bool pf = E->prefetch < 0 ? env_prefetch() : E->prefetch != 0;
+    const auto& bs = E->boundaries;
+    const size_t nseg = bs.size();
+    std::map<int64_t, std::pair<ackpt_ticket, int>> tickets;
+    auto issue = [&](int64_t key) {
+      int dst = acquire();
+      tickets[key] = {begin_fetch(key, dst), dst};
+      ledger.add_transfer(E->S);
+    };
+    if (pf) issue(bs[nseg - 1]);
+    for (size_t jj = nseg; jj-- > 0;) {
+      const int64_t start = bs[jj];
+      const int64_t end = jj + 1 < nseg ? bs[jj + 1] : E->n;
+      if (!pf) issue(start);
+      auto it = tickets.find(start);
+      auto tk = it->second;
+      tickets.erase(it);
+      wait_transfer(tk.first);
+      if (pf && jj > 0) issue(bs[jj - 1]);
+      ledger.drop_transfer(E->S);  // fetched bytes go live
+      const SegPlan& plan = E->seg_by_len.at(end - start);
+      int last = run_schedule(plan, start, tk.second);
+      release(last);
+    }
+  }
+
+  void finish_stats() {
+    st.peak_l1_bytes = ledger.peak;
+    st.interval = E->strategy == ACKPT_MULTISTAGE ? E->interval : 0;
+    st.fallback = E->fallback ? 1 : 0;
+    st.device_buffers = int64_t(E->bufs.size());
+  }
+};
+
+void alloc_pool(ackpt_engine* E, int64_t need_bufs, size_t need_events) {
+  if (int64_t(E->bufs.size()) < need_bufs) {
+    const int64_t add = need_bufs - int64_t(E->bufs.size());
+    void* slab = nullptr;
+    cudaError_t e = cudaMalloc(&slab, size_t(add) * size_t(E->S));
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      fail(ACKPT_STORAGE_FULL, "HBM buffer pool of " + std::to_string(need_bufs) + " x " +
+                                   std::to_string(E->S) + " B: " + cudaGetErrorString(e));
+    }
+    E->slabs.push_back(slab);
+    for (int64_t i = 0; i < add; ++i)
+      E->bufs.push_back(static_cast<char*>(slab) + size_t(i) * size_t(E->S));
+  }
+  if (!E->adj_internal) ACKPT_CUDA_CHECK(cudaMalloc(&E->adj_internal, size_t(E->S)));
+  while (E->timing.size() < need_events) {
+    cudaEvent_t ev;
+    ACKPT_CUDA_CHECK(cudaEventCreate(&ev));
+    E->timing.push_back(ev);
+  }
+}
+
+SegPlan make_plan(std::vector<Action>&& acts) {
+  SegPlan p;
+  p.actions = std::move(acts);
+  slot_read_liveness(p.actions, p.last_read);
+  return p;
+}
+
+enum class Mode { kFull, kForwardSweep, kBackwardSweep };
+
+void run_impl(ackpt_engine* E, Mode mode, const void* initial_state, const void* seed,
+              void* adjoint_out, void* final_state, ackpt_stats* stats, cudaStream_t caller) {
+  if (!E->prepared) fail(ACKPT_VALUE_ERROR, "engine not prepared");
+  const bool ms = E->strategy == ACKPT_MULTISTAGE && !E->fallback;
+  if (mode != Mode::kFull && !ms)
+    fail(ACKPT_VALUE_ERROR, "fallback plans have no Level-2 phase; use execute()");  // runtime.py:395-396
+  if (mode == Mode::kFull && !adjoint_out) fail(ACKPT_VALUE_ERROR, "adjoint_out is required");
+  if (mode == Mode::kBackwardSweep && !seed) fail(ACKPT_VALUE_ERROR, "seed is required");
+
+  Run r(E, false, E->compute);
+  r.ext = initial_state;
+  r.seed_bytes = seed;
+  r.adj[0] = adjoint_out;
+  r.adj[1] = E->adj_internal;
+  if (mode == Mode::kForwardSweep) {
+    r.adj[0] = E->adj_internal;  // seed computed at step n is discarded
+    r.adj[1] = E->adj_internal;
+  }
+
+  // Order after the caller's stream, then time on the engine's stream.
+  ACKPT_CUDA_CHECK(cudaEventRecord(E->ev_sync, caller));
+  ACKPT_CUDA_CHECK(cudaStreamWaitEvent(E->compute, E->ev_sync, 0));
+  const auto t0 = std::chrono::steady_clock::now();
+  ACKPT_CUDA_CHECK(cudaEventRecord(E->ev_start, E->compute));
+
+  if (mode == Mode::kFull) {
+    if (ms) {
+      int last = r.multistage_forward(kExt);
+      r.release(last);
+      r.multistage_backward();
+    } else {
+      int last = r.run_schedule(E->plain, 0, kExt);
+      r.release(last);
+    }
+  } else if (mode == Mode::kForwardSweep) {
+    r.seeded = true;  // the caller derives the seed from the final state
+    int last = r.multistage_forward(kExt);
+    if (final_state)
+      ACKPT_CUDA_CHECK(cudaMemcpyAsync(final_state, r.ptr(last), size_t(E->S),
+                                       cudaMemcpyDeviceToDevice, E->compute));
+    r.release(last);
+  } else {
+    r.a = (E->n % 2 == 0) ? 0 : 1;
+    ACKPT_CUDA_CHECK(cudaMemcpyAsync(r.adj[r.a], seed, size_t(E->S), cudaMemcpyDeviceToDevice,
+                                     E->compute));
+    r.seeded = true;
+    r.multistage_backward();
+  }
+
+  ACKPT_CUDA_CHECK(cudaEventRecord(E->ev_end, E->compute));
+  ACKPT_CUDA_CHECK(cudaEventSynchronize(E->ev_end));
+  const auto t1 = std::chrono::steady_clock::now();
+  ACKPT_CUDA_CHECK(cudaStreamWaitEvent(caller, E->ev_end, 0));
+  if (mode == Mode::kFull && !r.seeded)
+    fail(ACKPT_EXECUTION_ERROR, "execution finished without producing an adjoint");  // runtime.py:379-380
+
+  r.finish_stats();
+  r.st.wall_seconds = std::chrono::duration<double>(t1 - t0).count();
+  float ms_gpu = 0.f;
+  ACKPT_CUDA_CHECK(cudaEventElapsedTime(&ms_gpu, E->ev_start, E->ev_end));
+  r.st.gpu_seconds = double(ms_gpu) * 1e-3;
+  double stall = 0.0;
+  for (auto& pr : r.stall_pairs) {
+    float msv = 0.f;
+    ACKPT_CUDA_CHECK(cudaEventElapsedTime(&msv, pr.first, pr.second));
+    stall += std::max(0.0, double(msv) * 1e-3);
+  }
+  r.st.stall_seconds = stall;
+  if (stats) *stats = r.st;
+}
+
+// A failed run may leave kernels queued that read caller buffers: drain the
+// engine's stream before reporting the error.
+template <class F>
+void run_guarded(ackpt_engine* E, F&& fn) {
+  try {
+    fn();
+  } catch (...) {
+    cudaStreamSynchronize(E->compute);
+    throw;
+  }
+}
+
+}  // namespace
+}  // namespace ackpt
+
+extern "C" {
+
+ACKPT_API int ackpt_engine_create(const ackpt_operator* op, ackpt_engine** out) {
+  return ackpt::guard([&] {
+    if (!op || !op->forward || !op->backward) ackpt::fail(ACKPT_VALUE_ERROR, "operator needs forward and backward");
+    if (op->n_steps < 1) ackpt::fail(ACKPT_VALUE_ERROR, "n_steps must be >= 1");  // runtime.py:79-80
+    if (op->state_bytes <= 0) ackpt::fail(ACKPT_VALUE_ERROR, "state_size must be positive");
+    std::unique_ptr<ackpt_engine> e(new ackpt_engine());
+    e->op = *op;
+    e->S = op->state_bytes;
+    e->n = op->n_steps;
+    ACKPT_CUDA_CHECK(cudaStreamCreateWithFlags(&e->compute, cudaStreamNonBlocking));
+    ACKPT_CUDA_CHECK(cudaEventCreate(&e->ev_start));
+    ACKPT_CUDA_CHECK(cudaEventCreate(&e->ev_end));
+    ACKPT_CUDA_CHECK(cudaEventCreateWithFlags(&e->ev_sync, cudaEventDisableTiming));
+    *out = e.release();
+  });
+}
+
+ACKPT_API int ackpt_engine_destroy(ackpt_engine* e) {
+  return ackpt::guard([&] {
+    if (!e) return;
+    if (e->compute) cudaStreamSynchronize(e->compute);
+    for (auto s : e->slabs) cudaFree(s);
+    if (e->adj_internal) cudaFree(e->adj_internal);
+    for (auto ev : e->timing) cudaEventDestroy(ev);
+    if (e->ev_start) cudaEventDestroy(e->ev_start);
+    if (e->ev_end) cudaEventDestroy(e->ev_end);
+    if (e->ev_sync) cudaEventDestroy(e->ev_sync);
+    if (e->compute) cudaStreamDestroy(e->compute);
+    delete e;
+  });
+}
+
+ACKPT_API int ackpt_engine_prepare(ackpt_engine* E, int32_t strategy, int64_t slots,
+                                   int64_t interval, ackpt_tier* tier) {
+  return ackpt::guard([&] {
+    using namespace ackpt;
+    E->prepared = false;
+    E->strategy = strategy;
+    E->slots = slots;
+    E->interval = 0;
+    E->fallback = false;
+    E->tier = tier;
+    E->boundaries.clear();
+    E->seg_by_len.clear();
+    E->plain = SegPlan{};
+    const int64_t n = E->n;
+    std::vector<Action> acts;
+    if (strategy == ACKPT_FULL_STORAGE) {
+      taped_actions(n, acts);  // runtime.py:364-365
+      E->slots = 0;
+      E->plain = make_plan(std::move(acts));
+    } else if (strategy == ACKPT_REVOLVE) {
+      revolve_actions(n, slots, acts);  // runtime.py:366-368
+      E->plain = make_plan(std::move(acts));
+    } else if (strategy == ACKPT_MULTISTAGE) {
+      // plan_multistage (schedule.py:288-329)
+      if (!tier) fail(ACKPT_VALUE_ERROR, "Multistage requires a Level-2 backend");
+      if (interval < 1) fail(ACKPT_VALUE_ERROR, "interval must be >= 1, got " + std::to_string(interval));
+      if (tier_slot_bytes(tier) < E->S) fail(ACKPT_SIZE_MISMATCH, "tier slots are smaller than the state");
+      E->interval = interval;
+      if (interval >= n) {
+        E->fallback = true;
+        revolve_actions(n, slots, acts);
+        E->plain = make_plan(std::move(acts));
+      } else {
+        for (int64_t b = 0; b < n; b += interval) E->boundaries.push_back(b);
+        for (int64_t b : E->boundaries) {
+          const int64_t len = std::min(b + interval, n) - b;
+          if (E->seg_by_len.count(len)) continue;
+          std::vector<Action> seg;
+          if (len <= slots + 1) taped_actions(len, seg);
+          else revolve_actions(len, slots, seg);
+          E->seg_by_len[len] = make_plan(std::move(seg));
+        }
+        tier_reserve_keys(tier, E->boundaries);
+      }
+    } else {
+      fail(ACKPT_VALUE_ERROR, "unknown strategy " + std::to_string(strategy));
+    }
+    // Dry run: sizes the HBM pool and the timing-event pool exactly.
+    Run r(E, true, nullptr);
+    r.adj[0] = r.adj[1] = nullptr;
+    if (E->strategy == ACKPT_MULTISTAGE && !E->fallback) {
+      int last = r.multistage_forward(kExt);
+      r.release(last);
+      r.multistage_backward();
+      // the backward sweep alone needs the same pool; the forward sweep less
+    } else {
+      int last = r.run_schedule(E->plain, 0, kExt);
+      r.release(last);
+    }
+    alloc_pool(E, r.peak_in_use + 1, r.next_ev);
+    E->prepared = true;
+  });
+}
+
+ACKPT_API int ackpt_engine_set_fusion(ackpt_engine* e, int32_t fuse_advance) {
+  e->fuse = fuse_advance;
+  return ACKPT_OK;
+}
+
+ACKPT_API int ackpt_engine_set_prefetch(ackpt_engine* e, int32_t prefetch) {
+  e->prefetch = prefetch;
+  return ACKPT_OK;
+}
+
+ACKPT_API int ackpt_engine_run(ackpt_engine* e, const void* initial_state, const void* seed,
+                               void* adjoint_out, ackpt_stats* stats, void* stream) {
+  return ackpt::guard([&] {
+    ackpt::run_guarded(e, [&] {
+      ackpt::run_impl(e, ackpt::Mode::kFull, initial_state, seed, adjoint_out, nullptr, stats,
+                      static_cast<cudaStream_t>(stream));
+    });
+  });
+}
+
+ACKPT_API int ackpt_engine_forward_sweep(ackpt_engine* e, const void* initial_state,
+                                         void* final_state, ackpt_stats* stats, void* stream) {
+  return ackpt::guard([&] {
+    ackpt::run_guarded(e, [&] {
+      ackpt::run_impl(e, ackpt::Mode::kForwardSweep, initial_state, nullptr, nullptr, final_state,
+                      stats, static_cast<cudaStream_t>(stream));
+    });
+  });
+}
+
+ACKPT_API int ackpt_engine_backward_sweep(ackpt_engine* e, const void* seed, void* adjoint_out,
+                                          ackpt_stats* stats, void* stream) {
+  return ackpt::guard([&] {
+    ackpt::run_guarded(e, [&] {
+      ackpt::run_impl(e, ackpt::Mode::kBackwardSweep, nullptr, seed, adjoint_out, nullptr, stats,
+                      static_cast<cudaStream_t>(stream));
+    });
+  });
+}
+
+ACKPT_API int ackpt_engine_calibrate(ackpt_engine* E, ackpt_tier* tier, int64_t trials,
+                                     const void* initial_state, double* t_a, double* t_b,
+                                     double* t_t) {
+  return ackpt::guard([&] {
+    using namespace ackpt;
+    if (trials < 3) fail(ACKPT_VALUE_ERROR, "trial_steps must be >= 3, got " + std::to_string(trials));
+    if (!tier) fail(ACKPT_VALUE_ERROR, "calibrate requires a Level-2 backend");
+    cudaStream_t s = E->compute;
+    const size_t S = size_t(E->S);
+    // trials + 2 states, 2 adjoints
+    std::vector<void*> st(size_t(trials) + 2, nullptr);
+    void* adj[2] = {nullptr, nullptr};
+    auto cleanup = [&] {
+      for (void* p : st)
+        if (p) cudaFree(p);
+      for (void* p : adj)
+        if (p) cudaFree(p);
+    };
+    std::vector<cudaEvent_t> evs(size_t(6 * trials));
+    for (auto& ev : evs) ACKPT_CUDA_CHECK(cudaEventCreate(&ev));
+    try {
+      for (auto& p : st) ACKPT_CUDA_CHECK(cudaMalloc(&p, S));
+      for (auto& p : adj) ACKPT_CUDA_CHECK(cudaMalloc(&p, S));
+      ACKPT_CUDA_CHECK(cudaMemcpyAsync(st[0], initial_state, S, cudaMemcpyDeviceToDevice, s));
+      // warm-up forward (runtime.py:438)
+      check_op(E->op.forward(E->op.ctx, 0, st[0], st[1], s));
+      // trial forwards: states[i] is the input of trial i (runtime.py:440-446)
+      std::vector<int64_t> steps(static_cast<size_t>(trials));
+      for (int64_t i = 0; i < trials; ++i) {
+        steps[size_t(i)] = i % E->n;
+        ACKPT_CUDA_CHECK(cudaEventRecord(evs[size_t(2 * i)], s));
+        check_op(E->op.forward(E->op.ctx, steps[size_t(i)], st[size_t(i) + 1], st[size_t(i) + 2], s));
+        ACKPT_CUDA_CHECK(cudaEventRecord(evs[size_t(2 * i + 1)], s));
+      }
+      // seed from the last state, then trial backwards in reverse (runtime.py:448-453)
+      void* fin = st[size_t(trials) + 1];
+      if (E->op.seed) check_op(E->op.seed(E->op.ctx, fin, adj[0], s));
+      else ACKPT_CUDA_CHECK(cudaMemsetAsync(adj[0], 0, S, s));
+      int ai = 0;
+      for (int64_t i = trials - 1, k = 0; i >= 0; --i, ++k) {
+        ACKPT_CUDA_CHECK(cudaEventRecord(evs[size_t(2 * trials + 2 * k)], s));
+        check_op(E->op.backward(E->op.ctx, steps[size_t(i)], st[size_t(i) + 1], adj[ai], adj[1 - ai], s));
+        ACKPT_CUDA_CHECK(cudaEventRecord(evs[size_t(2 * trials + 2 * k + 1)], s));
+        ai = 1 - ai;
+      }
+      // store round trips of the final state under keys 0..trials-1 (runtime.py:455-460)
+      ACKPT_CUDA_CHECK(cudaStreamSynchronize(s));
+      cudaStream_t d2h = tier_d2h(tier);
+      for (int64_t i = 0; i < trials; ++i) {
+        ACKPT_CUDA_CHECK(cudaEventRecord(evs[size_t(4 * trials + 2 * i)], d2h));
+        ackpt_ticket tk;
+        check_op(ackpt_tier_begin_store(tier, i, i, fin, E->S, nullptr, &tk));
+        ACKPT_CUDA_CHECK(cudaEventRecord(evs[size_t(4 * trials + 2 * i + 1)], d2h));
+        check_op(ackpt_tier_wait(tier, tk, nullptr));
+      }
+      ACKPT_CUDA_CHECK(cudaStreamSynchronize(d2h));
+      ACKPT_CUDA_CHECK(cudaStreamSynchronize(s));
+      auto median = [&](int64_t base) {
+        std::vector<double> v;
+        for (int64_t i = 0; i < trials; ++i) {
+          float msv = 0.f;
+          ACKPT_CUDA_CHECK(cudaEventElapsedTime(&msv, evs[size_t(base + 2 * i)], evs[size_t(base + 2 * i + 1)]));
+          v.push_back(double(msv) * 1e-3);
+        }
+        std::sort(v.begin(), v.end());
+        const size_t m = v.size();
+        return m % 2 ? v[m / 2] : 0.5 * (v[m / 2 - 1] + v[m / 2]);  // statistics.median
+      };
+      *t_a = median(0);
+      *t_b = median(2 * trials);
+      *t_t = median(4 * trials);
+    } catch (...) {
+      cleanup();
+      for (auto ev : evs) cudaEventDestroy(ev);
+      throw;
+    }
+    cleanup();
+    for (auto ev : evs) cudaEventDestroy(ev);
+  });
+}
+
+ACKPT_API int64_t ackpt_engine_interval(const ackpt_engine* e) { return e ? e->interval : 0; }
+
+}  // extern "C"

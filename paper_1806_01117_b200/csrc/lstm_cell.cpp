@@ -1,0 +1,231 @@
+// Device LSTM cell object and the ackpt_lstm_* C ABI (lstm.py:39-173).
+#include "lstm_cell.h"
+
+#include <algorithm>
+#include <cstring>
+#include <memory>
+#include <string>
+
+namespace ackpt {
+namespace {
+
+template <typename T>
+void round_into(const std::vector<double>& src, std::vector<unsigned char>& dst) {
+  dst.resize(src.size() * sizeof(T));
+  T* p = reinterpret_cast<T*>(dst.data());
+  for (size_t i = 0; i < src.size(); ++i) p[i] = T(src[i]);
+}
+
+void check_step(const ackpt_lstm* c, int64_t step) {
+  if (step < 0 || step >= c->n)
+    fail(ACKPT_VALUE_ERROR,
+         "step " + std::to_string(step) + " outside [0, " + std::to_string(c->n) + ")");
+}
+
+void check_launch() {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) fail(ACKPT_CUDA_ERROR, std::string("kernel launch: ") + cudaGetErrorString(e));
+}
+
+// fp32 pair kernels need an even batch and 8-byte aligned rows.
+bool f32_fast(const ackpt_lstm* c, std::initializer_list<const void*> ptrs) {
+  if (c->dtype != ACKPT_F32 || (c->d != 4 && c->d != 8) || (c->B & 1)) return false;
+  for (const void* p : ptrs)
+    if (reinterpret_cast<uintptr_t>(p) & 7u) return false;
+  return true;
+}
+
+}  // namespace
+
+int lstm_op_forward(void* ctx, int64_t step, const void* in, void* out, void* stream) {
+  return ackpt_lstm_forward(static_cast<ackpt_lstm*>(ctx), step, in, out, stream);
+}
+int lstm_op_backward(void* ctx, int64_t step, const void* st, const void* ai, void* ao,
+                     void* stream) {
+  return ackpt_lstm_backward(static_cast<ackpt_lstm*>(ctx), step, st, ai, ao, stream);
+}
+int lstm_op_seed(void* ctx, const void* fin, void* adj, void* stream) {
+  return ackpt_lstm_seed(static_cast<ackpt_lstm*>(ctx), fin, adj, stream);
+}
+int lstm_op_advance(void* ctx, int64_t from, int64_t to, const void* in, void* out, void* stream) {
+  return ackpt_lstm_advance(static_cast<ackpt_lstm*>(ctx), from, to, in, out, stream);
+}
+
+}  // namespace ackpt
+
+extern "C" {
+
+ACKPT_API int ackpt_lstm_create(int32_t d, int64_t n_steps, int64_t batch, int32_t dtype,
+                                const double* w_f, const double* w_i, const double* w_o,
+                                const double* w_c, const double* b_f, const double* b_i,
+                                const double* b_o, const double* b_c, const double* xs,
+                                const double* target, ackpt_lstm** out) {
+  return ackpt::guard([&] {
+    using ackpt::fail;
+    if (d < 1 || d > ackpt::kMaxD) fail(ACKPT_VALUE_ERROR, "hidden size must be in [1, 128]");
+    if (n_steps < 1) fail(ACKPT_VALUE_ERROR, "n_steps must be >= 1");
+    if (batch < 1) fail(ACKPT_VALUE_ERROR, "batch must be >= 1");
+    if (dtype != ACKPT_F32 && dtype != ACKPT_F64) fail(ACKPT_VALUE_ERROR, "dtype must be f32 or f64");
+    std::unique_ptr<ackpt_lstm> c(new ackpt_lstm());
+    c->d = d;
+    c->n = n_steps;
+    c->B = batch;
+    c->dtype = dtype;
+    c->esize = dtype == ACKPT_F32 ? 4 : 8;
+    const double* W[4] = {w_f, w_i, w_o, w_c};
+    const double* Bv[4] = {b_f, b_i, b_o, b_c};
+    const size_t D = size_t(d);
+    // W_h: the first d columns of each d x 2d gate matrix (z = [h; x], lstm.py:115)
+    c->wh64.resize(4 * D * D);
+    for (size_t g = 0; g < 4; ++g)
+      for (size_t j = 0; j < D; ++j)
+        for (size_t i = 0; i < D; ++i) c->wh64[(g * D + j) * D + i] = W[g][j * 2 * D + i];
+    // xb[k][g][j] = sum_i W_g[j][d + i] x_k[i] + b_g[j], in float64
+    c->xb64.resize(size_t(n_steps) * 4 * D);
+    for (int64_t k = 0; k < n_steps; ++k)
+      for (size_t g = 0; g < 4; ++g)
+        for (size_t j = 0; j < D; ++j) {
+          double acc = 0.0;
+          for (size_t i = 0; i < D; ++i) acc += W[g][j * 2 * D + D + i] * xs[size_t(k) * D + i];
+          c->xb64[(size_t(k) * 4 + g) * D + j] = acc + Bv[g][j];
+        }
+    c->target64.assign(target, target + D);
+    if (dtype == ACKPT_F32) {
+      ackpt::round_into<float>(c->wh64, c->wh_t);
+      ackpt::round_into<float>(c->xb64, c->xb_t);
+      ackpt::round_into<float>(c->target64, c->target_t);
+    } else {
+      ackpt::round_into<double>(c->wh64, c->wh_t);
+      ackpt::round_into<double>(c->xb64, c->xb_t);
+      ackpt::round_into<double>(c->target64, c->target_t);
+    }
+    ACKPT_CUDA_CHECK(cudaMalloc(&c->d_wh, c->wh_t.size()));
+    ACKPT_CUDA_CHECK(cudaMalloc(&c->d_xb, c->xb_t.size()));
+    ACKPT_CUDA_CHECK(cudaMemcpy(c->d_wh, c->wh_t.data(), c->wh_t.size(), cudaMemcpyHostToDevice));
+    ACKPT_CUDA_CHECK(cudaMemcpy(c->d_xb, c->xb_t.data(), c->xb_t.size(), cudaMemcpyHostToDevice));
+    *out = c.release();
+  });
+}
+
+ACKPT_API int ackpt_lstm_destroy(ackpt_lstm* cell) {
+  return ackpt::guard([&] {
+    if (!cell) return;
+    if (cell->d_wh) cudaFree(cell->d_wh);
+    if (cell->d_xb) cudaFree(cell->d_xb);
+    delete cell;
+  });
+}
+
+ACKPT_API int64_t ackpt_lstm_state_bytes(const ackpt_lstm* cell) {
+  return cell ? 2 * int64_t(cell->d) * cell->B * int64_t(cell->esize) : -1;
+}
+
+ACKPT_API int ackpt_lstm_forward(const ackpt_lstm* cell, int64_t step, const void* state_in,
+                                 void* state_out, void* stream) {
+  return ackpt::guard([&] {
+    ackpt::check_step(cell, step);
+    auto s = static_cast<cudaStream_t>(stream);
+    if (ackpt::f32_fast(cell, {state_in, state_out})) {
+      auto i = static_cast<const float*>(state_in);
+      auto o = static_cast<float*>(state_out);
+      if (cell->d == 8) ackpt::f32_forward<8>(cell, step, i, o, s);
+      else ackpt::f32_forward<4>(cell, step, i, o, s);
+    } else if (cell->dtype == ACKPT_F32) {
+      ackpt::generic_forward<float>(cell, step, static_cast<const float*>(state_in),
+                                    static_cast<float*>(state_out), s);
+    } else {
+      ackpt::generic_forward<double>(cell, step, static_cast<const double*>(state_in),
+                                     static_cast<double*>(state_out), s);
+    }
+    ackpt::check_launch();
+  });
+}
+
+ACKPT_API int ackpt_lstm_advance(const ackpt_lstm* cell, int64_t from_step, int64_t to_step,
+                                 const void* state_in, void* state_out, void* stream) {
+  return ackpt::guard([&] {
+    if (from_step < 0 || to_step > cell->n || from_step >= to_step)
+      ackpt::fail(ACKPT_VALUE_ERROR, "advance range out of bounds");
+    auto s = static_cast<cudaStream_t>(stream);
+    if (ackpt::f32_fast(cell, {state_in, state_out})) {
+      auto i = static_cast<const float*>(state_in);
+      auto o = static_cast<float*>(state_out);
+      if (cell->d == 8) ackpt::f32_advance<8>(cell, from_step, to_step, i, o, s);
+      else ackpt::f32_advance<4>(cell, from_step, to_step, i, o, s);
+    } else if (cell->dtype == ACKPT_F32) {
+      ackpt::generic_advance<float>(cell, from_step, to_step, static_cast<const float*>(state_in),
+                                    static_cast<float*>(state_out), s);
+    } else {
+      ackpt::generic_advance<double>(cell, from_step, to_step,
+                                     static_cast<const double*>(state_in),
+                                     static_cast<double*>(state_out), s);
+    }
+    ackpt::check_launch();
+  });
+}
+
+ACKPT_API int ackpt_lstm_backward(const ackpt_lstm* cell, int64_t step, const void* state,
+                                  const void* adjoint_in, void* adjoint_out, void* stream) {
+  return ackpt::guard([&] {
+    ackpt::check_step(cell, step);
+    auto s = static_cast<cudaStream_t>(stream);
+    if (ackpt::f32_fast(cell, {state, adjoint_in, adjoint_out})) {
+      auto x = static_cast<const float*>(state);
+      auto a = static_cast<const float*>(adjoint_in);
+      auto o = static_cast<float*>(adjoint_out);
+      if (cell->d == 8) ackpt::f32_backward<8>(cell, step, x, a, o, s);
+      else ackpt::f32_backward<4>(cell, step, x, a, o, s);
+    } else if (cell->dtype == ACKPT_F32) {
+      ackpt::generic_backward<float>(cell, step, static_cast<const float*>(state),
+                                     static_cast<const float*>(adjoint_in),
+                                     static_cast<float*>(adjoint_out), s);
+    } else {
+      ackpt::generic_backward<double>(cell, step, static_cast<const double*>(state),
+                                      static_cast<const double*>(adjoint_in),
+                                      static_cast<double*>(adjoint_out), s);
+    }
+    ackpt::check_launch();
+  });
+}
+
+ACKPT_API int ackpt_lstm_seed(const ackpt_lstm* cell, const void* final_state, void* adjoint_out,
+                              void* stream) {
+  return ackpt::guard([&] {
+    auto s = static_cast<cudaStream_t>(stream);
+    if (cell->dtype == ACKPT_F32)
+      ackpt::launch_seed<float>(cell, static_cast<const float*>(final_state),
+                                static_cast<float*>(adjoint_out), s);
+    else
+      ackpt::launch_seed<double>(cell, static_cast<const double*>(final_state),
+                                 static_cast<double*>(adjoint_out), s);
+    ackpt::check_launch();
+  });
+}
+
+ACKPT_API int ackpt_lstm_loss(const ackpt_lstm* cell, const void* final_state, void* loss_out,
+                              void* stream) {
+  return ackpt::guard([&] {
+    auto s = static_cast<cudaStream_t>(stream);
+    if (cell->dtype == ACKPT_F32)
+      ackpt::launch_loss<float>(cell, static_cast<const float*>(final_state),
+                                static_cast<float*>(loss_out), s);
+    else
+      ackpt::launch_loss<double>(cell, static_cast<const double*>(final_state),
+                                 static_cast<double*>(loss_out), s);
+    ackpt::check_launch();
+  });
+}
+
+ACKPT_API int ackpt_lstm_operator(ackpt_lstm* cell, ackpt_operator* out) {
+  return ackpt::guard([&] {
+    out->ctx = cell;
+    out->forward = ackpt::lstm_op_forward;
+    out->backward = ackpt::lstm_op_backward;
+    out->seed = ackpt::lstm_op_seed;
+    out->advance = ackpt::lstm_op_advance;
+    out->state_bytes = ackpt_lstm_state_bytes(cell);
+    out->n_steps = cell->n;
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,68 @@
+// Device-resident LSTM cell (lstm.py:39-69 LstmCell, batched) and the kernel
+// launch entry points shared by the kernel translation units.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <vector>
+
+#include "common.h"
+
+struct ackpt_lstm {
+  int d = 0;
+  int64_t n = 0, B = 0;
+  int dtype = ACKPT_F32;
+  size_t esize = 4;
+  std::vector<double> wh64, xb64, target64;         // float64 master copies
+  std::vector<unsigned char> wh_t, xb_t, target_t;  // rounded to the cell dtype
+  void* d_wh = nullptr;                             // 4 x d x d, dtype
+  void* d_xb = nullptr;                             // n x 4 x d, dtype
+};
+
+namespace ackpt {
+
+// Parameter block of the fast step kernels (lives in the constant bank).
+template <typename T, int D>
+struct StepParams {
+  T wh[4][D][D];  // gate g (f, i, o, c), row j, column i over h
+  T xb[4][D];     // W_x x_k + b of this step
+};
+
+template <typename T>
+struct TargetParams {
+  T target[128];
+};
+
+constexpr int kMaxD = 128;
+
+// fp32 fast path, d in {4, 8}: float2-paired kernels (lstm_f32_d*.cu).
+template <int D>
+void f32_forward(const ackpt_lstm* c, int64_t step, const float* in, float* out, cudaStream_t s);
+template <int D>
+void f32_backward(const ackpt_lstm* c, int64_t step, const float* st, const float* ai, float* ao,
+                  cudaStream_t s);
+template <int D>
+void f32_advance(const ackpt_lstm* c, int64_t from, int64_t to, const float* in, float* out,
+                 cudaStream_t s);
+
+// Generic path, any d <= 128, f32 or f64 (lstm_generic.cu).
+template <typename T>
+void generic_forward(const ackpt_lstm* c, int64_t step, const T* in, T* out, cudaStream_t s);
+template <typename T>
+void generic_backward(const ackpt_lstm* c, int64_t step, const T* st, const T* ai, T* ao,
+                      cudaStream_t s);
+template <typename T>
+void generic_advance(const ackpt_lstm* c, int64_t from, int64_t to, const T* in, T* out,
+                     cudaStream_t s);
+template <typename T>
+void launch_seed(const ackpt_lstm* c, const T* st, T* adj, cudaStream_t s);
+template <typename T>
+void launch_loss(const ackpt_lstm* c, const T* st, T* loss, cudaStream_t s);
+
+inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+inline unsigned blocks_for(int64_t items, int threads) {
+  return unsigned((items + threads - 1) / threads);
+}
+
+}  // namespace ackpt

@@ -1,0 +1,403 @@
+// Level-2 tier: asynchronous HBM <-> pinned host DRAM checkpoint store.
+//
+// Replaces the reference's Level2Backend + TransferTicket (storage.py:181-278):
+// the FIFO queue and worker thread become two copy-engine streams (one D2H for
+// stores, one H2D for fetches) and each TransferTicket becomes a CUDA event.
+// The reference's FIFO guarantees ("a fetch enqueued after a store of the same
+// key always sees the stored bytes", storage.py:4-6) are kept per key: a
+// fetch waits for the key's last store event, and a store into a key waits
+// for the key's last fetch event before overwriting the host bytes.
+// Worker exceptions surfaced at wait() (storage.py:271-278) map to a ticket
+// status returned by ackpt_tier_wait (MissingKey, StorageFull, SizeMismatch).
+#include <cuda_runtime.h>
+
+#include <chrono>
+#include <deque>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <thread>
+#include <unordered_map>
+#include <vector>
+
+#include "common.h"
+
+namespace ackpt {
+
+struct TierTicket {
+  cudaEvent_t done = nullptr;
+  int kind = 0;  // 0 store, 1 fetch
+  int64_t key = 0;
+  int64_t step = 0;
+  int err = ACKPT_OK;
+  std::string msg;
+  bool complete = false;
+  double hold_seconds = 0.0;  // throttle: host-func sleep on the copy stream
+};
+
+struct KeyEntry {
+  int64_t slot = -1;
+  int64_t step = 0;
+  int64_t len = 0;
+  cudaEvent_t last_store = nullptr;
+  cudaEvent_t last_fetch = nullptr;
+  bool stored = false, fetched = false;
+};
+
+}  // namespace ackpt
+
+struct ackpt_tier {
+  int64_t capacity = 0;  // max keys (0 = bounded by host memory only)
+  int64_t slot_bytes = 0;
+  std::vector<unsigned char*> chunks;  // cudaHostAlloc'd
+  std::vector<unsigned char*> slot_ptr;
+  std::vector<int64_t> free_slots;
+  std::unordered_map<int64_t, ackpt::KeyEntry> keys;
+  std::deque<ackpt::TierTicket> tickets;
+  std::vector<cudaEvent_t> event_pool;
+  std::vector<cudaEvent_t> all_events;
+  cudaStream_t d2h = nullptr, h2d = nullptr;
+  cudaEvent_t after = nullptr;
+  double latency_s = 0.0, bandwidth = 0.0;
+  std::mutex mu;
+};
+
+namespace ackpt {
+namespace {
+
+cudaEvent_t new_event(ackpt_tier* t) {
+  if (!t->event_pool.empty()) {
+    cudaEvent_t e = t->event_pool.back();
+    t->event_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  ACKPT_CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  t->all_events.push_back(e);
+  return e;
+}
+
+void CUDART_CB hold_stream(void* arg) {
+  const double s = *static_cast<const double*>(arg);
+  if (s > 0) std::this_thread::sleep_for(std::chrono::duration<double>(s));
+}
+
+void reserve_slots(ackpt_tier* t, int64_t count) {
+  int64_t have = int64_t(t->slot_ptr.size());
+  if (count <= have) return;
+  if (t->capacity > 0 && count > t->capacity)
+    fail(ACKPT_STORAGE_FULL, "tier capacity " + std::to_string(t->capacity) + " keys exceeded");
+  const int64_t add = count - have;
+  unsigned char* chunk = nullptr;
+  cudaError_t e = cudaHostAlloc(reinterpret_cast<void**>(&chunk), size_t(add) * size_t(t->slot_bytes),
+                                cudaHostAllocDefault);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    fail(ACKPT_STORAGE_FULL, std::string("pinned host allocation failed: ") + cudaGetErrorString(e));
+  }
+  t->chunks.push_back(chunk);
+  for (int64_t i = 0; i < add; ++i) {
+    t->slot_ptr.push_back(chunk + size_t(i) * size_t(t->slot_bytes));
+    t->free_slots.push_back(have + i);
+  }
+}
+
+ackpt_ticket add_ticket(ackpt_tier* t, TierTicket&& tk) {
+  t->tickets.push_back(std::move(tk));
+  return ackpt_ticket(t->tickets.size() - 1);
+}
+
+TierTicket& get_ticket(ackpt_tier* t, ackpt_ticket id) {
+  if (id < 0 || size_t(id) >= t->tickets.size()) fail(ACKPT_VALUE_ERROR, "unknown transfer ticket");
+  return t->tickets[size_t(id)];
+}
+
+void hold(ackpt_tier* t, cudaStream_t s, TierTicket& tk, int64_t bytes) {
+  double secs = t->latency_s + (t->bandwidth > 0 ? double(bytes) / t->bandwidth : 0.0);
+  if (secs <= 0) return;
+  tk.hold_seconds = secs;
+  ACKPT_CUDA_CHECK(cudaLaunchHostFunc(s, hold_stream, &tk.hold_seconds));
+}
+
+void retire(ackpt_tier* t, TierTicket& tk) {
+  if (tk.complete) return;
+  tk.complete = true;
+  if (tk.done) {
+    t->event_pool.push_back(tk.done);
+    tk.done = nullptr;
+  }
+}
+
+}  // namespace
+
+// Engine-side helpers (engine.cpp).
+void tier_reserve_keys(ackpt_tier* t, const std::vector<int64_t>& keys) {
+  std::lock_guard<std::mutex> lk(t->mu);
+  int64_t absent = 0;
+  for (int64_t k : keys) {
+    auto it = t->keys.find(k);
+    if (it == t->keys.end() || it->second.slot < 0) ++absent;
+  }
+  const int64_t used = int64_t(t->slot_ptr.size() - t->free_slots.size());
+  reserve_slots(t, used + absent);
+}
+cudaEvent_t tier_ticket_event(ackpt_tier* t, ackpt_ticket id) {
+  std::lock_guard<std::mutex> lk(t->mu);
+  TierTicket& tk = get_ticket(t, id);
+  return tk.complete ? nullptr : tk.done;
+}
+int tier_ticket_status(ackpt_tier* t, ackpt_ticket id, std::string* msg) {
+  std::lock_guard<std::mutex> lk(t->mu);
+  TierTicket& tk = get_ticket(t, id);
+  if (msg) *msg = tk.msg;
+  return tk.err;
+}
+void tier_retire(ackpt_tier* t, ackpt_ticket id) {
+  std::lock_guard<std::mutex> lk(t->mu);
+  retire(t, get_ticket(t, id));
+}
+int64_t tier_slot_bytes(const ackpt_tier* t) { return t->slot_bytes; }
+cudaStream_t tier_d2h(const ackpt_tier* t) { return t->d2h; }
+double tier_throttle_seconds(const ackpt_tier* t, int64_t bytes) {
+  return t->latency_s + (t->bandwidth > 0 ? double(bytes) / t->bandwidth : 0.0);
+}
+
+}  // namespace ackpt
+
+extern "C" {
+
+ACKPT_API int ackpt_tier_create(int64_t capacity, int64_t slot_bytes, ackpt_tier** out) {
+  return ackpt::guard([&] {
+    if (slot_bytes <= 0) ackpt::fail(ACKPT_VALUE_ERROR, "slot_bytes must be positive");
+    if (capacity < 0) ackpt::fail(ACKPT_VALUE_ERROR, "capacity must be >= 0");
+    std::unique_ptr<ackpt_tier> t(new ackpt_tier());
+    t->capacity = capacity;
+    t->slot_bytes = slot_bytes;
+    int lo = 0, hi = 0;
+    ACKPT_CUDA_CHECK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    ACKPT_CUDA_CHECK(cudaStreamCreateWithPriority(&t->d2h, cudaStreamNonBlocking, hi));
+    ACKPT_CUDA_CHECK(cudaStreamCreateWithPriority(&t->h2d, cudaStreamNonBlocking, hi));
+    ACKPT_CUDA_CHECK(cudaEventCreateWithFlags(&t->after, cudaEventDisableTiming));
+    if (capacity > 0) ackpt::reserve_slots(t.get(), capacity);
+    *out = t.release();
+  });
+}
+
+ACKPT_API int ackpt_tier_destroy(ackpt_tier* t) {
+  return ackpt::guard([&] {
+    if (!t) return;
+    if (t->d2h) cudaStreamSynchronize(t->d2h);
+    if (t->h2d) cudaStreamSynchronize(t->h2d);
+    for (auto e : t->all_events) cudaEventDestroy(e);
+    for (auto& kv : t->keys) {
+      if (kv.second.last_store) cudaEventDestroy(kv.second.last_store);
+      if (kv.second.last_fetch) cudaEventDestroy(kv.second.last_fetch);
+    }
+    if (t->after) cudaEventDestroy(t->after);
+    for (auto c : t->chunks) cudaFreeHost(c);
+    if (t->d2h) cudaStreamDestroy(t->d2h);
+    if (t->h2d) cudaStreamDestroy(t->h2d);
+    delete t;
+  });
+}
+
+ACKPT_API int ackpt_tier_set_throttle(ackpt_tier* t, double latency_s, double bandwidth) {
+  return ackpt::guard([&] {
+    if (latency_s < 0) ackpt::fail(ACKPT_VALUE_ERROR, "latency must be >= 0");
+    t->latency_s = latency_s;
+    t->bandwidth = bandwidth;
+  });
+}
+
+ACKPT_API int ackpt_tier_begin_store(ackpt_tier* t, int64_t key, int64_t step, const void* src,
+                                     int64_t bytes, void* after_stream, ackpt_ticket* out) {
+  return ackpt::guard([&] {
+    std::lock_guard<std::mutex> lk(t->mu);
+    if (step < 0) ackpt::fail(ACKPT_VALUE_ERROR, "step must be >= 0");
+    ackpt::TierTicket tk;
+    tk.kind = 0;
+    tk.key = key;
+    tk.step = step;
+    if (bytes < 0 || bytes > t->slot_bytes) {
+      tk.err = ACKPT_SIZE_MISMATCH;
+      tk.msg = "payload is " + std::to_string(bytes) + " bytes, tier slots hold " +
+               std::to_string(t->slot_bytes);
+      tk.complete = true;
+      *out = ackpt::add_ticket(t, std::move(tk));
+      return;
+    }
+    auto it = t->keys.find(key);
+    if (it == t->keys.end() || it->second.slot < 0) {
+      if (t->free_slots.empty()) {
+        try {
+          ackpt::reserve_slots(t, int64_t(t->slot_ptr.size()) + 1);
+        } catch (const ackpt::Error& e) {
+          tk.err = e.code;
+          tk.msg = e.what();
+          tk.complete = true;
+          *out = ackpt::add_ticket(t, std::move(tk));
+          return;
+        }
+      }
+      ackpt::KeyEntry& ke = t->keys[key];
+      ke.slot = t->free_slots.back();
+      t->free_slots.pop_back();
+      it = t->keys.find(key);
+    }
+    ackpt::KeyEntry& ke = it->second;
+    if (after_stream) {
+      ACKPT_CUDA_CHECK(cudaEventRecord(t->after, static_cast<cudaStream_t>(after_stream)));
+      ACKPT_CUDA_CHECK(cudaStreamWaitEvent(t->d2h, t->after, 0));
+    }
+    if (ke.fetched) ACKPT_CUDA_CHECK(cudaStreamWaitEvent(t->d2h, ke.last_fetch, 0));
+    if (bytes > 0)
+      ACKPT_CUDA_CHECK(cudaMemcpyAsync(t->slot_ptr[size_t(ke.slot)], src, size_t(bytes),
+                                       cudaMemcpyDeviceToHost, t->d2h));
+    ke.step = step;
+    ke.len = bytes;
+    ackpt_ticket id = ackpt::add_ticket(t, std::move(tk));
+    ackpt::TierTicket& ref = t->tickets[size_t(id)];
+    ackpt::hold(t, t->d2h, ref, bytes);
+    ref.done = ackpt::new_event(t);
+    ACKPT_CUDA_CHECK(cudaEventRecord(ref.done, t->d2h));
+    if (!ke.last_store) ACKPT_CUDA_CHECK(cudaEventCreateWithFlags(&ke.last_store, cudaEventDisableTiming));
+    ACKPT_CUDA_CHECK(cudaEventRecord(ke.last_store, t->d2h));
+    ke.stored = true;
+    *out = id;
+  });
+}
+
+ACKPT_API int ackpt_tier_begin_fetch(ackpt_tier* t, int64_t key, void* dst, int64_t bytes,
+                                     void* after_stream, ackpt_ticket* out) {
+  return ackpt::guard([&] {
+    std::lock_guard<std::mutex> lk(t->mu);
+    ackpt::TierTicket tk;
+    tk.kind = 1;
+    tk.key = key;
+    auto it = t->keys.find(key);
+    if (it == t->keys.end() || !it->second.stored) {
+      tk.err = ACKPT_MISSING_KEY;  // storage.py:310-311
+      tk.msg = "key " + std::to_string(key) + " never stored";
+      tk.complete = true;
+      *out = ackpt::add_ticket(t, std::move(tk));
+      return;
+    }
+    ackpt::KeyEntry& ke = it->second;
+    if (bytes >= 0 && bytes < ke.len) {
+      tk.err = ACKPT_SIZE_MISMATCH;
+      tk.msg = "destination holds " + std::to_string(bytes) + " bytes, key " +
+               std::to_string(key) + " holds " + std::to_string(ke.len);
+      tk.complete = true;
+      *out = ackpt::add_ticket(t, std::move(tk));
+      return;
+    }
+    tk.step = ke.step;
+    if (after_stream) {
+      ACKPT_CUDA_CHECK(cudaEventRecord(t->after, static_cast<cudaStream_t>(after_stream)));
+      ACKPT_CUDA_CHECK(cudaStreamWaitEvent(t->h2d, t->after, 0));
+    }
+    ACKPT_CUDA_CHECK(cudaStreamWaitEvent(t->h2d, ke.last_store, 0));
+    if (ke.len > 0)
+      ACKPT_CUDA_CHECK(cudaMemcpyAsync(dst, t->slot_ptr[size_t(ke.slot)], size_t(ke.len),
+                                       cudaMemcpyHostToDevice, t->h2d));
+    ackpt_ticket id = ackpt::add_ticket(t, std::move(tk));
+    ackpt::TierTicket& ref = t->tickets[size_t(id)];
+    ackpt::hold(t, t->h2d, ref, ke.len);
+    ref.done = ackpt::new_event(t);
+    ACKPT_CUDA_CHECK(cudaEventRecord(ref.done, t->h2d));
+    if (!ke.last_fetch) ACKPT_CUDA_CHECK(cudaEventCreateWithFlags(&ke.last_fetch, cudaEventDisableTiming));
+    ACKPT_CUDA_CHECK(cudaEventRecord(ke.last_fetch, t->h2d));
+    ke.fetched = true;
+    *out = id;
+  });
+}
+
+ACKPT_API int ackpt_tier_wait(ackpt_tier* t, ackpt_ticket ticket, int64_t* step_out) {
+  cudaEvent_t ev = nullptr;
+  int rc = ackpt::guard([&] {
+    std::lock_guard<std::mutex> lk(t->mu);
+    ackpt::TierTicket& tk = ackpt::get_ticket(t, ticket);
+    if (step_out) *step_out = tk.step;
+    if (tk.err != ACKPT_OK) ackpt::fail(tk.err, tk.msg);
+    ev = tk.complete ? nullptr : tk.done;
+  });
+  if (rc != ACKPT_OK || !ev) return rc;
+  // Block without holding the lock (other threads may issue transfers).
+  return ackpt::guard([&] {
+    ACKPT_CUDA_CHECK(cudaEventSynchronize(ev));
+    std::lock_guard<std::mutex> lk(t->mu);
+    ackpt::retire(t, ackpt::get_ticket(t, ticket));
+  });
+}
+
+ACKPT_API int ackpt_tier_stream_wait(ackpt_tier* t, ackpt_ticket ticket, void* stream) {
+  return ackpt::guard([&] {
+    std::lock_guard<std::mutex> lk(t->mu);
+    ackpt::TierTicket& tk = ackpt::get_ticket(t, ticket);
+    if (tk.err != ACKPT_OK) ackpt::fail(tk.err, tk.msg);
+    if (!tk.complete && tk.done)
+      ACKPT_CUDA_CHECK(cudaStreamWaitEvent(static_cast<cudaStream_t>(stream), tk.done, 0));
+  });
+}
+
+ACKPT_API int ackpt_tier_poll(ackpt_tier* t, ackpt_ticket ticket) {
+  int ready = ACKPT_OK;
+  int rc = ackpt::guard([&] {
+    std::lock_guard<std::mutex> lk(t->mu);
+    ackpt::TierTicket& tk = ackpt::get_ticket(t, ticket);
+    if (tk.complete) return;
+    cudaError_t e = cudaEventQuery(tk.done);
+    if (e == cudaErrorNotReady) {
+      ready = ACKPT_NOT_READY;
+      return;
+    }
+    ACKPT_CUDA_CHECK(e);
+    ackpt::retire(t, tk);
+  });
+  return rc != ACKPT_OK ? rc : ready;
+}
+
+ACKPT_API int ackpt_tier_contains(ackpt_tier* t, int64_t key, int32_t* out) {
+  return ackpt::guard([&] {
+    std::lock_guard<std::mutex> lk(t->mu);
+    auto it = t->keys.find(key);
+    *out = (it != t->keys.end() && it->second.stored) ? 1 : 0;
+  });
+}
+
+ACKPT_API int ackpt_tier_key_bytes(ackpt_tier* t, int64_t key, int64_t* out) {
+  return ackpt::guard([&] {
+    std::lock_guard<std::mutex> lk(t->mu);
+    auto it = t->keys.find(key);
+    if (it == t->keys.end() || !it->second.stored)
+      ackpt::fail(ACKPT_MISSING_KEY, "key " + std::to_string(key) + " never stored");
+    *out = it->second.len;
+  });
+}
+
+ACKPT_API int ackpt_tier_host_ptr(ackpt_tier* t, int64_t key, void** out) {
+  return ackpt::guard([&] {
+    std::lock_guard<std::mutex> lk(t->mu);
+    auto it = t->keys.find(key);
+    if (it == t->keys.end() || !it->second.stored)
+      ackpt::fail(ACKPT_MISSING_KEY, "key " + std::to_string(key) + " never stored");
+    *out = t->slot_ptr[size_t(it->second.slot)];
+  });
+}
+
+ACKPT_API int ackpt_tier_clear(ackpt_tier* t) {
+  return ackpt::guard([&] {
+    ACKPT_CUDA_CHECK(cudaStreamSynchronize(t->d2h));
+    ACKPT_CUDA_CHECK(cudaStreamSynchronize(t->h2d));
+    std::lock_guard<std::mutex> lk(t->mu);
+    for (auto& kv : t->keys) {
+      if (kv.second.slot >= 0) t->free_slots.push_back(kv.second.slot);
+      if (kv.second.last_store) cudaEventDestroy(kv.second.last_store);
+      if (kv.second.last_fetch) cudaEventDestroy(kv.second.last_fetch);
+    }
+    t->keys.clear();
+    for (auto& tk : t->tickets) ackpt::retire(t, tk);
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,395 @@
+"""Executes a forward/backward operator pair under a reversal strategy on
+the GPU.  Same API as the reference runtime (pkg/src/asyncckpt/runtime.py):
+``OperatorPair``, ``ExecutionStats``, ``FullStorage`` / ``Revolve`` /
+``Multistage``, ``execute``, ``run_forward_sweep``, ``run_backward_sweep``,
+``calibrate``.
+
+The action interpreter, the multistage sweeps, the byte ledger and all waits
+run in C++ (csrc/engine.cpp) on CUDA streams; Python only prepares the call.
+States are torch CUDA tensors of ``state_size`` bytes (``bytes`` inputs are
+staged to the device and the adjoint is returned as ``bytes`` then).
+
+Operators come in two kinds:
+  * native (``OperatorPair.native`` set, e.g. ``lstm.operator_pair``): the
+    engine launches the sm_100a step kernels directly;
+  * Python callables over CUDA tensors: wrapped as C callbacks of the
+    ackpt_operator plugin interface (one GIL round trip per step).
+
+Setting CKPT_DISABLE_PREFETCH=1 issues each fetch right before its interval
+(runtime.py:19-21, 302); results are unchanged, only stalls grow.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import asdict, dataclass, field
+from typing import Any, Callable, Optional, Union
+
+import torch
+
+from . import _native as N
+from .errors import SizeMismatch
+from .perfmodel import interval_length
+from .schedule import MultistagePlan
+from .storage import Level2Backend, as_device_bytes, as_host_bytes, nbytes_of
+
+ForwardStep = Callable[[int, Any], Any]
+BackwardStep = Callable[[int, Any, Any], Any]
+SeedSource = Union[bytes, torch.Tensor, Callable[[Any], Any]]
+
+
+@dataclass(frozen=True)
+class OperatorPair:
+    """Deterministic forward and backward operators over fixed-size states.
+
+    forward_step(k, state_k) -> state_{k+1}; backward_step(k, state_k,
+    adjoint_{k+1}) -> adjoint_k; adjoint_seed: adjoint at step n, concrete or
+    a callable of the final state (runtime.py:62-87).  ``native`` optionally
+    carries the device operator the engine calls without Python.
+    """
+
+    forward_step: ForwardStep
+    backward_step: BackwardStep
+    state_size: int
+    n_steps: int
+    adjoint_seed: SeedSource
+    native: Any = field(default=None, compare=False, repr=False)
+
+    def __post_init__(self) -> None:
+        if self.n_steps < 1:
+            raise ValueError(f"n_steps must be >= 1, got {self.n_steps}")
+        if self.state_size <= 0:
+            raise ValueError(f"state_size must be positive, got {self.state_size}")
+
+    def seed_for(self, final_state):
+        if callable(self.adjoint_seed):
+            return self.adjoint_seed(final_state)
+        return self.adjoint_seed
+
+
+@dataclass
+class ExecutionStats:
+    """The reference's seven counters (runtime.py:90-101).  B200 extras
+    (gpu_seconds, kernel_launches, interval, ...) are in ``.device``."""
+
+    forward_evals: int = 0
+    backward_evals: int = 0
+    stores_issued: int = 0
+    prefetches_issued: int = 0
+    stall_seconds: float = 0.0
+    peak_l1_bytes: int = 0
+    wall_seconds: float = 0.0
+
+    def to_dict(self) -> dict:
+        return asdict(self)
+
+
+@dataclass(frozen=True)
+class FullStorage:
+    pass
+
+
+@dataclass(frozen=True)
+class Revolve:
+    slots: int
+
+
+@dataclass(frozen=True)
+class Multistage:
+    slots: int
+    interval: Optional[int] = None  # None: calibrate, then ceil(t_t / t_a)
+
+
+Strategy = Union[FullStorage, Revolve, Multistage]
+
+
+def _stats_from(st: N.Stats) -> ExecutionStats:
+    out = ExecutionStats(
+        forward_evals=st.forward_evals,
+        backward_evals=st.backward_evals,
+        stores_issued=st.stores_issued,
+        prefetches_issued=st.prefetches_issued,
+        stall_seconds=st.stall_seconds,
+        peak_l1_bytes=st.peak_l1_bytes,
+        wall_seconds=st.wall_seconds,
+    )
+    out.device = {
+        "gpu_seconds": st.gpu_seconds,
+        "kernel_launches": st.kernel_launches,
+        "interval": st.interval,
+        "fallback": bool(st.fallback),
+        "device_buffers": st.device_buffers,
+        "link_bytes": st.link_bytes,
+        "fused_advances": st.fused_advances,
+    }
+    return out
+
+
+# ---------------------------------------------------------------------------
+# Python-callable operators through the C plugin interface
+
+
+class _DevBuf:
+    """__cuda_array_interface__ view of a raw device pointer."""
+
+    def __init__(self, ptr: int, nbytes: int):
+        self.__cuda_array_interface__ = {
+            "shape": (nbytes,),
+            "typestr": "|u1",
+            "data": (ptr, False),
+            "version": 3,
+            "strides": None,
+            "stream": None,
+        }
+
+
+def _view(ptr: int, nbytes: int) -> torch.Tensor:
+    return torch.as_tensor(_DevBuf(ptr, nbytes), device="cuda")
+
+
+class _CallbackOperator:
+    """ackpt_operator whose functions call the OperatorPair's Python callables
+    on the engine's stream.  Callables see uint8 CUDA tensors of state_size
+    bytes and may return tensors (any dtype, same byte size) or bytes."""
+
+    def __init__(self, ops: OperatorPair):
+        self.ops = ops
+        S = ops.state_size
+        self.error: Optional[BaseException] = None
+
+        def put(ptr: int, value) -> None:
+            dst = _view(ptr, S)
+            src = as_device_bytes(value)
+            if src.numel() != S:
+                raise SizeMismatch(f"operator returned {src.numel()} bytes, expected {S}")
+            dst.copy_(src)
+
+        def guard(fn):
+            def call(*args):
+                stream = args[-1]
+                try:
+                    with torch.cuda.stream(torch.cuda.ExternalStream(stream)):
+                        fn(*args[:-1])
+                    return N.OK
+                except BaseException as exc:  # reported through the status code
+                    self.error = exc
+                    return N.EXECUTION_ERROR
+
+            return call
+
+        def fwd(ctx, step, inp, out):
+            put(out, ops.forward_step(step, _view(inp, S)))
+
+        def bwd(ctx, step, state, adj_in, adj_out):
+            put(adj_out, ops.backward_step(step, _view(state, S), _view(adj_in, S)))
+
+        def seed(ctx, final, adj_out):
+            put(adj_out, ops.seed_for(_view(final, S)))
+
+        self._fns = (
+            N.FORWARD_FN(guard(fwd)),
+            N.BACKWARD_FN(guard(bwd)),
+            N.SEED_FN(guard(seed)) if callable(ops.adjoint_seed) else N.SEED_FN(),
+        )
+        self.op = N.Operator(None, self._fns[0], self._fns[1], self._fns[2], N.ADVANCE_FN(), S, ops.n_steps)
+
+    def raise_pending(self) -> None:
+        if self.error is not None:
+            exc, self.error = self.error, None
+            raise exc
+
+
+class _Engine:
+    def __init__(self, op: N.Operator, owner):
+        self.owner = owner  # keeps callbacks / device cell alive
+        h = C.c_void_p()
+        N.check(N.lib.ackpt_engine_create(C.byref(op), C.byref(h)))
+        self.handle = h.value
+
+    def __del__(self):
+        try:
+            if self.handle:
+                N.lib.ackpt_engine_destroy(self.handle)
+        except Exception:
+            pass
+
+
+_CALLBACK_ENGINES: dict = {}
+
+
+def _engine_for(ops: OperatorPair) -> tuple:
+    """(engine, callback wrapper or None), cached per operator pair."""
+    if ops.native is not None:
+        eng = getattr(ops.native, "_engine", None)
+        if eng is None:
+            eng = _Engine(ops.native.operator(), ops.native)
+            ops.native._engine = eng
+        return eng, None
+    key = id(ops)
+    hit = _CALLBACK_ENGINES.get(key)
+    if hit is None or hit[2] is not ops:
+        cb = _CallbackOperator(ops)
+        hit = (_Engine(cb.op, cb), cb, ops)
+        _CALLBACK_ENGINES[key] = hit
+    return hit[0], hit[1]
+
+
+def _tier(backend: Optional[Level2Backend], state_size: int) -> Optional[int]:
+    if backend is None:
+        return None
+    if not isinstance(backend, Level2Backend):
+        raise TypeError("backend must be a paper_1806_01117_b200 Level2Backend")
+    return backend._ensure(state_size)
+
+
+def _stream() -> int:
+    return torch.cuda.current_stream().cuda_stream
+
+
+def _seed_ptr(ops: OperatorPair, cb) -> tuple:
+    """Device buffer of a concrete seed, or (None, None) when a seed function runs."""
+    if callable(ops.adjoint_seed):
+        return None, None
+    buf = as_device_bytes(ops.adjoint_seed)
+    if buf.numel() != ops.state_size:
+        raise SizeMismatch(f"adjoint seed is {buf.numel()} bytes, expected {ops.state_size}")
+    return buf.data_ptr(), buf
+
+
+def _output_like(state) -> torch.Tensor:
+    if isinstance(state, torch.Tensor):
+        return torch.empty_like(state, device=state.device if state.is_cuda else "cuda",
+                                memory_format=torch.contiguous_format)
+    return torch.empty(nbytes_of(state), dtype=torch.uint8, device="cuda")
+
+
+def _finish(out: torch.Tensor, like):
+    return out if isinstance(like, torch.Tensor) else as_host_bytes(out)
+
+
+def _prepare(engine: _Engine, strategy_code: int, slots: int, interval: int, tier) -> None:
+    N.check(N.lib.ackpt_engine_prepare(engine.handle, strategy_code, slots, interval, tier))
+
+
+def _device_state(initial_state) -> torch.Tensor:
+    if isinstance(initial_state, torch.Tensor):
+        t = initial_state.detach()
+        return (t if t.is_cuda else t.cuda()).contiguous()
+    return as_device_bytes(initial_state)
+
+
+def _resolve_interval(strategy: Multistage, ops, backend, initial_state) -> int:
+    # runtime.py:325-336
+    if strategy.interval is not None:
+        if strategy.interval < 1:
+            raise ValueError(f"interval must be >= 1, got {strategy.interval}")
+        return strategy.interval
+    t_a, _, t_t = calibrate(ops, backend, 5, initial_state)
+    return interval_length(t_t, t_a)
+
+
+def execute(
+    strategy: Strategy,
+    ops: OperatorPair,
+    initial_state,
+    backend: Optional[Level2Backend] = None,
+    *,
+    fuse: bool = False,
+):
+    """One forward/backward pass; returns (step-0 adjoint, stats).
+
+    The adjoint is bit-identical across strategies (deterministic kernels,
+    no atomics).  Multistage requires a backend.  ``fuse=True`` runs each
+    Advance action as one fused launch (counters unchanged).  Planning,
+    calibration and HBM pool allocation happen before the timed window
+    (runtime.py:355-363).
+    """
+    if nbytes_of(initial_state) != ops.state_size:
+        raise SizeMismatch(
+            f"initial state is {nbytes_of(initial_state)} bytes, expected {ops.state_size}"
+        )
+    tier = None
+    if isinstance(strategy, Multistage):
+        if backend is None:
+            raise ValueError("Multistage requires a Level-2 backend")
+        interval = _resolve_interval(strategy, ops, backend, initial_state)
+        tier = _tier(backend, ops.state_size)
+        code, slots = N.MULTISTAGE, strategy.slots
+    elif isinstance(strategy, Revolve):
+        code, slots, interval = N.REVOLVE, strategy.slots, 0
+    elif isinstance(strategy, FullStorage):
+        code, slots, interval = N.FULL_STORAGE, 0, 0
+    else:
+        raise TypeError(f"unknown strategy {strategy!r}")
+    engine, cb = _engine_for(ops)
+    _prepare(engine, code, slots, interval, tier)
+    N.check(N.lib.ackpt_engine_set_fusion(engine.handle, 1 if fuse else 0))
+    state = _device_state(initial_state)
+    out = _output_like(initial_state)
+    seed_ptr, seed_keep = _seed_ptr(ops, cb)
+    st = N.Stats()
+    rc = N.lib.ackpt_engine_run(engine.handle, state.data_ptr(), seed_ptr, out.data_ptr(), C.byref(st), _stream())
+    if cb is not None:
+        cb.raise_pending()
+    N.check(rc)
+    return _finish(out, initial_state), _stats_from(st)
+
+
+def _sweep_engine(plan: MultistagePlan, ops: OperatorPair, backend) -> _Engine:
+    if plan.fallback:
+        raise ValueError("fallback plans have no Level-2 phase; use execute()")
+    engine, cb = _engine_for(ops)
+    _prepare(engine, N.MULTISTAGE, plan.s, plan.interval, _tier(backend, ops.state_size))
+    return engine, cb
+
+
+def run_forward_sweep(plan: MultistagePlan, ops: OperatorPair, backend, initial_state):
+    """Store every boundary state of a non-fallback plan; returns the stored
+    keys and the final state (runtime.py:384-399)."""
+    engine, cb = _sweep_engine(plan, ops, backend)
+    state = _device_state(initial_state)
+    final = _output_like(initial_state)
+    st = N.Stats()
+    rc = N.lib.ackpt_engine_forward_sweep(engine.handle, state.data_ptr(), final.data_ptr(), C.byref(st), _stream())
+    if cb is not None:
+        cb.raise_pending()
+    N.check(rc)
+    return list(plan.boundaries), _finish(final, initial_state)
+
+
+def run_backward_sweep(plan: MultistagePlan, ops: OperatorPair, backend, adjoint_seed):
+    """Reverse all intervals from boundary states already in the backend;
+    MissingKey propagates for a boundary never stored (runtime.py:402-417)."""
+    engine, cb = _sweep_engine(plan, ops, backend)
+    seed = _device_state(adjoint_seed)
+    if seed.numel() * seed.element_size() != ops.state_size:
+        raise SizeMismatch("adjoint seed does not match state_size")
+    out = _output_like(adjoint_seed)
+    st = N.Stats()
+    rc = N.lib.ackpt_engine_backward_sweep(engine.handle, seed.data_ptr(), out.data_ptr(), C.byref(st), _stream())
+    if cb is not None:
+        cb.raise_pending()
+    N.check(rc)
+    return _finish(out, adjoint_seed)
+
+
+def calibrate(ops: OperatorPair, backend, trial_steps: int, initial_state) -> tuple:
+    """Median (t_a, t_b, t_t) in seconds over trial_steps forward steps,
+    backward steps and store round trips, timed with CUDA events
+    (runtime.py:420-466).  Keys 0..trial_steps-1 are overwritten."""
+    if trial_steps < 3:
+        raise ValueError(f"trial_steps must be >= 3, got {trial_steps}")
+    if nbytes_of(initial_state) != ops.state_size:
+        raise SizeMismatch("initial state does not match state_size")
+    engine, cb = _engine_for(ops)
+    tier = _tier(backend, ops.state_size)
+    state = _device_state(initial_state)
+    t_a, t_b, t_t = C.c_double(), C.c_double(), C.c_double()
+    torch.cuda.current_stream().synchronize()
+    rc = N.lib.ackpt_engine_calibrate(
+        engine.handle, tier, trial_steps, state.data_ptr(), C.byref(t_a), C.byref(t_b), C.byref(t_t)
+    )
+    if cb is not None:
+        cb.raise_pending()
+    N.check(rc)
+    return t_a.value, t_b.value, t_t.value
