@@ -1,0 +1,444 @@
+#!/usr/bin/env python
+"""Headline benchmark: reverse-pass overhead vs store-all and steps/s at
+memory ratio 0.1, n = 10^4 (BASELINE.json), on BASELINE config 2:
+
+  one 64 MiB fp32 state per GPU = LSTM cell d=8 over B = 2^20 independent
+  sequences (layout (2, d, B)), n = 10^4 steps, Multistage(slots=999, I) with
+  I = interval_length(t_t, t_a) from calibration, HBM slot pool + async
+  pinned-host tier.
+
+A "step" of this benchmark is one full forward/backward pass (execute) over
+the n-step chain.  ``value`` = state-steps per second over all GPUs
+(n x N_gpus / pass time, weak scaling: every rank owns its own 64 MiB shard
+of the batch and runs the identical schedule; there is no collective in the
+timed region).  Launch: ``python bench.py`` (1 GPU) or
+``torchrun --nproc-per-node N bench.py --gpus N``.
+
+``--impl reference`` times the CPU restatement of the reference algorithm
+(oracle/, numpy, all host cores) on a bounded sample of the same workload.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+METRIC = "reverse-pass steps/s at memory ratio 0.1, n=10^4 (overhead vs store-all reported beside)"
+
+
+def parse_args(argv=None):
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=5)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    p.add_argument("--n", type=int, default=10_000)
+    p.add_argument("--d", type=int, default=8)
+    p.add_argument("--batch", type=int, default=1 << 20, help="sequences per GPU")
+    p.add_argument("--memory-ratio", type=float, default=0.1)
+    p.add_argument("--interval", type=int, default=0, help="0: calibrate")
+    p.add_argument("--fuse", action="store_true", help="fused Advance launches")
+    p.add_argument("--no-revolve", action="store_true")
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-cpu", action="store_true")
+    p.add_argument("--sample-every", type=int, default=8)
+    return p.parse_args(argv)
+
+
+# ---------------------------------------------------------------------------
+# clocks (B200_PROFILING.md "clocks DURING the timed region")
+
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except (OSError, FileNotFoundError):
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm, smax, power, reasons = [], [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.lines:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax.append(float(parts[1]))
+                power.append(float(parts[2]))
+            except ValueError:
+                continue
+            for name, flag in zip(names, parts[3:7]):
+                if flag.lower() == "active":
+                    reasons.add(name)
+        return {
+            "sm_mhz": statistics.median(sm) if sm else None,
+            "sm_max_mhz": max(smax) if smax else None,
+            "power_w_max": max(power) if power else None,
+            "samples": len(sm),
+            "reasons": sorted(reasons),
+        }
+
+
+# ---------------------------------------------------------------------------
+# CPU port (oracle/) -- the reference algorithm restated in numpy
+
+def _cpu_worker(args):
+    d, n, seed, state_seed, b, lo, slots, interval = args
+    os.environ.setdefault("OMP_NUM_THREADS", "1")
+    import numpy as np
+
+    from oracle import lstm_oracle as L
+    from oracle import runtime_oracle as R
+
+    cell = L.random_cell(d, n, seed)
+    s0 = L.random_states(d, state_seed, lo + b)[:, :, lo:]
+    t0 = time.perf_counter()
+    R.execute("multistage", cell, np.ascontiguousarray(s0), slots=slots, interval=interval, dtype=np.float32)
+    return time.perf_counter() - t0
+
+
+def cpu_port_steps(d, interval, slots, reps, cores, per_core=4096, pool=None):
+    """Times the oracle executor (Multistage over n = 2 I steps, fp32) on
+    cores x per_core sequences in parallel; returns (steps/s scaled to one
+    2^20-sequence state, description)."""
+    import multiprocessing as mp
+
+    n = 2 * interval
+    own = pool is None
+    if own:
+        pool = mp.get_context("spawn").Pool(cores, initializer=_pin_blas)
+    try:
+        walls = []
+        for _ in range(reps):
+            jobs = [(d, n, 0, 1, per_core, c * per_core, slots, interval) for c in range(cores)]
+            t0 = time.perf_counter()
+            pool.map(_cpu_worker, jobs)
+            walls.append(time.perf_counter() - t0)
+    finally:
+        if own:
+            pool.close()
+            pool.join()
+    seqs = cores * per_core
+    best = min(walls)
+    value = n / best * seqs / float(1 << 20)
+    sample = (f"oracle/runtime_oracle.execute Multistage(slots={slots}, I={interval}) over n={n} steps, "
+              f"{seqs} sequences (d={d}, fp32) split over {cores} processes; steps/s scaled to a "
+              f"2^20-sequence (64 MiB) state; best of {reps}")
+    return value, sample, walls
+
+
+def _pin_blas():
+    os.environ["OMP_NUM_THREADS"] = "1"
+    os.environ["OPENBLAS_NUM_THREADS"] = "1"
+    os.environ["MKL_NUM_THREADS"] = "1"
+
+
+def run_reference(args) -> None:
+    """--impl reference: the CPU restatement on this host's cores."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import multiprocessing as mp
+
+    cores = os.cpu_count() or 1
+    interval = args.interval or 58
+    slots = max(1, int(args.memory_ratio * args.n) - 1)
+    pool = mp.get_context("spawn").Pool(cores, initializer=_pin_blas)
+    try:
+        cpu_port_steps(args.d, interval, slots, max(1, args.warmup), cores, pool=pool)
+        value, sample, walls = cpu_port_steps(args.d, interval, slots, args.steps, cores, pool=pool)
+    finally:
+        pool.close()
+        pool.join()
+    n_sample = 2 * interval
+    ms = statistics.mean(walls) * 1e3
+    line = {
+        "impl": "reference",
+        "metric": METRIC,
+        "value": value,
+        "unit": "steps/s",
+        "n_gpus": args.gpus,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": ms,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f32",
+        "data": "synthetic",
+        "config": workload_config(args, interval, slots),
+        "cpu_baseline": {"value": value, "unit": "steps/s", "cores": cores, "kind": "port", "sample": sample},
+        "e2e": {"value": value, "unit": "steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "note": f"each step is one bounded sample ({n_sample} chain steps); the reference package is "
+                "pure Python/numpy (no native code), restated in oracle/ and run on all host cores",
+    }
+    print(json.dumps(line), flush=True)
+
+
+def workload_config(args, interval, slots) -> dict:
+    return {
+        "workload": "BASELINE config 2: 1 GPU, 64 MiB fp32 state, n=10^4, memory ratio 0.1, "
+                    "HBM snapshots + async pinned-host tier (LSTM d=8 over 2^20 sequences)",
+        "n": args.n,
+        "d": args.d,
+        "batch_per_gpu": args.batch,
+        "state_bytes_per_gpu": 2 * args.d * args.batch * 4,
+        "strategy": f"Multistage(slots={slots}, interval={interval})",
+        "memory_ratio": args.memory_ratio,
+        "fused_advance": bool(args.fuse),
+        "l2": "inputs larger than L2: every pass cycles >= I+2 distinct 64 MiB buffers (126 MB L2)",
+        "parallelism": f"batch-sharded x{args.gpus}, identical schedule per rank, no collective in the timed region",
+    }
+
+
+# ---------------------------------------------------------------------------
+
+
+def main(argv=None) -> None:
+    args = parse_args(argv)
+    if args.impl == "reference":
+        run_reference(args)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    import paper_1806_01117_b200 as pkg
+    import paper_1806_01117_b200.lstm as lstm
+
+    dev = torch.device("cuda", local)
+    cell = lstm.random_cell(args.d, args.n, 0)
+    ops = lstm.operator_pair(cell, args.batch, "f32")
+    S = ops.state_size
+    # each rank owns batch shard `rank` of the global batch (seeded per shard)
+    state0 = lstm.random_states(args.d, 1 + rank, args.batch, "f32", device=dev)
+    backend = pkg.PinnedHostBackend(slot_bytes=S)
+    slots = max(1, int(args.memory_ratio * args.n) - 1)
+
+    # --- calibration (outside the timed window, runtime.py:359-361) ---
+    t_a, t_b, t_t = pkg.calibrate(ops, backend, 5, state0)
+    interval = args.interval or pkg.interval_length(t_t, t_a)
+    if world > 1:  # identical schedule on every rank
+        t = torch.tensor([interval], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        interval = int(t.item())
+    strategy = pkg.Multistage(slots, interval)
+
+    def run_once(sample=0):
+        return pkg.execute(strategy, ops, state0, backend, fuse=args.fuse, sample_kernels=sample)
+
+    for _ in range(args.warmup):
+        adj, st = run_once()
+    torch.cuda.synchronize()
+
+    # --- timed region: K passes, inputs resident in HBM ---
+    clocks = ClockSampler(local)
+    clocks.start()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    stream = torch.cuda.current_stream()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    h0 = time.perf_counter()
+    stats = []
+    for _ in range(args.steps):
+        adj, st = run_once(args.sample_every)
+        stats.append(st)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    host_elapsed = time.perf_counter() - h0
+    elapsed = e0.elapsed_time(e1) * 1e-3
+    if world > 1:
+        dist.barrier()
+        t = torch.tensor([elapsed], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        elapsed = float(t.item())
+    clock = clocks.stop()
+    ms_per_step = elapsed / args.steps * 1e3
+    value = world * args.n * args.steps / elapsed
+
+    # --- per-kernel durations sampled inside the timed passes ---
+    fwd_s = sum(s.device["fwd_sample_seconds"] for s in stats)
+    fwd_n = sum(s.device["fwd_samples"] for s in stats)
+    bwd_s = sum(s.device["bwd_sample_seconds"] for s in stats)
+    bwd_n = sum(s.device["bwd_samples"] for s in stats)
+    t_fwd = fwd_s / max(1, fwd_n)
+    t_bwd = bwd_s / max(1, bwd_n)
+    last = stats[-1]
+    launches = sum(s.device["kernel_launches"] for s in stats)
+    t_inf = args.n * (t_fwd + t_bwd)  # store-all time from measured per-step kernels
+    overhead = (ms_per_step * 1e-3) / t_inf
+
+    # --- roofline: dominant kernel + whole pass ---
+    peaks = {}
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            peaks = json.load(fh)
+    except OSError:
+        pass
+    hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
+    peak_src = "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback 6.65 TB/s (B200_PROFILING.md)"
+    fwd_time_share = last.forward_evals * t_fwd
+    bwd_time_share = last.backward_evals * t_bwd
+    dominant = "lstm_fwd (K1)" if fwd_time_share >= bwd_time_share else "lstm_bwd (K2)"
+    bytes_dom = 2 * S if dominant.startswith("lstm_fwd") else 3 * S
+    t_dom = t_fwd if dominant.startswith("lstm_fwd") else t_bwd
+    achieved = bytes_dom / t_dom / 1e9
+    traffic = None
+    tfile = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tfile):
+        with open(tfile) as fh:
+            traffic = json.load(fh).get("fwd" if dominant.startswith("lstm_fwd") else "bwd")
+    link_gbs = S / t_t / 1e9
+    hbm_bytes = last.forward_evals * 2 * S + last.backward_evals * 3 * S
+    link_bytes = (last.stores_issued + last.prefetches_issued) * S
+    pass_roofline = max(hbm_bytes / (hbm_peak * 1e9), link_bytes / (link_gbs * 1e9))
+
+    # --- Revolve(s) at the same memory ratio, for comparison ---
+    revolve = None
+    if not args.no_revolve:
+        try:
+            pkg.execute(pkg.Revolve(slots), ops, state0)
+            _, rst = pkg.execute(pkg.Revolve(slots), ops, state0)
+            revolve = {
+                "slots": slots,
+                "wall_seconds": rst.wall_seconds,
+                "steps_per_s": args.n / rst.wall_seconds,
+                "overhead_vs_store_all": rst.wall_seconds / t_inf,
+                "forward_evals": rst.forward_evals,
+                "recompute_factor": rst.forward_evals / args.n,
+                "peak_l1_bytes": rst.peak_l1_bytes,
+            }
+        except pkg.CheckpointError as exc:  # e.g. HBM too small for s+1 states
+            revolve = {"error": str(exc)}
+
+    # --- end to end through the public API with host buffers ---
+    e2e = None
+    if not args.no_e2e:
+        host_in = state0.cpu().pin_memory()
+        host_out = torch.empty_like(host_in).pin_memory()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        g0 = torch.cuda.Event(enable_timing=True)
+        g1 = torch.cuda.Event(enable_timing=True)
+        g0.record()
+        for _ in range(args.steps):
+            adj_dev, _ = pkg.execute(strategy, ops, host_in, backend, fuse=args.fuse)
+            host_out.copy_(adj_dev)
+        g1.record()
+        torch.cuda.synchronize()
+        e2e_elapsed = g0.elapsed_time(g1) * 1e-3
+        if world > 1:
+            t = torch.tensor([e2e_elapsed], device=dev, dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e2e_elapsed = float(t.item())
+        e2e = {"value": world * args.n * args.steps / e2e_elapsed, "unit": "steps/s",
+               "h2d_bytes_per_step": S, "d2h_bytes_per_step": S,
+               "ms_per_step": e2e_elapsed / args.steps * 1e3}
+
+    # --- CPU baseline (rank 0, N=1 only) ---
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        cores = os.cpu_count() or 1
+        cval, sample, _ = cpu_port_steps(args.d, interval, slots, 3, cores)
+        cpu = {"value": cval, "unit": "steps/s", "cores": cores, "kind": "port", "sample": sample}
+
+    if world > 1:
+        dist.barrier()
+    if rank == 0:
+        line = {
+            "metric": METRIC,
+            "value": value,
+            "unit": "steps/s",
+            "n_gpus": world,
+            "steps": args.steps,
+            "warmup": args.warmup,
+            "ms_per_step": ms_per_step,
+            "higher_is_better": True,
+            "scaling": "weak",
+            "vs_baseline": None,
+            "dtype": "f32",
+            "data": "synthetic",
+            "config": workload_config(args, interval, slots),
+            "impl": "ours",
+            "overhead_vs_store_all": overhead,
+            "t_inf_seconds": t_inf,
+            "t_a_us": t_fwd * 1e6,
+            "t_b_us": t_bwd * 1e6,
+            "calibrated": {"t_a_us": t_a * 1e6, "t_b_us": t_b * 1e6, "t_t_ms": t_t * 1e3, "interval": interval},
+            "link_gbs": link_gbs,
+            "recompute_factor_measured": last.forward_evals / args.n,
+            "forward_evals": last.forward_evals,
+            "backward_evals": last.backward_evals,
+            "stores_issued": last.stores_issued,
+            "prefetches_issued": last.prefetches_issued,
+            "stall_seconds": last.stall_seconds,
+            "peak_l1_bytes": last.peak_l1_bytes,
+            "host_wall_seconds_per_pass": host_elapsed / args.steps,
+            "pass_roofline": {"seconds": pass_roofline, "frac": pass_roofline / (ms_per_step * 1e-3),
+                              "hbm_bytes": hbm_bytes, "link_bytes": link_bytes},
+            "roofline": {"kernel": dominant, "bound": "hbm", "achieved": achieved, "peak": hbm_peak,
+                         "unit": "GB/s", "frac": achieved / hbm_peak, "traffic": traffic,
+                         "algorithmic_bytes_per_launch": bytes_dom, "avg_launch_us": t_dom * 1e6,
+                         "samples": fwd_n if dominant.startswith("lstm_fwd") else bwd_n, "peak_source": peak_src},
+            "revolve": revolve,
+            "e2e": e2e,
+            "cpu_baseline": cpu,
+            "gpu_launches": launches,
+            "clocks": clock,
+        }
+        print(json.dumps(line), flush=True)
+    backend.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -149,6 +149,14 @@ typedef struct ackpt_operator {
 /* Fills *out with the built-in LSTM operator bound to cell. */
 ACKPT_API int ackpt_lstm_operator(ackpt_lstm* cell, ackpt_operator* out);
 
+/* Latency injection (test support, pkg/tests/test_runtime.py:33-52 pad_operators):
+ * *out wraps base so each forward / backward call first holds the stream for
+ * the given seconds with a device-side delay kernel.  Release with
+ * ackpt_pad_operator_destroy(out). */
+ACKPT_API int ackpt_pad_operator_create(const ackpt_operator* base, double forward_seconds,
+                                        double backward_seconds, ackpt_operator* out);
+ACKPT_API int ackpt_pad_operator_destroy(ackpt_operator* op);
+
 /* ---- Level-2 tier: HBM <-> pinned host DRAM (storage.py:181-278) ---- */
 typedef struct ackpt_tier ackpt_tier;
 typedef int64_t ackpt_ticket;
@@ -203,6 +211,12 @@ typedef struct ackpt_stats {
   int64_t device_buffers;   /* HBM state buffers held by the pool */
   int64_t link_bytes;       /* bytes moved over the host link */
   int64_t fused_advances;   /* Advance actions run as one fused launch */
+  /* sampled kernel timing (ackpt_engine_set_kernel_sampling): CUDA-event
+   * durations of every k-th forward / backward launch inside the run */
+  double fwd_sample_seconds;
+  int64_t fwd_samples;
+  double bwd_sample_seconds;
+  int64_t bwd_samples;
 } ackpt_stats;
 
 typedef struct ackpt_engine ackpt_engine;
@@ -219,6 +233,9 @@ ACKPT_API int ackpt_engine_prepare(ackpt_engine* engine, int32_t strategy, int64
  * forward step.  1: run whole Advance actions as one fused launch when the
  * operator provides advance(); counters are unchanged. */
 ACKPT_API int ackpt_engine_set_fusion(ackpt_engine* engine, int32_t fuse_advance);
+/* Time every k-th forward and backward launch with a CUDA event pair on the
+ * compute stream (0 = off).  Takes effect at the next prepare. */
+ACKPT_API int ackpt_engine_set_kernel_sampling(ackpt_engine* engine, int64_t every);
 /* Mirrors CKPT_DISABLE_PREFETCH=1 (runtime.py:302): -1 read the env var at run. */
 ACKPT_API int ackpt_engine_set_prefetch(ackpt_engine* engine, int32_t prefetch);
 /* One forward/backward pass (runtime.py:339-381).  seed may be NULL when the

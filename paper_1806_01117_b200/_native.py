@@ -76,6 +76,10 @@ class Stats(C.Structure):
         ("device_buffers", C.c_int64),
         ("link_bytes", C.c_int64),
         ("fused_advances", C.c_int64),
+        ("fwd_sample_seconds", C.c_double),
+        ("fwd_samples", C.c_int64),
+        ("bwd_sample_seconds", C.c_double),
+        ("bwd_samples", C.c_int64),
     ]
 
 
@@ -126,6 +130,8 @@ _SIGS = {
     "ackpt_lstm_seed": ([_vp, _vp, _vp, _vp], C.c_int),
     "ackpt_lstm_loss": ([_vp, _vp, _vp, _vp], C.c_int),
     "ackpt_lstm_operator": ([_vp, C.POINTER(Operator)], C.c_int),
+    "ackpt_pad_operator_create": ([C.POINTER(Operator), C.c_double, C.c_double, C.POINTER(Operator)], C.c_int),
+    "ackpt_pad_operator_destroy": ([C.POINTER(Operator)], C.c_int),
     "ackpt_tier_create": ([C.c_int64, C.c_int64, C.POINTER(_vp)], C.c_int),
     "ackpt_tier_destroy": ([_vp], C.c_int),
     "ackpt_tier_set_throttle": ([_vp, C.c_double, C.c_double], C.c_int),
@@ -143,6 +149,7 @@ _SIGS = {
     "ackpt_engine_prepare": ([_vp, C.c_int32, C.c_int64, C.c_int64, _vp], C.c_int),
     "ackpt_engine_set_fusion": ([_vp, C.c_int32], C.c_int),
     "ackpt_engine_set_prefetch": ([_vp, C.c_int32], C.c_int),
+    "ackpt_engine_set_kernel_sampling": ([_vp, C.c_int64], C.c_int),
     "ackpt_engine_run": ([_vp, _vp, _vp, _vp, C.POINTER(Stats), _vp], C.c_int),
     "ackpt_engine_forward_sweep": ([_vp, _vp, _vp, C.POINTER(Stats), _vp], C.c_int),
     "ackpt_engine_backward_sweep": ([_vp, _vp, _vp, C.POINTER(Stats), _vp], C.c_int),

@@ -79,6 +79,7 @@ struct ackpt_engine {
   cudaStream_t compute = nullptr;
   int fuse = 0;
   int prefetch = -1;
+  int64_t sample_every = 0;
 };
 
 namespace ackpt {
@@ -193,12 +194,31 @@ struct Run {
     seeded = true;
   }
 
+  // Sampled kernel timing: an event pair around every k-th launch.
+  int64_t fwd_calls = 0, bwd_calls = 0;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> fwd_pairs, bwd_pairs;
+
+  template <class F>
+  void timed(int64_t& calls, std::vector<std::pair<cudaEvent_t, cudaEvent_t>>& pairs, F&& launch) {
+    const bool sample = E->sample_every > 0 && (calls++ % E->sample_every) == 0;
+    if (!sample) {
+      if (!dry) launch();
+      return;
+    }
+    cudaEvent_t e0 = timing_event(), e1 = timing_event();
+    if (dry) return;
+    ACKPT_CUDA_CHECK(cudaEventRecord(e0, s));
+    launch();
+    ACKPT_CUDA_CHECK(cudaEventRecord(e1, s));
+    pairs.emplace_back(e0, e1);
+  }
+
   int forward(int64_t step, int cur) {
     int out = acquire();
-    if (!dry) {
+    timed(fwd_calls, fwd_pairs, [&] {
       check_op(E->op.forward(E->op.ctx, step, ptr(cur), wptr(out), s));
       ++st.kernel_launches;
-    }
+    });
     release(cur);
     ++st.forward_evals;
     if (step + 1 == E->n && !seeded) do_seed(out);
@@ -227,10 +247,10 @@ struct Run {
   void backward(int64_t step, int state) {
     if (!seeded)
       fail(ACKPT_EXECUTION_ERROR, "Reverse " + std::to_string(step) + " before the adjoint was seeded");
-    if (!dry) {
+    timed(bwd_calls, bwd_pairs, [&] {
       check_op(E->op.backward(E->op.ctx, step, ptr(state), adj[a], adj[1 - a], s));
       ++st.kernel_launches;
-    }
+    });
     a = 1 - a;
     ++st.backward_evals;
   }
@@ -516,6 +536,19 @@ void run_impl(ackpt_engine* E, Mode mode, const void* initial_state, const void*
     stall += std::max(0.0, double(msv) * 1e-3);
   }
   r.st.stall_seconds = stall;
+  auto sum_pairs = [](const std::vector<std::pair<cudaEvent_t, cudaEvent_t>>& v) {
+    double acc = 0.0;
+    for (auto& pr : v) {
+      float msv = 0.f;
+      ACKPT_CUDA_CHECK(cudaEventElapsedTime(&msv, pr.first, pr.second));
+      acc += double(msv) * 1e-3;
+    }
+    return acc;
+  };
+  r.st.fwd_sample_seconds = sum_pairs(r.fwd_pairs);
+  r.st.fwd_samples = int64_t(r.fwd_pairs.size());
+  r.st.bwd_sample_seconds = sum_pairs(r.bwd_pairs);
+  r.st.bwd_samples = int64_t(r.bwd_pairs.size());
   if (stats) *stats = r.st;
 }
 
@@ -634,6 +667,12 @@ ACKPT_API int ackpt_engine_prepare(ackpt_engine* E, int32_t strategy, int64_t sl
 
 ACKPT_API int ackpt_engine_set_fusion(ackpt_engine* e, int32_t fuse_advance) {
   e->fuse = fuse_advance;
+  return ACKPT_OK;
+}
+
+ACKPT_API int ackpt_engine_set_kernel_sampling(ackpt_engine* e, int64_t every) {
+  e->sample_every = every < 0 ? 0 : every;
+  e->prepared = false;  // the timing-event pool is sized by the next prepare
   return ACKPT_OK;
 }
 

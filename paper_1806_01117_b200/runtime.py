@@ -121,6 +121,10 @@ def _stats_from(st: N.Stats) -> ExecutionStats:
         "device_buffers": st.device_buffers,
         "link_bytes": st.link_bytes,
         "fused_advances": st.fused_advances,
+        "fwd_sample_seconds": st.fwd_sample_seconds,
+        "fwd_samples": st.fwd_samples,
+        "bwd_sample_seconds": st.bwd_sample_seconds,
+        "bwd_samples": st.bwd_samples,
     }
     return out
 
@@ -234,6 +238,41 @@ def _engine_for(ops: OperatorPair) -> tuple:
     return hit[0], hit[1]
 
 
+class _PaddedNative:
+    """Native operator whose steps also hold the compute stream (test support)."""
+
+    def __init__(self, base, forward_delay: float, backward_delay: float):
+        self.base = base
+        self._op = N.Operator()
+        N.check(N.lib.ackpt_pad_operator_create(C.byref(base.operator()), forward_delay, backward_delay, C.byref(self._op)))
+
+    def operator(self) -> N.Operator:
+        return self._op
+
+    def __del__(self):
+        try:
+            self._engine = None
+            N.lib.ackpt_pad_operator_destroy(C.byref(self._op))
+        except Exception:
+            pass
+
+
+def pad_operator(ops: OperatorPair, forward_delay: float, backward_delay: float) -> OperatorPair:
+    """Stretch every forward / backward step of a native operator pair by a
+    device-side delay (the reference tests' pad_operators, test_runtime.py:33-52,
+    which sleep on the compute thread).  Results are unchanged."""
+    if ops.native is None:
+        raise TypeError("pad_operator needs a native operator pair")
+    return OperatorPair(
+        forward_step=ops.forward_step,
+        backward_step=ops.backward_step,
+        state_size=ops.state_size,
+        n_steps=ops.n_steps,
+        adjoint_seed=ops.adjoint_seed,
+        native=_PaddedNative(ops.native, forward_delay, backward_delay),
+    )
+
+
 def _tier(backend: Optional[Level2Backend], state_size: int) -> Optional[int]:
     if backend is None:
         return None
@@ -295,6 +334,7 @@ def execute(
     backend: Optional[Level2Backend] = None,
     *,
     fuse: bool = False,
+    sample_kernels: int = 0,
 ):
     """One forward/backward pass; returns (step-0 adjoint, stats).
 
@@ -322,6 +362,7 @@ def execute(
     else:
         raise TypeError(f"unknown strategy {strategy!r}")
     engine, cb = _engine_for(ops)
+    N.check(N.lib.ackpt_engine_set_kernel_sampling(engine.handle, int(sample_kernels)))
     _prepare(engine, code, slots, interval, tier)
     N.check(N.lib.ackpt_engine_set_fusion(engine.handle, 1 if fuse else 0))
     state = _device_state(initial_state)

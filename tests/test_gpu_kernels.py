@@ -1,0 +1,127 @@
+"""Per-step parity of the sm_100a kernels (K1 forward, K2 adjoint, K3 seed,
+K4 loss, fused advance) against the CPU oracle and the reference's golden
+steps.  SURVEY §8(c) protocol 1: fp32 rel-L2 <= 1e-5 against the float64
+oracle evaluated on the same (fp32-rounded) inputs; the f64 build <= 1e-12.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import lstm_oracle as L
+
+pytestmark = pytest.mark.gpu
+
+F32_TOL = 1e-5  # rel-L2, fp32 kernels vs float64 oracle
+F64_TOL = 1e-12  # rel-L2, float64 kernels vs reference
+
+
+@pytest.fixture(scope="module")
+def P():
+    import paper_1806_01117_b200.lstm as lstm
+
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    return lstm
+
+
+def _cells(P, d, n, seed):
+    return P.random_cell(d, n, seed), L.random_cell(d, n, seed)
+
+
+def _states(d, seed, batch, scale=1.0):
+    rng = np.random.default_rng(seed)
+    return rng.uniform(-scale, scale, (2, d, batch))
+
+
+@pytest.mark.parametrize("d,batch", [(8, 4096), (8, 2), (4, 1024), (8, 1001), (5, 64), (16, 300), (32, 17)])
+def test_forward_backward_f32_vs_oracle(P, d, batch):
+    cell, ocell = _cells(P, d, 6, 11 + d)
+    x = _states(d, 3, batch).astype(np.float32)
+    a = _states(d, 4, batch).astype(np.float32)
+    dc = P.device_cell(cell, batch, "f32")
+    for k in (0, 3, 5):
+        xt = torch.from_numpy(x).cuda()
+        at = torch.from_numpy(a).cuda()
+        fwd = dc.forward(k, xt).cpu().numpy()
+        bwd = dc.backward(k, xt, at).cpu().numpy()
+        ref_f = L.forward_step(ocell, k, x.astype(np.float64))
+        ref_b = L.backward_step(ocell, k, x.astype(np.float64), a.astype(np.float64))
+        assert L.rel_l2(fwd, ref_f) <= F32_TOL, (k, L.rel_l2(fwd, ref_f))
+        assert L.rel_l2(bwd, ref_b) <= F32_TOL, (k, L.rel_l2(bwd, ref_b))
+        # every sequence individually, not just the aggregate
+        for b in np.linspace(0, batch - 1, min(batch, 16)).astype(int):
+            assert L.rel_l2(fwd[:, :, b], ref_f[:, :, b]) <= 2 * F32_TOL
+            assert L.rel_l2(bwd[:, :, b], ref_b[:, :, b]) <= 2 * F32_TOL
+
+
+def test_f32_saturating_inputs(P):
+    # large pre-activations exercise the clamped shared-reciprocal path
+    d, batch = 8, 512
+    cell, ocell = _cells(P, d, 2, 5)
+    x = _states(d, 9, batch, scale=60.0).astype(np.float32)
+    a = _states(d, 10, batch).astype(np.float32)
+    dc = P.device_cell(cell, batch, "f32")
+    fwd = dc.forward(1, torch.from_numpy(x).cuda()).cpu().numpy()
+    bwd = dc.backward(1, torch.from_numpy(x).cuda(), torch.from_numpy(a).cuda()).cpu().numpy()
+    assert np.isfinite(fwd).all() and np.isfinite(bwd).all()
+    assert L.rel_l2(fwd, L.forward_step(ocell, 1, x.astype(np.float64))) <= F32_TOL
+    assert L.rel_l2(bwd, L.backward_step(ocell, 1, x.astype(np.float64), a.astype(np.float64))) <= F32_TOL
+
+
+@pytest.mark.parametrize("d,n,seed", [(4, 6, 5), (8, 10, 6), (6, 5, 7), (16, 4, 8), (5, 3, 9)])
+def test_f64_steps_match_reference_golden(P, step_golden, d, n, seed):
+    cell = P.random_cell(d, n, seed)
+    for k in range(n):
+        x = step_golden[f"d{d}_s{seed}_k{k}_in"].tobytes()
+        a = step_golden[f"d{d}_s{seed}_k{k}_adjin"].tobytes()
+        fwd = np.frombuffer(P.lstm_forward_step(cell, k, x), "<f8")
+        bwd = np.frombuffer(P.lstm_backward_step(cell, k, x, a), "<f8")
+        assert L.rel_l2(fwd, step_golden[f"d{d}_s{seed}_k{k}_fwd"]) <= F64_TOL
+        assert L.rel_l2(bwd, step_golden[f"d{d}_s{seed}_k{k}_bwd"]) <= F64_TOL
+
+
+def test_seed_and_loss(P):
+    d, batch = 8, 1000
+    cell, ocell = _cells(P, d, 3, 2)
+    x = _states(d, 5, batch)
+    for dtype, tol in (("f64", 1e-14), ("f32", 1e-6)):
+        npdt = np.float64 if dtype == "f64" else np.float32
+        xt = torch.from_numpy(x.astype(npdt)).cuda()
+        dc = P.device_cell(cell, batch, dtype)
+        seed = dc.seed(xt).cpu().numpy()
+        assert L.rel_l2(seed, L.seed(ocell, x.astype(npdt).astype(np.float64))) <= tol
+        assert (seed[1] == 0).all()
+        losses = dc.losses(xt).cpu().numpy()
+        assert L.rel_l2(losses, L.loss(ocell, x.astype(npdt).astype(np.float64))) <= tol
+
+
+@pytest.mark.parametrize("d,batch,dtype", [(8, 4096, "f32"), (4, 512, "f32"), (8, 7, "f32"), (6, 64, "f64")])
+def test_fused_advance_equals_step_chain(P, d, batch, dtype):
+    cell, ocell = _cells(P, d, 12, 21)
+    npdt = np.float64 if dtype == "f64" else np.float32
+    x = torch.from_numpy(_states(d, 8, batch).astype(npdt)).cuda()
+    dc = P.device_cell(cell, batch, dtype)
+    chain = x
+    for k in range(2, 11):
+        chain = dc.forward(k, chain)
+    fused = dc.advance(2, 11, x)
+    # identical arithmetic per step: bit-identical results
+    assert torch.equal(fused, chain)
+
+
+def test_c2_shape_kernels_on_sampled_rows(P):
+    # BASELINE config 2 shape: d=8, B=2^20 fp32 -> 64 MiB states
+    d, batch = 8, 1 << 20
+    cell, ocell = _cells(P, d, 4, 0)
+    x = P.random_states(d, 1, batch, "f32")
+    assert x.numel() * x.element_size() == 64 << 20
+    dc = P.device_cell(cell, batch, "f32")
+    y = dc.forward(2, x)
+    a = dc.seed(y)
+    g = dc.backward(2, x, a)
+    idx = torch.tensor([0, 1, 2, 3, 12345, batch // 2, batch - 2, batch - 1], device="cuda")
+    xs = x[:, :, idx].double().cpu().numpy()
+    assert L.rel_l2(y[:, :, idx].cpu().numpy(), L.forward_step(ocell, 2, xs)) <= F32_TOL
+    ys = y[:, :, idx].double().cpu().numpy()
+    a_ref = L.seed(ocell, ys)
+    assert L.rel_l2(g[:, :, idx].cpu().numpy(), L.backward_step(ocell, 2, xs, a_ref)) <= F32_TOL

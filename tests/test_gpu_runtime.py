@@ -1,0 +1,338 @@
+"""The reference's runtime tests (pkg/tests/test_runtime.py) on the GPU
+executor, plus end-to-end parity with the reference's golden adjoints and
+counters.  States are B=1 float64 ``bytes`` (the reference's byte image) or
+batched fp32 device tensors."""
+
+import json
+import time
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import lstm_oracle as L
+from oracle import runtime_oracle as RO
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def P():
+    import paper_1806_01117_b200 as pkg
+    import paper_1806_01117_b200.lstm as lstm
+    import paper_1806_01117_b200.runtime as rt
+
+    assert torch.cuda.is_available()
+    return pkg, lstm, rt
+
+
+@pytest.fixture
+def fast_backend(P):
+    pkg, _, _ = P
+    backend = pkg.SimulatedBackend(bandwidth=1e12, latency=0.0)
+    yield backend
+    backend.close()
+
+
+def lstm_setup(P, n=8, d=6, seed=3):
+    _, lstm, _ = P
+    cell = lstm.random_cell(d=d, n=n, seed=seed)
+    return cell, lstm.operator_pair(cell), lstm.random_state(d, seed + 100)
+
+
+def test_full_storage_counts(P):
+    pkg, _, _ = P
+    _, ops, s0 = lstm_setup(P, n=8)
+    adjoint, stats = pkg.execute(pkg.FullStorage(), ops, s0)
+    assert (stats.forward_evals, stats.backward_evals) == (8, 8)
+    assert stats.peak_l1_bytes == 8 * ops.state_size
+    assert len(adjoint) == ops.state_size
+
+
+def test_revolve_counts_bit_identical(P):
+    pkg, _, _ = P
+    _, ops, s0 = lstm_setup(P, n=8)
+    baseline, _ = pkg.execute(pkg.FullStorage(), ops, s0)
+    adjoint, stats = pkg.execute(pkg.Revolve(3), ops, s0)
+    assert adjoint == baseline
+    assert stats.forward_evals == 14 and stats.backward_evals == 8
+
+
+def test_multistage_counts_and_transfers(P, fast_backend):
+    pkg, _, _ = P
+    _, ops, s0 = lstm_setup(P, n=8)
+    baseline, _ = pkg.execute(pkg.FullStorage(), ops, s0)
+    adjoint, stats = pkg.execute(pkg.Multistage(3, interval=4), ops, s0, fast_backend)
+    assert adjoint == baseline
+    assert (stats.forward_evals, stats.backward_evals) == (16, 8)
+    assert (stats.stores_issued, stats.prefetches_issued) == (2, 2)
+    assert stats.peak_l1_bytes <= 7 * ops.state_size
+
+
+def test_multistage_inner_revolve(P, fast_backend):
+    pkg, _, _ = P
+    _, ops, s0 = lstm_setup(P, n=24, d=5, seed=9)
+    baseline, _ = pkg.execute(pkg.FullStorage(), ops, s0)
+    adjoint, stats = pkg.execute(pkg.Multistage(2, interval=8), ops, s0, fast_backend)
+    assert adjoint == baseline
+    assert stats.forward_evals == 24 + 3 * 18 and stats.backward_evals == 24
+
+
+def test_gradient_equivalence_across_seeds(P, fast_backend):
+    pkg, _, _ = P
+    for seed in range(4):
+        _, ops, s0 = lstm_setup(P, n=12, d=4, seed=seed)
+        g_full, _ = pkg.execute(pkg.FullStorage(), ops, s0)
+        g_rev, _ = pkg.execute(pkg.Revolve(3), ops, s0)
+        g_ms, _ = pkg.execute(pkg.Multistage(3, interval=5), ops, s0, fast_backend)
+        assert g_full == g_rev == g_ms
+
+
+def test_fallback_equals_revolve(P, fast_backend):
+    pkg, _, _ = P
+    _, ops, s0 = lstm_setup(P, n=5, d=4)
+    g_rev, st_rev = pkg.execute(pkg.Revolve(2), ops, s0)
+    g_ms, st_ms = pkg.execute(pkg.Multistage(2, interval=8), ops, s0, fast_backend)
+    assert g_ms == g_rev
+    assert st_ms.forward_evals == st_rev.forward_evals == 8
+    assert st_ms.stores_issued == st_ms.prefetches_issued == 0
+
+
+def test_argument_errors(P):
+    pkg, _, _ = P
+    _, ops, s0 = lstm_setup(P, n=8)
+    with pytest.raises(ValueError):
+        pkg.execute(pkg.Multistage(3, interval=4), ops, s0, None)
+    with pytest.raises(pkg.SizeMismatch):
+        pkg.execute(pkg.FullStorage(), ops, b"short")
+    with pytest.raises(pkg.InfeasibleSchedule):
+        pkg.execute(pkg.Revolve(0), ops, s0)
+
+
+def test_stats_serialize_verbatim_field_names(P):
+    pkg, _, _ = P
+    blob = json.loads(json.dumps(pkg.ExecutionStats(forward_evals=3, backward_evals=2).to_dict()))
+    assert set(blob) == {"forward_evals", "backward_evals", "stores_issued", "prefetches_issued",
+                         "stall_seconds", "peak_l1_bytes", "wall_seconds"}
+
+
+def test_sweeps(P, fast_backend):
+    pkg, lstm, _ = P
+    cell, ops, s0 = lstm_setup(P, n=12, d=4)
+    plan = pkg.plan_multistage(12, 3, 4)
+    keys, final_state = pkg.run_forward_sweep(plan, ops, fast_backend, s0)
+    assert keys == [0, 4, 8]
+    assert all(fast_backend.contains(k) for k in keys)
+    state = s0
+    for k in range(12):
+        state = ops.forward_step(k, state)
+    assert final_state == state
+    seed = lstm.loss_gradient_seed(cell, final_state)
+    adjoint = pkg.run_backward_sweep(plan, ops, fast_backend, seed)
+    baseline, _ = pkg.execute(pkg.FullStorage(), ops, s0)
+    assert adjoint == baseline
+
+
+def test_backward_sweep_missing_boundary(P, fast_backend):
+    pkg, _, _ = P
+    _, ops, _ = lstm_setup(P, n=8, d=4)
+    with pytest.raises(pkg.MissingKey):
+        pkg.run_backward_sweep(pkg.plan_multistage(8, 3, 4), ops, fast_backend, b"\x00" * ops.state_size)
+
+
+def test_sweep_wrappers_reject_fallback_plans(P, fast_backend):
+    pkg, _, _ = P
+    _, ops, s0 = lstm_setup(P, n=4, d=4)
+    plan = pkg.plan_multistage(4, 3, 9)
+    with pytest.raises(ValueError):
+        pkg.run_forward_sweep(plan, ops, fast_backend, s0)
+    with pytest.raises(ValueError):
+        pkg.run_backward_sweep(plan, ops, fast_backend, b"\x00" * ops.state_size)
+
+
+# -- asynchrony: device-side step delays + throttled tier (test_runtime.py:187-232)
+
+
+def test_transfers_overlap_compute(P):
+    pkg, _, rt = P
+    _, raw, s0 = lstm_setup(P, n=32, d=4)
+    ops = rt.pad_operator(raw, 2e-3, 2e-3)
+    backend = pkg.SimulatedBackend(bandwidth=1e12, latency=4e-3)  # < I t_a = 16 ms
+    try:
+        adjoint, stats = pkg.execute(pkg.Multistage(7, interval=8), ops, s0, backend)
+    finally:
+        backend.close()
+    baseline, _ = pkg.execute(pkg.FullStorage(), raw, s0)
+    assert adjoint == baseline
+    assert stats.stall_seconds < 0.05 * stats.wall_seconds
+
+
+def test_forced_store_contention_still_correct(P):
+    pkg, _, rt = P
+    _, raw, s0 = lstm_setup(P, n=16, d=4)
+    ops = rt.pad_operator(raw, 1e-3, 1e-3)
+    backend = pkg.SimulatedBackend(bandwidth=1e12, latency=12e-3)  # 3 I t_a
+    try:
+        adjoint, stats = pkg.execute(pkg.Multistage(3, interval=4), ops, s0, backend)
+    finally:
+        backend.close()
+    baseline, _ = pkg.execute(pkg.FullStorage(), raw, s0)
+    assert adjoint == baseline
+    assert stats.stall_seconds > 0.01
+
+
+def test_disable_prefetch_hook(P, monkeypatch):
+    pkg, _, rt = P
+    _, raw, s0 = lstm_setup(P, n=32, d=4)
+    ops = rt.pad_operator(raw, 1e-3, 1e-3)
+
+    def run():
+        backend = pkg.SimulatedBackend(bandwidth=1e12, latency=5e-3)
+        try:
+            return pkg.execute(pkg.Multistage(7, interval=8), ops, s0, backend)
+        finally:
+            backend.close()
+
+    monkeypatch.delenv("CKPT_DISABLE_PREFETCH", raising=False)
+    g_async, st_async = run()
+    monkeypatch.setenv("CKPT_DISABLE_PREFETCH", "1")
+    g_sync, st_sync = run()
+    assert g_sync == g_async
+    assert st_sync.stall_seconds > st_async.stall_seconds
+    assert st_sync.prefetches_issued == st_async.prefetches_issued == 4
+
+
+def test_calibrate(P, fast_backend):
+    pkg, _, rt = P
+    _, raw, s0 = lstm_setup(P, n=8, d=4)
+    with pytest.raises(ValueError):
+        pkg.calibrate(raw, fast_backend, 1, s0)
+    ops = rt.pad_operator(raw, 1e-3, 2e-3)
+    backend = pkg.SimulatedBackend(bandwidth=1e12, latency=10e-3)
+    try:
+        t_a, t_b, t_t = pkg.calibrate(ops, backend, 5, s0)
+        assert 8 <= round(t_t / t_a) <= 12
+        assert t_b >= t_a
+        assert t_t == pytest.approx(10e-3, rel=0.10)
+    finally:
+        backend.close()
+
+
+def test_calibrated_interval_selection(P):
+    pkg, _, rt = P
+    _, raw, s0 = lstm_setup(P, n=24, d=4)
+    ops = rt.pad_operator(raw, 1.5e-3, 1.5e-3)
+    backend = pkg.SimulatedBackend(bandwidth=1e12, latency=8e-3)
+    try:
+        adjoint, stats = pkg.execute(pkg.Multistage(7), ops, s0, backend)
+    finally:
+        backend.close()
+    baseline, _ = pkg.execute(pkg.FullStorage(), raw, s0)
+    assert adjoint == baseline
+    assert 3 <= stats.stores_issued <= 6
+
+
+def test_peaks_linear_vs_constant(P, fast_backend):
+    pkg, _, _ = P
+    _, o16, a = lstm_setup(P, n=16, d=4)
+    _, o32, b = lstm_setup(P, n=32, d=4)
+    assert pkg.execute(pkg.FullStorage(), o32, b)[1].peak_l1_bytes == 2 * pkg.execute(pkg.FullStorage(), o16, a)[1].peak_l1_bytes
+    peaks = []
+    for n in (32, 64):
+        _, ops, s0 = lstm_setup(P, n=n, d=4)
+        peaks.append(pkg.execute(pkg.Multistage(3, interval=8), ops, s0, fast_backend)[1].peak_l1_bytes)
+    assert peaks[0] == peaks[1]
+
+
+# -- parity with the reference (golden adjoints and counters) ----------------
+
+
+def test_end_to_end_matches_reference_golden(P, runtime_golden, fast_backend):
+    pkg, lstm, _ = P
+    cfgs, arrays = runtime_golden
+    strat = {
+        "full": lambda c: pkg.FullStorage(),
+        "revolve": lambda c: pkg.Revolve(c["slots"]),
+        "multistage": lambda c: pkg.Multistage(c["slots"], c["interval"]),
+    }
+    for cfg in cfgs:
+        cell = lstm.random_cell(cfg["d"], cfg["n"], cfg["seed"])
+        ops = lstm.operator_pair(cell)
+        s0 = lstm.random_state(cfg["d"], cfg["state_seed"])
+        adj, st = pkg.execute(strat[cfg["strategy"]](cfg), ops, s0, fast_backend)
+        for k, v in cfg["stats"].items():
+            assert getattr(st, k) == v, (cfg["key"], k)
+        ref = arrays[cfg["key"] + "_adjoint"]
+        assert L.rel_l2(np.frombuffer(adj, "<f8"), ref) <= 1e-12, cfg["key"]
+
+
+def test_fp32_batched_end_to_end_vs_reference(P, runtime_golden, fast_backend):
+    # SURVEY §8(c) protocol 2: fp32 batched adjoints vs the fp64 reference at n <= 100
+    pkg, lstm, _ = P
+    cfgs, arrays = runtime_golden
+    batch = 4096
+    for cfg in cfgs:
+        if cfg["n"] > 100:
+            continue
+        d = cfg["d"]
+        cell = lstm.random_cell(d, cfg["n"], cfg["seed"])
+        ops = lstm.operator_pair(cell, batch, "f32")
+        row = np.frombuffer(lstm.random_state(d, cfg["state_seed"]), "<f8").reshape(2, d, 1)
+        s0 = torch.from_numpy(np.repeat(row, batch, axis=2)).float().cuda().contiguous()
+        strategy = {"full": pkg.FullStorage(), "revolve": pkg.Revolve(cfg["slots"]),
+                    "multistage": pkg.Multistage(cfg["slots"], cfg["interval"])}[cfg["strategy"]]
+        adj, st = pkg.execute(strategy, ops, s0, fast_backend)
+        ref = arrays[cfg["key"] + "_adjoint"].reshape(2, d)
+        got = adj.double().cpu().numpy()
+        for b in (0, batch // 3, batch - 1):
+            assert L.rel_l2(got[:, :, b], ref) <= 1e-5, (cfg["key"], L.rel_l2(got[:, :, b], ref))
+        assert st.forward_evals == cfg["stats"]["forward_evals"]
+        assert st.peak_l1_bytes == cfg["stats"]["peak_l1_bytes"] // (2 * d * 8) * ops.state_size
+
+
+def test_fp32_strategies_bit_identical_at_long_n(P):
+    # SURVEY §8(c) protocol 3: at any n the GPU strategies agree bit for bit
+    pkg, lstm, _ = P
+    d, n, batch = 8, 400, 1 << 14
+    cell = lstm.random_cell(d, n, 0)
+    ops = lstm.operator_pair(cell, batch, "f32")
+    s0 = lstm.random_states(d, 1, batch, "f32")
+    backend = pkg.PinnedHostBackend()
+    try:
+        g_full, _ = pkg.execute(pkg.FullStorage(), ops, s0)
+        g_rev, _ = pkg.execute(pkg.Revolve(20), ops, s0)
+        g_ms, st = pkg.execute(pkg.Multistage(19, interval=20), ops, s0, backend)
+        g_fused, st_f = pkg.execute(pkg.Multistage(19, interval=20), ops, s0, backend, fuse=True)
+        g_rev_fused, _ = pkg.execute(pkg.Revolve(20), ops, s0, fuse=True)
+    finally:
+        backend.close()
+    assert torch.equal(g_full, g_rev) and torch.equal(g_full, g_ms)
+    assert torch.equal(g_full, g_fused) and torch.equal(g_full, g_rev_fused)
+    assert st.forward_evals == st_f.forward_evals == 2 * n
+    # counters and ledger equal the CPU oracle executor's
+    _, ost = RO.execute("multistage", L.random_cell(d, n, 0), np.zeros((2, d, 1)), slots=19, interval=20)
+    assert st.forward_evals == ost["forward_evals"] and st.stores_issued == ost["stores_issued"]
+    assert st.peak_l1_bytes == ost["peak_l1_bytes"] // (2 * d * 8) * ops.state_size
+
+
+def test_python_callback_operator_pair(P, fast_backend):
+    # a user-defined OperatorPair of Python callables over CUDA tensors runs
+    # through the C plugin interface with the same counters and results
+    pkg, lstm, _ = P
+    cell = lstm.random_cell(4, 10, 7)
+    dc = lstm.device_cell(cell, 1, "f64")
+    ops = pkg.OperatorPair(
+        forward_step=lambda k, s: dc.forward(k, s.view(torch.float64)),
+        backward_step=lambda k, s, a: dc.backward(k, s.view(torch.float64), a.view(torch.float64)),
+        state_size=dc.state_bytes,
+        n_steps=10,
+        adjoint_seed=lambda fin: dc.seed(fin.view(torch.float64)),
+    )
+    s0 = lstm.random_state(4, 8)
+    native = lstm.operator_pair(cell)
+    want, st_want = pkg.execute(pkg.Revolve(2), native, s0)
+    got, st_got = pkg.execute(pkg.Revolve(2), ops, s0)
+    assert got == want
+    assert st_got.forward_evals == st_want.forward_evals
+    got_ms, _ = pkg.execute(pkg.Multistage(2, interval=4), ops, s0, fast_backend)
+    assert got_ms == want
