@@ -41,7 +41,7 @@
 
 namespace ackpt {
 // tier.cpp
-void tier_reserve_keys(ackpt_tier* t, const std::vector<int64_t>& keys);
+void tier_reserve_keys(ackpt_tier* t, const std::vector<int64_t>& keys, int64_t bytes);
 cudaEvent_t tier_ticket_event(ackpt_tier* t, ackpt_ticket id);
 int tier_ticket_status(ackpt_tier* t, ackpt_ticket id, std::string* msg);
 void tier_retire(ackpt_tier* t, ackpt_ticket id);
@@ -627,7 +627,6 @@ ACKPT_API int ackpt_engine_prepare(ackpt_engine* E, int32_t strategy, int64_t sl
       // plan_multistage (schedule.py:288-329)
       if (!tier) fail(ACKPT_VALUE_ERROR, "Multistage requires a Level-2 backend");
       if (interval < 1) fail(ACKPT_VALUE_ERROR, "interval must be >= 1, got " + std::to_string(interval));
-      if (tier_slot_bytes(tier) < E->S) fail(ACKPT_SIZE_MISMATCH, "tier slots are smaller than the state");
       E->interval = interval;
       if (interval >= n) {
         E->fallback = true;
@@ -643,7 +642,7 @@ ACKPT_API int ackpt_engine_prepare(ackpt_engine* E, int32_t strategy, int64_t sl
           else revolve_actions(len, slots, seg);
           E->seg_by_len[len] = make_plan(std::move(seg));
         }
-        tier_reserve_keys(tier, E->boundaries);
+        tier_reserve_keys(tier, E->boundaries, E->S);
       }
     } else {
       fail(ACKPT_VALUE_ERROR, "unknown strategy " + std::to_string(strategy));
@@ -756,7 +755,11 @@ ACKPT_API int ackpt_engine_calibrate(ackpt_engine* E, ackpt_tier* tier, int64_t 
         ACKPT_CUDA_CHECK(cudaEventRecord(evs[size_t(2 * trials + 2 * k + 1)], s));
         ai = 1 - ai;
       }
-      // store round trips of the final state under keys 0..trials-1 (runtime.py:455-460)
+      // store round trips of the final state under keys 0..trials-1 (runtime.py:455-460);
+      // host storage for the keys is allocated first so only the copy is timed
+      std::vector<int64_t> keys;
+      for (int64_t i = 0; i < trials; ++i) keys.push_back(i);
+      tier_reserve_keys(tier, keys, E->S);
       ACKPT_CUDA_CHECK(cudaStreamSynchronize(s));
       cudaStream_t d2h = tier_d2h(tier);
       for (int64_t i = 0; i < trials; ++i) {

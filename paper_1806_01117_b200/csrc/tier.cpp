@@ -37,6 +37,8 @@ struct TierTicket {
 
 struct KeyEntry {
   int64_t slot = -1;
+  unsigned char* big = nullptr;  // dedicated pinned buffer for payloads > slot_bytes
+  int64_t big_cap = 0;
   int64_t step = 0;
   int64_t len = 0;
   cudaEvent_t last_store = nullptr;
@@ -128,18 +130,59 @@ void retire(ackpt_tier* t, TierTicket& tk) {
   }
 }
 
+unsigned char* key_ptr(const ackpt_tier* t, const KeyEntry& ke) {
+  return ke.big ? ke.big : t->slot_ptr[size_t(ke.slot)];
+}
+
+// Gives `key` host storage for `bytes`: a slab slot when it fits slot_bytes,
+// else a dedicated pinned buffer (grown on demand; pending copies on the key
+// are drained before a buffer is replaced).  Throws StorageFull.
+KeyEntry& ensure_storage(ackpt_tier* t, int64_t key, int64_t bytes) {
+  KeyEntry& ke = t->keys[key];
+  if (bytes <= t->slot_bytes) {
+    if (ke.big || ke.slot >= 0) return ke;
+    if (t->free_slots.empty()) reserve_slots(t, int64_t(t->slot_ptr.size()) + 1);
+    ke.slot = t->free_slots.back();
+    t->free_slots.pop_back();
+    return ke;
+  }
+  if (ke.big_cap < bytes) {
+    if (ke.stored) ACKPT_CUDA_CHECK(cudaEventSynchronize(ke.last_store));
+    if (ke.fetched) ACKPT_CUDA_CHECK(cudaEventSynchronize(ke.last_fetch));
+    if (ke.big) cudaFreeHost(ke.big);
+    ke.big = nullptr;
+    ke.big_cap = 0;
+    cudaError_t e = cudaHostAlloc(reinterpret_cast<void**>(&ke.big), size_t(bytes), cudaHostAllocDefault);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      ke.big = nullptr;
+      fail(ACKPT_STORAGE_FULL, std::string("pinned host allocation failed: ") + cudaGetErrorString(e));
+    }
+    ke.big_cap = bytes;
+  }
+  if (ke.slot >= 0) {
+    t->free_slots.push_back(ke.slot);
+    ke.slot = -1;
+  }
+  return ke;
+}
+
 }  // namespace
 
-// Engine-side helpers (engine.cpp).
-void tier_reserve_keys(ackpt_tier* t, const std::vector<int64_t>& keys) {
+// Engine-side helpers (engine.cpp): host storage for every key of a plan is
+// allocated at prepare time, outside the timed window.
+void tier_reserve_keys(ackpt_tier* t, const std::vector<int64_t>& keys, int64_t bytes) {
   std::lock_guard<std::mutex> lk(t->mu);
-  int64_t absent = 0;
-  for (int64_t k : keys) {
-    auto it = t->keys.find(k);
-    if (it == t->keys.end() || it->second.slot < 0) ++absent;
+  if (bytes <= t->slot_bytes) {
+    int64_t absent = 0;
+    for (int64_t k : keys) {
+      auto it = t->keys.find(k);
+      if (it == t->keys.end() || (it->second.slot < 0 && !it->second.big)) ++absent;
+    }
+    const int64_t used = int64_t(t->slot_ptr.size() - t->free_slots.size());
+    reserve_slots(t, used + absent);
   }
-  const int64_t used = int64_t(t->slot_ptr.size() - t->free_slots.size());
-  reserve_slots(t, used + absent);
+  for (int64_t k : keys) ensure_storage(t, k, bytes);
 }
 cudaEvent_t tier_ticket_event(ackpt_tier* t, ackpt_ticket id) {
   std::lock_guard<std::mutex> lk(t->mu);
@@ -192,6 +235,7 @@ ACKPT_API int ackpt_tier_destroy(ackpt_tier* t) {
     for (auto& kv : t->keys) {
       if (kv.second.last_store) cudaEventDestroy(kv.second.last_store);
       if (kv.second.last_fetch) cudaEventDestroy(kv.second.last_fetch);
+      if (kv.second.big) cudaFreeHost(kv.second.big);
     }
     if (t->after) cudaEventDestroy(t->after);
     for (auto c : t->chunks) cudaFreeHost(c);
@@ -218,40 +262,25 @@ ACKPT_API int ackpt_tier_begin_store(ackpt_tier* t, int64_t key, int64_t step, c
     tk.kind = 0;
     tk.key = key;
     tk.step = step;
-    if (bytes < 0 || bytes > t->slot_bytes) {
-      tk.err = ACKPT_SIZE_MISMATCH;
-      tk.msg = "payload is " + std::to_string(bytes) + " bytes, tier slots hold " +
-               std::to_string(t->slot_bytes);
+    if (bytes < 0) ackpt::fail(ACKPT_VALUE_ERROR, "bytes must be >= 0");
+    ackpt::KeyEntry* kp = nullptr;
+    try {
+      kp = &ackpt::ensure_storage(t, key, bytes);
+    } catch (const ackpt::Error& e) {  // surfaced at wait (storage.py:271-278)
+      tk.err = e.code;
+      tk.msg = e.what();
       tk.complete = true;
       *out = ackpt::add_ticket(t, std::move(tk));
       return;
     }
-    auto it = t->keys.find(key);
-    if (it == t->keys.end() || it->second.slot < 0) {
-      if (t->free_slots.empty()) {
-        try {
-          ackpt::reserve_slots(t, int64_t(t->slot_ptr.size()) + 1);
-        } catch (const ackpt::Error& e) {
-          tk.err = e.code;
-          tk.msg = e.what();
-          tk.complete = true;
-          *out = ackpt::add_ticket(t, std::move(tk));
-          return;
-        }
-      }
-      ackpt::KeyEntry& ke = t->keys[key];
-      ke.slot = t->free_slots.back();
-      t->free_slots.pop_back();
-      it = t->keys.find(key);
-    }
-    ackpt::KeyEntry& ke = it->second;
+    ackpt::KeyEntry& ke = *kp;
     if (after_stream) {
       ACKPT_CUDA_CHECK(cudaEventRecord(t->after, static_cast<cudaStream_t>(after_stream)));
       ACKPT_CUDA_CHECK(cudaStreamWaitEvent(t->d2h, t->after, 0));
     }
     if (ke.fetched) ACKPT_CUDA_CHECK(cudaStreamWaitEvent(t->d2h, ke.last_fetch, 0));
     if (bytes > 0)
-      ACKPT_CUDA_CHECK(cudaMemcpyAsync(t->slot_ptr[size_t(ke.slot)], src, size_t(bytes),
+      ACKPT_CUDA_CHECK(cudaMemcpyAsync(ackpt::key_ptr(t, ke), src, size_t(bytes),
                                        cudaMemcpyDeviceToHost, t->d2h));
     ke.step = step;
     ke.len = bytes;
@@ -298,7 +327,7 @@ ACKPT_API int ackpt_tier_begin_fetch(ackpt_tier* t, int64_t key, void* dst, int6
     }
     ACKPT_CUDA_CHECK(cudaStreamWaitEvent(t->h2d, ke.last_store, 0));
     if (ke.len > 0)
-      ACKPT_CUDA_CHECK(cudaMemcpyAsync(dst, t->slot_ptr[size_t(ke.slot)], size_t(ke.len),
+      ACKPT_CUDA_CHECK(cudaMemcpyAsync(dst, ackpt::key_ptr(t, ke), size_t(ke.len),
                                        cudaMemcpyHostToDevice, t->h2d));
     ackpt_ticket id = ackpt::add_ticket(t, std::move(tk));
     ackpt::TierTicket& ref = t->tickets[size_t(id)];
@@ -381,7 +410,7 @@ ACKPT_API int ackpt_tier_host_ptr(ackpt_tier* t, int64_t key, void** out) {
     auto it = t->keys.find(key);
     if (it == t->keys.end() || !it->second.stored)
       ackpt::fail(ACKPT_MISSING_KEY, "key " + std::to_string(key) + " never stored");
-    *out = t->slot_ptr[size_t(it->second.slot)];
+    *out = ackpt::key_ptr(t, it->second);
   });
 }
 
@@ -392,6 +421,7 @@ ACKPT_API int ackpt_tier_clear(ackpt_tier* t) {
     std::lock_guard<std::mutex> lk(t->mu);
     for (auto& kv : t->keys) {
       if (kv.second.slot >= 0) t->free_slots.push_back(kv.second.slot);
+      if (kv.second.big) cudaFreeHost(kv.second.big);
       if (kv.second.last_store) cudaEventDestroy(kv.second.last_store);
       if (kv.second.last_fetch) cudaEventDestroy(kv.second.last_fetch);
     }

@@ -257,8 +257,7 @@ class Level2Backend:
             self._slot_bytes = size
             if self._latency or self._bandwidth:
                 N.check(N.lib.ackpt_tier_set_throttle(self._handle, float(self._latency), float(self._bandwidth)))
-        elif nbytes > self._slot_bytes:
-            raise SizeMismatch(f"payload of {nbytes} bytes exceeds tier slots of {self._slot_bytes}")
+        # payloads larger than the slab slots get dedicated pinned buffers per key
         return self._handle
 
     @property
