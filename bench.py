@@ -52,7 +52,8 @@ def parse_args(argv=None):
     p.add_argument("--no-revolve", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
-    p.add_argument("--sample-every", type=int, default=8)
+    p.add_argument("--sample-every", type=int, default=64,
+                   help="event-pair timing of every k-th launch (sparse: each pair perturbs the stream)")
     return p.parse_args(argv)
 
 

@@ -217,6 +217,7 @@ typedef struct ackpt_stats {
   int64_t fwd_samples;
   double bwd_sample_seconds;
   int64_t bwd_samples;
+  double host_enqueue_seconds; /* host time to enqueue the whole run */
 } ackpt_stats;
 
 typedef struct ackpt_engine ackpt_engine;

@@ -80,6 +80,7 @@ class Stats(C.Structure):
         ("fwd_samples", C.c_int64),
         ("bwd_sample_seconds", C.c_double),
         ("bwd_samples", C.c_int64),
+        ("host_enqueue_seconds", C.c_double),
     ]
 
 

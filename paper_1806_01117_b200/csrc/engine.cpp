@@ -518,6 +518,7 @@ void run_impl(ackpt_engine* E, Mode mode, const void* initial_state, const void*
   }
 
   ACKPT_CUDA_CHECK(cudaEventRecord(E->ev_end, E->compute));
+  const auto t_enq = std::chrono::steady_clock::now();
   ACKPT_CUDA_CHECK(cudaEventSynchronize(E->ev_end));
   const auto t1 = std::chrono::steady_clock::now();
   ACKPT_CUDA_CHECK(cudaStreamWaitEvent(caller, E->ev_end, 0));
@@ -526,6 +527,7 @@ void run_impl(ackpt_engine* E, Mode mode, const void* initial_state, const void*
 
   r.finish_stats();
   r.st.wall_seconds = std::chrono::duration<double>(t1 - t0).count();
+  r.st.host_enqueue_seconds = std::chrono::duration<double>(t_enq - t0).count();
   float ms_gpu = 0.f;
   ACKPT_CUDA_CHECK(cudaEventElapsedTime(&ms_gpu, E->ev_start, E->ev_end));
   r.st.gpu_seconds = double(ms_gpu) * 1e-3;

@@ -125,6 +125,7 @@ def _stats_from(st: N.Stats) -> ExecutionStats:
         "fwd_samples": st.fwd_samples,
         "bwd_sample_seconds": st.bwd_sample_seconds,
         "bwd_samples": st.bwd_samples,
+        "host_enqueue_seconds": st.host_enqueue_seconds,
     }
     return out
 
