@@ -2,6 +2,7 @@
 #include "lstm_cell.h"
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -32,6 +33,30 @@ bool f32_fast(const ackpt_lstm* c, std::initializer_list<const void*> ptrs) {
   if (c->dtype != ACKPT_F32 || (c->d != 4 && c->d != 8) || (c->B & 1)) return false;
   for (const void* p : ptrs)
     if (reinterpret_cast<uintptr_t>(p) & 7u) return false;
+  return true;
+}
+
+// Kernel family for the d=8 fp32 fast path.  Default: the TMA-pipelined
+// persistent kernels; ACKPT_KERNEL_VARIANT=ldg selects the register-staged
+// kernels, tma128 / tma_bwd2 other pipeline shapes (for A/B measurements).
+enum class Variant { kTma, kLdg, kTma128, kTmaBwd2 };
+Variant variant() {
+  static const Variant v = [] {
+    const char* e = std::getenv("ACKPT_KERNEL_VARIANT");
+    std::string s = e ? e : "tma";
+    if (s == "ldg") return Variant::kLdg;
+    if (s == "tma128") return Variant::kTma128;
+    if (s == "tma_bwd2") return Variant::kTmaBwd2;
+    return Variant::kTma;
+  }();
+  return v;
+}
+
+// TMA path: d=8, B % 4 == 0 (16-byte row segments), 16-byte aligned rows.
+bool tma_ok(const ackpt_lstm* c, std::initializer_list<const void*> ptrs) {
+  if (c->dtype != ACKPT_F32 || c->d != 8 || (c->B & 3) || variant() == Variant::kLdg) return false;
+  for (const void* p : ptrs)
+    if (reinterpret_cast<uintptr_t>(p) & 15u) return false;
   return true;
 }
 
@@ -125,7 +150,12 @@ ACKPT_API int ackpt_lstm_forward(const ackpt_lstm* cell, int64_t step, const voi
   return ackpt::guard([&] {
     ackpt::check_step(cell, step);
     auto s = static_cast<cudaStream_t>(stream);
-    if (ackpt::f32_fast(cell, {state_in, state_out})) {
+    if (ackpt::tma_ok(cell, {state_in, state_out})) {
+      auto i = static_cast<const float*>(state_in);
+      auto o = static_cast<float*>(state_out);
+      if (ackpt::variant() == ackpt::Variant::kTma128) ackpt::tma_launch<8, 0, 128, 4>(cell, step, i, nullptr, o, s);
+      else ackpt::tma_launch<8, 0, 256, 3>(cell, step, i, nullptr, o, s);
+    } else if (ackpt::f32_fast(cell, {state_in, state_out})) {
       auto i = static_cast<const float*>(state_in);
       auto o = static_cast<float*>(state_out);
       if (cell->d == 8) ackpt::f32_forward<8>(cell, step, i, o, s);
@@ -169,7 +199,16 @@ ACKPT_API int ackpt_lstm_backward(const ackpt_lstm* cell, int64_t step, const vo
   return ackpt::guard([&] {
     ackpt::check_step(cell, step);
     auto s = static_cast<cudaStream_t>(stream);
-    if (ackpt::f32_fast(cell, {state, adjoint_in, adjoint_out})) {
+    if (ackpt::tma_ok(cell, {state, adjoint_in, adjoint_out})) {
+      auto x = static_cast<const float*>(state);
+      auto a = static_cast<const float*>(adjoint_in);
+      auto o = static_cast<float*>(adjoint_out);
+      switch (ackpt::variant()) {
+        case ackpt::Variant::kTma128: ackpt::tma_launch<8, 1, 128, 3>(cell, step, x, a, o, s); break;
+        case ackpt::Variant::kTmaBwd2: ackpt::tma_launch<8, 1, 256, 2>(cell, step, x, a, o, s); break;
+        default: ackpt::tma_launch<8, 1, 256, 3>(cell, step, x, a, o, s);
+      }
+    } else if (ackpt::f32_fast(cell, {state, adjoint_in, adjoint_out})) {
       auto x = static_cast<const float*>(state);
       auto a = static_cast<const float*>(adjoint_in);
       auto o = static_cast<float*>(adjoint_out);

@@ -46,6 +46,11 @@ template <int D>
 void f32_advance(const ackpt_lstm* c, int64_t from, int64_t to, const float* in, float* out,
                  cudaStream_t s);
 
+// TMA-pipelined persistent fp32 kernels (lstm_f32_tma_d*.cu); MODE 0 = fwd, 1 = bwd.
+template <int D, int MODE, int THREADS, int STAGES>
+void tma_launch(const ackpt_lstm* c, int64_t step, const float* x, const float* a, float* y,
+                cudaStream_t s);
+
 // Generic path, any d <= 128, f32 or f64 (lstm_generic.cu).
 template <typename T>
 void generic_forward(const ackpt_lstm* c, int64_t step, const T* in, T* out, cudaStream_t s);

@@ -33,7 +33,12 @@ def _states(d, seed, batch, scale=1.0):
     return rng.uniform(-scale, scale, (2, d, batch))
 
 
-@pytest.mark.parametrize("d,batch", [(8, 4096), (8, 2), (4, 1024), (8, 1001), (5, 64), (16, 300), (32, 17)])
+@pytest.mark.parametrize(
+    "d,batch",
+    # 4096/4100/516: TMA tiles (full, partial last tile, tiny); 2/1002: float2
+    # kernels; odd B and other d: generic kernels
+    [(8, 4096), (8, 4100), (8, 516), (8, 2), (8, 1002), (4, 1024), (8, 1001), (5, 64), (16, 300), (32, 17)],
+)
 def test_forward_backward_f32_vs_oracle(P, d, batch):
     cell, ocell = _cells(P, d, 6, 11 + d)
     x = _states(d, 3, batch).astype(np.float32)

@@ -68,7 +68,7 @@ def launches(path, out):
         name = r[hdr.index("Kernel Name")].split("(")[0]
         val = float(r[hdr.index("Metric Value")].replace(",", ""))
         unit = r[hdr.index("Metric Unit")]
-        scale = {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3}.get(unit, 1.0)
+        scale = {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3}.get(unit, 1.0)
         agg[name][0] += 1
         agg[name][1] += val * scale
     total = sum(v[1] for v in agg.values())
