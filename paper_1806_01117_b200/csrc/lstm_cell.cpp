@@ -36,25 +36,28 @@ bool f32_fast(const ackpt_lstm* c, std::initializer_list<const void*> ptrs) {
   return true;
 }
 
-// Kernel family for the d=8 fp32 fast path.  Default: the TMA-pipelined
-// persistent kernels; ACKPT_KERNEL_VARIANT=ldg selects the register-staged
-// kernels, tma128 / tma_bwd2 other pipeline shapes (for A/B measurements).
-enum class Variant { kTma, kLdg, kTma128, kTmaBwd2 };
+// Kernel family for the d=8 fp32 fast path (all variants compute identical
+// bits).  ACKPT_KERNEL_VARIANT: ldg (register-staged, 2 CTAs/SM, default),
+// ldg3 (3 CTAs/SM), tma / tma128 / tma_bwd2 (bulk-copy smem pipelines).
+enum class Variant { kLdg, kLdg3, kTma, kTma128, kTmaBwd2 };
 Variant variant() {
   static const Variant v = [] {
     const char* e = std::getenv("ACKPT_KERNEL_VARIANT");
-    std::string s = e ? e : "tma";
-    if (s == "ldg") return Variant::kLdg;
+    std::string s = e ? e : "ldg";
+    if (s == "ldg3") return Variant::kLdg3;
+    if (s == "tma") return Variant::kTma;
     if (s == "tma128") return Variant::kTma128;
     if (s == "tma_bwd2") return Variant::kTmaBwd2;
-    return Variant::kTma;
+    return Variant::kLdg;
   }();
   return v;
 }
 
 // TMA path: d=8, B % 4 == 0 (16-byte row segments), 16-byte aligned rows.
 bool tma_ok(const ackpt_lstm* c, std::initializer_list<const void*> ptrs) {
-  if (c->dtype != ACKPT_F32 || c->d != 8 || (c->B & 3) || variant() == Variant::kLdg) return false;
+  const Variant v = variant();
+  if (v == Variant::kLdg || v == Variant::kLdg3) return false;
+  if (c->dtype != ACKPT_F32 || c->d != 8 || (c->B & 3)) return false;
   for (const void* p : ptrs)
     if (reinterpret_cast<uintptr_t>(p) & 15u) return false;
   return true;
@@ -128,6 +131,20 @@ ACKPT_API int ackpt_lstm_create(int32_t d, int64_t n_steps, int64_t batch, int32
     ACKPT_CUDA_CHECK(cudaMalloc(&c->d_xb, c->xb_t.size()));
     ACKPT_CUDA_CHECK(cudaMemcpy(c->d_wh, c->wh_t.data(), c->wh_t.size(), cudaMemcpyHostToDevice));
     ACKPT_CUDA_CHECK(cudaMemcpy(c->d_xb, c->xb_t.data(), c->xb_t.size(), cudaMemcpyHostToDevice));
+    if (dtype == ACKPT_F32 && d <= 16) {
+      // per-gate pre-scaled projections for the fused fp32 advance (lstm_f32_math.cuh)
+      const float scale[4] = {-1.4426950408889634f, -1.4426950408889634f, -1.4426950408889634f,
+                              2.0f * 1.4426950408889634f};
+      std::vector<float> xbs(c->xb64.size());
+      for (int64_t k = 0; k < n_steps; ++k)
+        for (size_t g = 0; g < 4; ++g)
+          for (size_t j = 0; j < D; ++j) {
+            const size_t at = (size_t(k) * 4 + g) * D + j;
+            xbs[at] = float(c->xb64[at] * double(scale[g]));
+          }
+      ACKPT_CUDA_CHECK(cudaMalloc(&c->d_xbs, xbs.size() * sizeof(float)));
+      ACKPT_CUDA_CHECK(cudaMemcpy(c->d_xbs, xbs.data(), xbs.size() * sizeof(float), cudaMemcpyHostToDevice));
+    }
     *out = c.release();
   });
 }
@@ -137,6 +154,7 @@ ACKPT_API int ackpt_lstm_destroy(ackpt_lstm* cell) {
     if (!cell) return;
     if (cell->d_wh) cudaFree(cell->d_wh);
     if (cell->d_xb) cudaFree(cell->d_xb);
+    if (cell->d_xbs) cudaFree(cell->d_xbs);
     delete cell;
   });
 }
@@ -158,8 +176,12 @@ ACKPT_API int ackpt_lstm_forward(const ackpt_lstm* cell, int64_t step, const voi
     } else if (ackpt::f32_fast(cell, {state_in, state_out})) {
       auto i = static_cast<const float*>(state_in);
       auto o = static_cast<float*>(state_out);
-      if (cell->d == 8) ackpt::f32_forward<8>(cell, step, i, o, s);
-      else ackpt::f32_forward<4>(cell, step, i, o, s);
+      if (cell->d == 8) {
+        if (ackpt::variant() == ackpt::Variant::kLdg3) ackpt::f32_forward_v<8, 3>(cell, step, i, o, s);
+        else ackpt::f32_forward<8>(cell, step, i, o, s);
+      } else {
+        ackpt::f32_forward<4>(cell, step, i, o, s);
+      }
     } else if (cell->dtype == ACKPT_F32) {
       ackpt::generic_forward<float>(cell, step, static_cast<const float*>(state_in),
                                     static_cast<float*>(state_out), s);
@@ -212,8 +234,12 @@ ACKPT_API int ackpt_lstm_backward(const ackpt_lstm* cell, int64_t step, const vo
       auto x = static_cast<const float*>(state);
       auto a = static_cast<const float*>(adjoint_in);
       auto o = static_cast<float*>(adjoint_out);
-      if (cell->d == 8) ackpt::f32_backward<8>(cell, step, x, a, o, s);
-      else ackpt::f32_backward<4>(cell, step, x, a, o, s);
+      if (cell->d == 8) {
+        if (ackpt::variant() == ackpt::Variant::kLdg3) ackpt::f32_backward_v<8, 3>(cell, step, x, a, o, s);
+        else ackpt::f32_backward<8>(cell, step, x, a, o, s);
+      } else {
+        ackpt::f32_backward<4>(cell, step, x, a, o, s);
+      }
     } else if (cell->dtype == ACKPT_F32) {
       ackpt::generic_backward<float>(cell, step, static_cast<const float*>(state),
                                      static_cast<const float*>(adjoint_in),

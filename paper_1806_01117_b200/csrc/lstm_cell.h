@@ -18,6 +18,7 @@ struct ackpt_lstm {
   std::vector<unsigned char> wh_t, xb_t, target_t;  // rounded to the cell dtype
   void* d_wh = nullptr;                             // 4 x d x d, dtype
   void* d_xb = nullptr;                             // n x 4 x d, dtype
+  void* d_xbs = nullptr;  // n x 4 x d fp32, pre-scaled per gate (fp32 fast path, d <= 16)
 };
 
 namespace ackpt {
@@ -45,6 +46,12 @@ void f32_backward(const ackpt_lstm* c, int64_t step, const float* st, const floa
 template <int D>
 void f32_advance(const ackpt_lstm* c, int64_t from, int64_t to, const float* in, float* out,
                  cudaStream_t s);
+// Occupancy variants (MINB resident 256-thread CTAs per SM).
+template <int D, int MINB>
+void f32_forward_v(const ackpt_lstm* c, int64_t step, const float* in, float* out, cudaStream_t s);
+template <int D, int MINB>
+void f32_backward_v(const ackpt_lstm* c, int64_t step, const float* st, const float* ai, float* ao,
+                    cudaStream_t s);
 
 // TMA-pipelined persistent fp32 kernels (lstm_f32_tma_d*.cu); MODE 0 = fwd, 1 = bwd.
 template <int D, int MODE, int THREADS, int STAGES>

@@ -1,0 +1,152 @@
+// Packed-fp32 (f32x2) math shared by the fp32 LSTM step kernels.
+//
+// The gate activations are computed from PRE-SCALED accumulators: the
+// weights and input projections are multiplied on the host by
+// -log2(e) (gates f, i, o) or +2 log2(e) (gate g), so an accumulator is
+// directly the argument of ex2:
+//   sigmoid(a) = 1 / (1 + 2^(-log2e a)),   tanh(a) = 1 - 2 / (1 + 2^(2 log2e a)).
+// The four activations of a hidden unit share ONE reciprocal on the MUFU
+// pipe: 1/y_f = (y_i y_o y_g) / (y_f y_i y_o y_g).  If the product overflows
+// (pre-activations beyond ~22) a branch computes separate reciprocals, which
+// is exact there because rcp(inf) = 0.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstring>
+
+#include "lstm_cell.h"
+
+namespace ackpt {
+namespace f32m {
+
+constexpr float kL2e = 1.4426950408889634f;
+constexpr float kLn2 = 0.69314718055994531f;
+// per-gate exponent scales (f, i, o, c) and their inverses
+constexpr float kScale[4] = {-kL2e, -kL2e, -kL2e, 2.0f * kL2e};
+
+union P2 {
+  float2 f;
+  unsigned long long u;
+};
+__device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) {
+  P2 x{a}, y{b}, z{c}, r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r.u) : "l"(x.u), "l"(y.u), "l"(z.u));
+  return r.f;
+}
+__device__ __forceinline__ float2 mul2(float2 a, float2 b) {
+  P2 x{a}, y{b}, r;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r.u) : "l"(x.u), "l"(y.u));
+  return r.f;
+}
+__device__ __forceinline__ float2 add2(float2 a, float2 b) {
+  P2 x{a}, y{b}, r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r.u) : "l"(x.u), "l"(y.u));
+  return r.f;
+}
+__device__ __forceinline__ float2 bc(float s) { return make_float2(s, s); }
+__device__ __forceinline__ float2 neg(float2 a) { return make_float2(-a.x, -a.y); }
+__device__ __forceinline__ float ex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float rcp(float x) {
+  float y;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float2 ex2_2(float2 t) { return make_float2(ex2(t.x), ex2(t.y)); }
+__device__ __forceinline__ float2 rcp2(float2 y) { return make_float2(rcp(y.x), rcp(y.y)); }
+
+__device__ __forceinline__ void activate(float2 tf, float2 ti, float2 to, float2 tg, float2& f,
+                                         float2& i, float2& o, float2& g) {
+  const float2 one = bc(1.0f);
+  const float2 yf = add2(ex2_2(tf), one), yi = add2(ex2_2(ti), one);
+  const float2 yo = add2(ex2_2(to), one), yg = add2(ex2_2(tg), one);
+  const float2 p12 = mul2(yf, yi), p34 = mul2(yo, yg);
+  const float2 P = mul2(p12, p34);
+  if (__builtin_expect(P.x <= 3.0e38f && P.y <= 3.0e38f, 1)) {
+    const float2 r = rcp2(P);
+    const float2 q34 = mul2(r, p34), q12 = mul2(r, p12);
+    f = mul2(q34, yi);
+    i = mul2(q34, yf);
+    o = mul2(q12, yg);
+    g = fma2(mul2(q12, yo), bc(-2.0f), one);
+  } else {
+    f = rcp2(yf);
+    i = rcp2(yi);
+    o = rcp2(yo);
+    g = fma2(rcp2(yg), bc(-2.0f), one);
+  }
+}
+
+__device__ __forceinline__ float2 tanh2(float2 x) {
+  const float2 y = add2(ex2_2(mul2(x, bc(2.0f * kL2e))), bc(1.0f));
+  return fma2(rcp2(y), bc(-2.0f), bc(1.0f));
+}
+
+// Weights pre-scaled per gate (see file comment).
+template <int D>
+struct ScaledParams {
+  float ws[4][D][D];
+  float xbs[4][D];
+};
+
+template <int D>
+inline void fill_scaled(const ackpt_lstm* c, int64_t step, ScaledParams<D>& p) {
+  for (int g = 0; g < 4; ++g)
+    for (int j = 0; j < D; ++j) {
+      for (int k = 0; k < D; ++k)
+        p.ws[g][j][k] = float(c->wh64[(size_t(g) * D + j) * D + k] * double(kScale[g]));
+      p.xbs[g][j] = step >= 0 ? float(c->xb64[(size_t(step) * 4 + g) * D + j] * double(kScale[g])) : 0.0f;
+    }
+}
+
+// Pre-activations of unit j (scaled) for one pair, from h and scaled xb.
+template <int D>
+__device__ __forceinline__ void preacts(const float (&ws)[4][D][D], const float (&xbs)[4][D],
+                                        const float2 (&h)[D], int j, float2& af, float2& ai,
+                                        float2& ao, float2& ag) {
+  af = bc(xbs[0][j]);
+  ai = bc(xbs[1][j]);
+  ao = bc(xbs[2][j]);
+  ag = bc(xbs[3][j]);
+#pragma unroll
+  for (int k = 0; k < D; ++k) {
+    af = fma2(bc(ws[0][j][k]), h[k], af);
+    ai = fma2(bc(ws[1][j][k]), h[k], ai);
+    ao = fma2(bc(ws[2][j][k]), h[k], ao);
+    ag = fma2(bc(ws[3][j][k]), h[k], ag);
+  }
+}
+
+// Forward of unit j: c <- f c + i g, returns h' = o tanh(c')   (lstm.py:127-128)
+__device__ __forceinline__ float2 fwd_unit(float2 af, float2 ai, float2 ao, float2 ag, float2& c) {
+  float2 f, ig, o, g;
+  activate(af, ai, ao, ag, f, ig, o, g);
+  c = fma2(f, c, mul2(ig, g));
+  return mul2(o, tanh2(c));
+}
+
+// Adjoint of unit j (lstm.py:141-151).  Returns the four scaled gate
+// adjoints da_g / scale_g (so that sum_g (scale_g W_g)^T (da_g / scale_g) =
+// W^T da) and dc_k in dco_f.
+__device__ __forceinline__ void bwd_unit(float2 af, float2 ai, float2 ao, float2 ag, float2 c,
+                                         float2 dhn, float2 dcn, float2& daf, float2& dai,
+                                         float2& dao, float2& dag, float2& dck) {
+  float2 f, ig, o, g;
+  activate(af, ai, ao, ag, f, ig, o, g);
+  const float2 cn = fma2(f, c, mul2(ig, g));
+  const float2 t = tanh2(cn);
+  const float2 dco = fma2(mul2(dhn, o), fma2(neg(t), t, bc(1.0f)), dcn);  // :143
+  const float2 dcs = mul2(dco, bc(-kLn2));
+  daf = mul2(mul2(dcs, c), fma2(neg(f), f, f));                               // :144
+  dai = mul2(mul2(dcs, g), fma2(neg(ig), ig, ig));                            // :145
+  dao = mul2(mul2(dhn, mul2(t, bc(-kLn2))), fma2(neg(o), o, o));             // :142, :146
+  dag = mul2(mul2(dco, mul2(ig, bc(0.5f * kLn2))), fma2(neg(g), g, bc(1.0f)));  // :147
+  dck = mul2(dco, f);                                                          // :151
+}
+
+}  // namespace f32m
+}  // namespace ackpt

@@ -1,5 +1,6 @@
 // fp32 LSTM step kernels, TMA-pipelined persistent variant (K1 forward, K2
-// adjoint) for sm_100a.  Same arithmetic contract as lstm.py:110-152.
+// adjoint) for sm_100a.  Same arithmetic as lstm_f32.cuh (shared helpers in
+// lstm_f32_math.cuh), so both variants give bit-identical results.
 //
 // Data movement.  A tile is TILE = 2*THREADS consecutive batch elements.  Its
 // input rows (h, c [, dh, dc]) are TILE*4-byte contiguous segments of the
@@ -8,28 +9,18 @@
 // slots complete on an mbarrier (expect_tx).  Each thread reads its float2
 // pair with LDS.64 (conflict-free), computes, writes its results back into
 // the same smem slots, and the tile leaves with bulk stores (smem -> global).
-// Memory requests therefore do not depend on registers or occupancy: the ring
-// keeps STAGES-1 tiles in flight per CTA while the warps compute.
-//
-// Arithmetic per element (d=8): the recurrent matvec is d*d*2 FFMA2 with
-// weights broadcast from uniform registers; the exponent scales of the gate
-// activations are pre-folded into the weights (-log2e for f, i, o; +2 log2e
-// for g), so each accumulator is directly the ex2 argument; the four
-// activations of a hidden unit share one MUFU reciprocal (1/y_f = y_i y_o y_g
-// / (y_f y_i y_o y_g)), with a branch to separate reciprocals only when that
-// product overflows (pre-activations beyond ~22).
+// Memory requests do not depend on registers or occupancy: the ring keeps
+// STAGES-1 tiles in flight per CTA while the warps compute.
 #pragma once
 
 #include <cuda_runtime.h>
 
-#include <cstring>
-
-#include "lstm_cell.h"
+#include "lstm_f32_math.cuh"
 
 namespace ackpt {
 namespace tma {
 
-constexpr float kL2e = 1.4426950408889634f;
+using namespace f32m;
 
 // ---------------------------------------------------------------- PTX helpers
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -76,97 +67,21 @@ __device__ __forceinline__ void fence_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 
-// ------------------------------------------------------------ packed fp32 math
-union P2 {
-  float2 f;
-  unsigned long long u;
-};
-__device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) {
-  P2 x{a}, y{b}, z{c}, r;
-  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r.u) : "l"(x.u), "l"(y.u), "l"(z.u));
-  return r.f;
-}
-__device__ __forceinline__ float2 mul2(float2 a, float2 b) {
-  P2 x{a}, y{b}, r;
-  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r.u) : "l"(x.u), "l"(y.u));
-  return r.f;
-}
-__device__ __forceinline__ float2 add2(float2 a, float2 b) {
-  P2 x{a}, y{b}, r;
-  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r.u) : "l"(x.u), "l"(y.u));
-  return r.f;
-}
-__device__ __forceinline__ float2 bc(float s) { return make_float2(s, s); }
-__device__ __forceinline__ float2 neg(float2 a) { return make_float2(-a.x, -a.y); }
-__device__ __forceinline__ float ex2(float x) {
-  float y;
-  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
-  return y;
-}
-__device__ __forceinline__ float rcp(float x) {
-  float y;
-  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
-  return y;
-}
-__device__ __forceinline__ float2 ex2_2(float2 t) { return make_float2(ex2(t.x), ex2(t.y)); }
-__device__ __forceinline__ float2 rcp2(float2 y) { return make_float2(rcp(y.x), rcp(y.y)); }
-
-// Activations of one hidden unit from pre-scaled accumulators:
-// tf = -log2e a_f, ti = -log2e a_i, to = -log2e a_o, tg = 2 log2e a_g.
-__device__ __forceinline__ void activate(float2 tf, float2 ti, float2 to, float2 tg, float2& f,
-                                         float2& i, float2& o, float2& g) {
-  const float2 one = bc(1.0f);
-  const float2 yf = add2(ex2_2(tf), one), yi = add2(ex2_2(ti), one);
-  const float2 yo = add2(ex2_2(to), one), yg = add2(ex2_2(tg), one);
-  const float2 p12 = mul2(yf, yi), p34 = mul2(yo, yg);
-  const float2 P = mul2(p12, p34);
-  if (__builtin_expect(P.x <= 3.0e38f && P.y <= 3.0e38f, 1)) {
-    const float2 r = rcp2(P);
-    const float2 q34 = mul2(r, p34), q12 = mul2(r, p12);
-    f = mul2(q34, yi);
-    i = mul2(q34, yf);
-    o = mul2(q12, yg);
-    g = fma2(mul2(q12, yo), bc(-2.0f), one);
-  } else {  // a product overflowed: separate reciprocals (1/inf = 0 is exact here)
-    f = rcp2(yf);
-    i = rcp2(yi);
-    o = rcp2(yo);
-    g = fma2(rcp2(yg), bc(-2.0f), one);
-  }
-}
-// tanh(x) = 1 - 2 / (1 + e^{2x})
-__device__ __forceinline__ float2 tanh2(float2 x) {
-  const float2 y = add2(ex2_2(mul2(x, bc(2.0f * kL2e))), bc(1.0f));
-  return fma2(rcp2(y), bc(-2.0f), bc(1.0f));
-}
-
-// Pre-scaled weights: ws[g][j][i] = scale_g W_g[j][i], xbs[g][j] = scale_g xb[g][j].
-template <int D>
-struct ScaledParams {
-  float ws[4][D][D];
-  float xbs[4][D];
-};
-
-constexpr float kScale[4] = {-kL2e, -kL2e, -kL2e, 2.0f * kL2e};
-
-// ------------------------------------------------------------------- kernels
 enum Mode { kFwd = 0, kBwd = 1 };
 
 template <int D, int MODE, int THREADS>
 struct Geometry {
-  static constexpr int kTile = 2 * THREADS;                       // elements per tile
-  static constexpr int kRows = MODE == kFwd ? 2 * D : 4 * D;      // input rows
-  static constexpr int kRowBytes = kTile * 4;
+  static constexpr int kTile = 2 * THREADS;                   // elements per tile
+  static constexpr int kRows = MODE == kFwd ? 2 * D : 4 * D;  // input rows
   static constexpr int kStageFloats = kRows * kTile;
   static constexpr int kStageBytes = kStageFloats * 4;
 };
 
 // grid: persistent; tile t = blockIdx.x + k * gridDim.x.
 // x: state (2D rows of B), a: adjoint in (2D rows, bwd only), y: output (2D rows).
-// Pipeline per CTA: the prologue loads tiles 0..STAGES-2; iteration i waits
-// for tile i, computes it in place, bulk-stores it, then refills the stage of
-// tile i-1 (whose store has been reading smem for one iteration) with tile
-// i+STAGES-1.
+// Per CTA: the prologue loads tiles 0..STAGES-2; iteration i waits for tile
+// i, computes it in place, bulk-stores it, then refills the stage of tile i-1
+// (whose store has been reading smem for one iteration) with tile i+STAGES-1.
 template <int D, int MODE, int THREADS, int STAGES>
 __global__ void __launch_bounds__(THREADS, MODE == kFwd ? 2 : 1)
     step_kernel(const float* __restrict__ x, const float* __restrict__ a, float* __restrict__ y,
@@ -222,56 +137,29 @@ __global__ void __launch_bounds__(THREADS, MODE == kFwd ? 2 : 1)
       float2 hn[D];
 #pragma unroll
       for (int j = 0; j < D; ++j) {
-        float2 af = bc(p.xbs[0][j]), ai = bc(p.xbs[1][j]), ao = bc(p.xbs[2][j]), ag = bc(p.xbs[3][j]);
-#pragma unroll
-        for (int k = 0; k < D; ++k) {
-          af = fma2(bc(p.ws[0][j][k]), h[k], af);
-          ai = fma2(bc(p.ws[1][j][k]), h[k], ai);
-          ao = fma2(bc(p.ws[2][j][k]), h[k], ao);
-          ag = fma2(bc(p.ws[3][j][k]), h[k], ag);
-        }
-        float2 f, ig, o, g;
-        activate(af, ai, ao, ag, f, ig, o, g);
+        float2 af, ai, ao, ag;
+        preacts<D>(p.ws, p.xbs, h, j, af, ai, ao, ag);
         float2* cslot = st2 + (D + j) * kHalf + tid;
-        const float2 cn = fma2(f, *cslot, mul2(ig, g));  // c' = f c + i g   (lstm.py:127)
-        *cslot = cn;
-        hn[j] = mul2(o, tanh2(cn));                      // h' = o tanh(c')  (lstm.py:128)
+        float2 c = *cslot;
+        hn[j] = fwd_unit(af, ai, ao, ag, c);
+        *cslot = c;
       }
 #pragma unroll
       for (int j = 0; j < D; ++j) st2[j * kHalf + tid] = hn[j];
     } else {
-      constexpr float kLn2 = 0.69314718055994531f;
       float2 acc[D];
 #pragma unroll
       for (int m = 0; m < D; ++m) acc[m] = bc(0.0f);
 #pragma unroll
       for (int j = 0; j < D; ++j) {
-        float2 af = bc(p.xbs[0][j]), ai = bc(p.xbs[1][j]), ao = bc(p.xbs[2][j]), ag = bc(p.xbs[3][j]);
-#pragma unroll
-        for (int k = 0; k < D; ++k) {
-          af = fma2(bc(p.ws[0][j][k]), h[k], af);
-          ai = fma2(bc(p.ws[1][j][k]), h[k], ai);
-          ao = fma2(bc(p.ws[2][j][k]), h[k], ao);
-          ag = fma2(bc(p.ws[3][j][k]), h[k], ag);
-        }
-        float2 f, ig, o, g;
-        activate(af, ai, ao, ag, f, ig, o, g);
+        float2 af, ai, ao, ag, daf, dai, dao, dag, dck;
+        preacts<D>(p.ws, p.xbs, h, j, af, ai, ao, ag);
         float2* cslot = st2 + (D + j) * kHalf + tid;
-        const float2 c = *cslot;
-        const float2 dhn = st2[(2 * D + j) * kHalf + tid];
-        const float2 dcn = st2[(3 * D + j) * kHalf + tid];
-        const float2 cn = fma2(f, c, mul2(ig, g));
-        const float2 t = tanh2(cn);
-        const float2 dco = fma2(mul2(dhn, o), fma2(neg(t), t, bc(1.0f)), dcn);  // lstm.py:143
-        // da_g / scale_g, so that sum_g (scale_g W_g)^T (da_g / scale_g) = W^T da
-        const float2 dcs = mul2(dco, bc(-kLn2));
-        const float2 daf = mul2(mul2(dcs, c), fma2(neg(f), f, f));                      // :144
-        const float2 dai = mul2(mul2(dcs, g), fma2(neg(ig), ig, ig));                   // :145
-        const float2 dao = mul2(mul2(dhn, mul2(t, bc(-kLn2))), fma2(neg(o), o, o));    // :142,146
-        const float2 dag = mul2(mul2(dco, mul2(ig, bc(0.5f * kLn2))), fma2(neg(g), g, bc(1.0f)));  // :147
-        *cslot = mul2(dco, f);                                                          // :151
+        bwd_unit(af, ai, ao, ag, *cslot, st2[(2 * D + j) * kHalf + tid], st2[(3 * D + j) * kHalf + tid],
+                 daf, dai, dao, dag, dck);
+        *cslot = dck;
 #pragma unroll
-        for (int m = 0; m < D; ++m) {                                                   // :149-150
+        for (int m = 0; m < D; ++m) {  // lstm.py:149-150
           acc[m] = fma2(bc(p.ws[0][j][m]), daf, acc[m]);
           acc[m] = fma2(bc(p.ws[1][j][m]), dai, acc[m]);
           acc[m] = fma2(bc(p.ws[2][j][m]), dao, acc[m]);
@@ -291,7 +179,6 @@ __global__ void __launch_bounds__(THREADS, MODE == kFwd ? 2 : 1)
 #pragma unroll
       for (int r = 0; r < 2 * D; ++r) bulk_store(y + int64_t(r) * B + base, st + r * G::kTile, bytes);
       bulk_commit();
-      // refill the stage of tile i-1 with tile i+STAGES-1 once its store has read smem
       const int64_t tn = t + int64_t(STAGES - 1) * stride;
       if (tn < ntiles) {
         bulk_wait_read<1>();
@@ -300,18 +187,6 @@ __global__ void __launch_bounds__(THREADS, MODE == kFwd ? 2 : 1)
     }
   }
   if (tid == 0) bulk_wait_all();
-}
-
-template <int D>
-ScaledParams<D> scaled_params(const ackpt_lstm* c, int64_t step) {
-  ScaledParams<D> p;
-  for (int g = 0; g < 4; ++g) {
-    for (int j = 0; j < D; ++j) {
-      for (int k = 0; k < D; ++k) p.ws[g][j][k] = float(c->wh64[(size_t(g) * D + j) * D + k] * double(kScale[g]));
-      p.xbs[g][j] = float(c->xb64[(size_t(step) * 4 + g) * D + j] * double(kScale[g]));
-    }
-  }
-  return p;
 }
 
 }  // namespace tma
@@ -333,7 +208,9 @@ void tma_launch(const ackpt_lstm* c, int64_t step, const float* x, const float* 
   }();
   const int64_t ntiles = (c->B + G::kTile - 1) / G::kTile;
   const int grid = int(ntiles < grid_cap ? ntiles : grid_cap);
-  kern<<<grid, THREADS, kSmem, s>>>(x, a, y, c->B, ntiles, tma::scaled_params<D>(c, step));
+  f32m::ScaledParams<D> p;
+  f32m::fill_scaled<D>(c, step, p);
+  kern<<<grid, THREADS, kSmem, s>>>(x, a, y, c->B, ntiles, p);
 }
 
 }  // namespace ackpt
