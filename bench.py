@@ -52,8 +52,8 @@ def parse_args(argv=None):
     p.add_argument("--no-revolve", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
-    p.add_argument("--sample-every", type=int, default=64,
-                   help="event-pair timing of every k-th launch (sparse: each pair perturbs the stream)")
+    p.add_argument("--full-n", type=int, default=1000, help="n of the measured FullStorage run")
+    p.add_argument("--no-fused", action="store_true")
     return p.parse_args(argv)
 
 
@@ -213,6 +213,31 @@ def run_reference(args) -> None:
     print(json.dumps(line), flush=True)
 
 
+def kernel_chain_times(dc, state0, chain=64):
+    """Mean K1 / K2 launch durations at the bench shape: CUDA events around
+    `chain` back-to-back launches through distinct buffers (like the pass)."""
+    import torch
+
+    bufs = [torch.empty_like(state0) for _ in range(6)]
+    bufs[0].copy_(state0)
+    adj = [torch.empty_like(state0) for _ in range(2)]
+    out = []
+    for kind in ("fwd", "bwd"):
+        for rep in range(2):
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            for k in range(chain):
+                if kind == "fwd":
+                    bufs[(k + 1) % 6] = dc.forward(k % dc.cell.n_steps, bufs[k % 6])
+                else:
+                    adj[(k + 1) % 2] = dc.backward(k % dc.cell.n_steps, bufs[k % 6], adj[k % 2])
+            e1.record()
+            torch.cuda.synchronize()
+        out.append(e0.elapsed_time(e1) * 1e-3 / chain)
+    return out[0], out[1]
+
+
 def workload_config(args, interval, slots) -> dict:
     return {
         "workload": "BASELINE config 2: 1 GPU, 64 MiB fp32 state, n=10^4, memory ratio 0.1, "
@@ -261,7 +286,7 @@ def main(argv=None) -> None:
     slots = max(1, int(args.memory_ratio * args.n) - 1)
 
     # --- calibration (outside the timed window, runtime.py:359-361) ---
-    t_a, t_b, t_t = pkg.calibrate(ops, backend, 5, state0)
+    t_a, t_b, t_t = pkg.calibrate(ops, backend, 5, state0, fuse=args.fuse)
     interval = args.interval or pkg.interval_length(t_t, t_a)
     if world > 1:  # identical schedule on every rank
         t = torch.tensor([interval], device=dev)
@@ -269,14 +294,14 @@ def main(argv=None) -> None:
         interval = int(t.item())
     strategy = pkg.Multistage(slots, interval)
 
-    def run_once(sample=0):
-        return pkg.execute(strategy, ops, state0, backend, fuse=args.fuse, sample_kernels=sample)
+    def run_once():
+        return pkg.execute(strategy, ops, state0, backend, fuse=args.fuse)
 
     for _ in range(args.warmup):
         adj, st = run_once()
     torch.cuda.synchronize()
 
-    # --- timed region: K passes, inputs resident in HBM ---
+    # --- timed region: K passes, inputs resident in HBM, nothing else on the GPU ---
     clocks = ClockSampler(local)
     clocks.start()
     if world > 1:
@@ -289,7 +314,7 @@ def main(argv=None) -> None:
     h0 = time.perf_counter()
     stats = []
     for _ in range(args.steps):
-        adj, st = run_once(args.sample_every)
+        adj, st = run_once()
         stats.append(st)
     e1.record(stream)
     torch.cuda.synchronize()
@@ -303,18 +328,26 @@ def main(argv=None) -> None:
     clock = clocks.stop()
     ms_per_step = elapsed / args.steps * 1e3
     value = world * args.n * args.steps / elapsed
-
-    # --- per-kernel durations sampled inside the timed passes ---
-    fwd_s = sum(s.device["fwd_sample_seconds"] for s in stats)
-    fwd_n = sum(s.device["fwd_samples"] for s in stats)
-    bwd_s = sum(s.device["bwd_sample_seconds"] for s in stats)
-    bwd_n = sum(s.device["bwd_samples"] for s in stats)
-    t_fwd = fwd_s / max(1, fwd_n)
-    t_bwd = bwd_s / max(1, bwd_n)
     last = stats[-1]
     launches = sum(s.device["kernel_launches"] for s in stats)
-    t_inf = args.n * (t_fwd + t_bwd)  # store-all time from measured per-step kernels
+
+    # --- per-kernel durations: CUDA-event-timed chains of the same launches
+    # (event pairs inside the pass would perturb it: each completion flushes
+    # the dirty L2 lines the next step reuses) ---
+    t_fwd, t_bwd = kernel_chain_times(ops.native, state0, chain=64)
+
+    # --- store-all (FullStorage) measured at the largest n kept affordable in
+    # HBM next to the other pools; T_inf = n x its per-step time ---
+    n_full = min(args.n, args.full_n)
+    full_ops = lstm.operator_pair(lstm.random_cell(args.d, n_full, 0), args.batch, "f32")
+    pkg.execute(pkg.FullStorage(), full_ops, state0)
+    _, fst = pkg.execute(pkg.FullStorage(), full_ops, state0)
+    t_store_all_step = fst.wall_seconds / n_full
+    t_inf = args.n * t_store_all_step
+    t_inf_kernels = args.n * (t_fwd + t_bwd)
     overhead = (ms_per_step * 1e-3) / t_inf
+    del full_ops
+    torch.cuda.empty_cache()
 
     # --- roofline: dominant kernel + whole pass ---
     peaks = {}
@@ -340,6 +373,28 @@ def main(argv=None) -> None:
     hbm_bytes = last.forward_evals * 2 * S + last.backward_evals * 3 * S
     link_bytes = (last.stores_issued + last.prefetches_issued) * S
     pass_roofline = max(hbm_bytes / (hbm_peak * 1e9), link_bytes / (link_gbs * 1e9))
+
+    # --- fused Advance launches (same schedule, same counters, bit-identical) ---
+    fused = None
+    if not args.fuse and not args.no_fused:
+        ft_a, _, ft_t = pkg.calibrate(ops, backend, 5, state0, fuse=True)
+        f_interval = pkg.interval_length(ft_t, ft_a)
+        f_strategy = pkg.Multistage(slots, f_interval)
+        for _ in range(2):
+            f_adj, _ = pkg.execute(f_strategy, ops, state0, backend, fuse=True)
+        torch.cuda.synchronize()
+        g0 = torch.cuda.Event(enable_timing=True)
+        g1 = torch.cuda.Event(enable_timing=True)
+        g0.record()
+        for _ in range(args.steps):
+            f_adj, fst2 = pkg.execute(f_strategy, ops, state0, backend, fuse=True)
+        g1.record()
+        torch.cuda.synchronize()
+        f_el = g0.elapsed_time(g1) * 1e-3 / args.steps
+        fused = {"interval": f_interval, "ms_per_step": f_el * 1e3, "steps_per_s": world * args.n / f_el,
+                 "overhead_vs_store_all": f_el / t_inf, "t_a_fused_us": ft_a * 1e6,
+                 "forward_evals": fst2.forward_evals, "stall_seconds": fst2.stall_seconds,
+                 "adjoint_bit_identical_to_unfused": bool(torch.equal(f_adj, adj))}
 
     # --- Revolve(s) at the same memory ratio, for comparison ---
     revolve = None
@@ -411,6 +466,8 @@ def main(argv=None) -> None:
             "impl": "ours",
             "overhead_vs_store_all": overhead,
             "t_inf_seconds": t_inf,
+            "t_inf_source": f"measured FullStorage pass at n={n_full}: {t_store_all_step * 1e6:.2f} us/step x n",
+            "t_inf_from_kernel_chains_seconds": t_inf_kernels,
             "t_a_us": t_fwd * 1e6,
             "t_b_us": t_bwd * 1e6,
             "calibrated": {"t_a_us": t_a * 1e6, "t_b_us": t_b * 1e6, "t_t_ms": t_t * 1e3, "interval": interval},
@@ -428,7 +485,8 @@ def main(argv=None) -> None:
             "roofline": {"kernel": dominant, "bound": "hbm", "achieved": achieved, "peak": hbm_peak,
                          "unit": "GB/s", "frac": achieved / hbm_peak, "traffic": traffic,
                          "algorithmic_bytes_per_launch": bytes_dom, "avg_launch_us": t_dom * 1e6,
-                         "samples": fwd_n if dominant.startswith("lstm_fwd") else bwd_n, "peak_source": peak_src},
+                         "timing": "CUDA events around 64 back-to-back launches", "peak_source": peak_src},
+            "fused": fused,
             "revolve": revolve,
             "e2e": e2e,
             "cpu_baseline": cpu,

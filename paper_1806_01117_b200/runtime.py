@@ -318,13 +318,13 @@ def _device_state(initial_state) -> torch.Tensor:
     return as_device_bytes(initial_state)
 
 
-def _resolve_interval(strategy: Multistage, ops, backend, initial_state) -> int:
+def _resolve_interval(strategy: Multistage, ops, backend, initial_state, fuse: bool) -> int:
     # runtime.py:325-336
     if strategy.interval is not None:
         if strategy.interval < 1:
             raise ValueError(f"interval must be >= 1, got {strategy.interval}")
         return strategy.interval
-    t_a, _, t_t = calibrate(ops, backend, 5, initial_state)
+    t_a, _, t_t = calibrate(ops, backend, 5, initial_state, fuse=fuse)
     return interval_length(t_t, t_a)
 
 
@@ -353,7 +353,7 @@ def execute(
     if isinstance(strategy, Multistage):
         if backend is None:
             raise ValueError("Multistage requires a Level-2 backend")
-        interval = _resolve_interval(strategy, ops, backend, initial_state)
+        interval = _resolve_interval(strategy, ops, backend, initial_state, fuse)
         tier = _tier(backend, ops.state_size)
         code, slots = N.MULTISTAGE, strategy.slots
     elif isinstance(strategy, Revolve):
@@ -415,15 +415,18 @@ def run_backward_sweep(plan: MultistagePlan, ops: OperatorPair, backend, adjoint
     return _finish(out, adjoint_seed)
 
 
-def calibrate(ops: OperatorPair, backend, trial_steps: int, initial_state) -> tuple:
+def calibrate(ops: OperatorPair, backend, trial_steps: int, initial_state, *, fuse: bool = False) -> tuple:
     """Median (t_a, t_b, t_t) in seconds over trial_steps forward steps,
     backward steps and store round trips, timed with CUDA events
-    (runtime.py:420-466).  Keys 0..trial_steps-1 are overwritten."""
+    (runtime.py:420-466).  Keys 0..trial_steps-1 are overwritten.  With
+    ``fuse`` t_a is the per-step cost of a fused Advance launch, the rate at
+    which a fused forward sweep runs."""
     if trial_steps < 3:
         raise ValueError(f"trial_steps must be >= 3, got {trial_steps}")
     if nbytes_of(initial_state) != ops.state_size:
         raise SizeMismatch("initial state does not match state_size")
     engine, cb = _engine_for(ops)
+    N.check(N.lib.ackpt_engine_set_fusion(engine.handle, 1 if fuse else 0))
     tier = _tier(backend, ops.state_size)
     state = _device_state(initial_state)
     t_a, t_b, t_t = C.c_double(), C.c_double(), C.c_double()
