@@ -115,6 +115,13 @@ ACKPT_API int ackpt_lstm_forward(const ackpt_lstm* cell, int64_t step, const voi
 /* Fused run of steps [from, to): one launch, state kept in registers. */
 ACKPT_API int ackpt_lstm_advance(const ackpt_lstm* cell, int64_t from_step, int64_t to_step,
                                  const void* state_in, void* state_out, void* stream);
+/* Fused TapeForward: count (<= 64) steps from from_step, every output kept. */
+ACKPT_API int ackpt_lstm_forward_many(const ackpt_lstm* cell, int64_t from_step, int64_t count,
+                                      const void* state_in, void* const* states_out, void* stream);
+/* Fused Reverse run: steps from+count-1 .. from, adjoint in registers. */
+ACKPT_API int ackpt_lstm_backward_many(const ackpt_lstm* cell, int64_t from_step, int64_t count,
+                                       const void* const* states, const void* adjoint_in,
+                                       void* adjoint_out, void* stream);
 /* One adjoint step k (lstm.py:132-152). */
 ACKPT_API int ackpt_lstm_backward(const ackpt_lstm* cell, int64_t step, const void* state,
                                   const void* adjoint_in, void* adjoint_out, void* stream);
@@ -136,6 +143,17 @@ typedef int (*ackpt_seed_fn)(void* ctx, const void* final_state, void* adjoint_o
 typedef int (*ackpt_advance_fn)(void* ctx, int64_t from_step, int64_t to_step,
                                 const void* state_in, void* state_out, void* stream);
 
+/* Optional temporal fusion of a TapeForward run: steps [from, from+count),
+ * writing the state after each step to states_out[i] (count <= 64). */
+typedef int (*ackpt_forward_many_fn)(void* ctx, int64_t from_step, int64_t count,
+                                     const void* state_in, void* const* states_out, void* stream);
+/* Optional temporal fusion of a run of Reverse actions: steps
+ * from+count-1 down to from, states[i] = state of step from+i, the adjoint
+ * kept on chip in between (count <= 64). */
+typedef int (*ackpt_backward_many_fn)(void* ctx, int64_t from_step, int64_t count,
+                                      const void* const* states, const void* adjoint_in,
+                                      void* adjoint_out, void* stream);
+
 typedef struct ackpt_operator {
   void* ctx;
   ackpt_forward_fn forward;
@@ -144,7 +162,11 @@ typedef struct ackpt_operator {
   ackpt_advance_fn advance;
   int64_t state_bytes; /* OperatorPair.state_size */
   int64_t n_steps;     /* OperatorPair.n_steps */
+  ackpt_forward_many_fn forward_many;   /* NULL: per-step forward */
+  ackpt_backward_many_fn backward_many; /* NULL: per-step backward */
 } ackpt_operator;
+
+#define ACKPT_MAX_FUSED 64
 
 /* Fills *out with the built-in LSTM operator bound to cell. */
 ACKPT_API int ackpt_lstm_operator(ackpt_lstm* cell, ackpt_operator* out);

@@ -94,6 +94,15 @@ ADVANCE_FN = C.CFUNCTYPE(
 )
 
 
+FORWARD_MANY_FN = C.CFUNCTYPE(
+    C.c_int, C.c_void_p, C.c_int64, C.c_int64, C.c_void_p, C.POINTER(C.c_void_p), C.c_void_p
+)
+BACKWARD_MANY_FN = C.CFUNCTYPE(
+    C.c_int, C.c_void_p, C.c_int64, C.c_int64, C.POINTER(C.c_void_p), C.c_void_p, C.c_void_p, C.c_void_p
+)
+MAX_FUSED = 64
+
+
 class Operator(C.Structure):
     _fields_ = [
         ("ctx", C.c_void_p),
@@ -103,6 +112,8 @@ class Operator(C.Structure):
         ("advance", ADVANCE_FN),
         ("state_bytes", C.c_int64),
         ("n_steps", C.c_int64),
+        ("forward_many", FORWARD_MANY_FN),
+        ("backward_many", BACKWARD_MANY_FN),
     ]
 
 
@@ -128,6 +139,8 @@ _SIGS = {
     "ackpt_lstm_forward": ([_vp, C.c_int64, _vp, _vp, _vp], C.c_int),
     "ackpt_lstm_advance": ([_vp, C.c_int64, C.c_int64, _vp, _vp, _vp], C.c_int),
     "ackpt_lstm_backward": ([_vp, C.c_int64, _vp, _vp, _vp, _vp], C.c_int),
+    "ackpt_lstm_forward_many": ([_vp, C.c_int64, C.c_int64, _vp, C.POINTER(_vp), _vp], C.c_int),
+    "ackpt_lstm_backward_many": ([_vp, C.c_int64, C.c_int64, C.POINTER(_vp), _vp, _vp, _vp], C.c_int),
     "ackpt_lstm_seed": ([_vp, _vp, _vp, _vp], C.c_int),
     "ackpt_lstm_loss": ([_vp, _vp, _vp, _vp], C.c_int),
     "ackpt_lstm_operator": ([_vp, C.POINTER(Operator)], C.c_int),

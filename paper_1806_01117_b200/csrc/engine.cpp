@@ -316,7 +316,36 @@ struct Run {
           fail(ACKPT_EXECUTION_ERROR, "action " + std::to_string(idx) + " starts at " +
                                           std::to_string(act.a) + ", state is at " +
                                           std::to_string(current));
-        if (act.op == ACKPT_TAPE) {
+        if (act.op == ACKPT_TAPE && E->fuse && E->op.forward_many) {
+          // Temporal fusion: up to 64 taped steps per launch, every output
+          // kept (the tape holds the INPUT state of each step).
+          for (int64_t rel = act.a; rel < act.b;) {
+            const int64_t cnt = std::min<int64_t>(ACKPT_MAX_FUSED, act.b - rel);
+            void* outs[ACKPT_MAX_FUSED];
+            int ids[ACKPT_MAX_FUSED];
+            for (int64_t i = 0; i < cnt; ++i) {
+              ids[i] = acquire();
+              outs[i] = dry ? nullptr : wptr(ids[i]);
+            }
+            retain(state);
+            tape.emplace_back(rel, state);
+            ledger.add_tape(E->S);
+            for (int64_t i = 0; i + 1 < cnt; ++i) {  // out[i] is the input of step rel+i+1
+              tape.emplace_back(rel + i + 1, ids[i]);
+              ledger.add_tape(E->S);
+            }
+            if (!dry) {
+              check_op(E->op.forward_many(E->op.ctx, offset + rel, cnt, ptr(state), outs, s));
+              ++st.kernel_launches;
+            }
+            release(state);
+            state = ids[cnt - 1];
+            st.forward_evals += cnt;
+            ++st.fused_advances;
+            if (offset + rel + cnt == E->n && !seeded) do_seed(state);
+            rel += cnt;
+          }
+        } else if (act.op == ACKPT_TAPE) {
           for (int64_t rel = act.a; rel < act.b; ++rel) {
             retain(state);
             tape.emplace_back(rel, state);  // the INPUT state of step rel
@@ -353,6 +382,36 @@ struct Run {
           free_slot(act.a);
           ledger.set_slots(occupied * E->S);
         }
+      } else if (act.op == ACKPT_REVERSE && E->fuse && E->op.backward_many) {
+        // Temporal fusion: a run of consecutive Reverse actions over taped
+        // states in one launch (the adjoint never leaves the chip).
+        size_t run = 1;
+        while (idx + run < acts.size() && run < size_t(ACKPT_MAX_FUSED) &&
+               acts[idx + run].op == ACKPT_REVERSE && acts[idx + run].a == act.a - int64_t(run))
+          ++run;
+        if (!seeded)
+          fail(ACKPT_EXECUTION_ERROR, "Reverse " + std::to_string(act.a) + " before the adjoint was seeded");
+        if (tape.size() < run) fail(ACKPT_EXECUTION_ERROR, "Reverse " + std::to_string(act.a) + " without taped state");
+        const void* states[ACKPT_MAX_FUSED];
+        int held[ACKPT_MAX_FUSED];
+        const int64_t lo = act.a - int64_t(run) + 1;
+        for (size_t r = 0; r < run; ++r) {  // pop tops: steps act.a, act.a-1, ...
+          const int64_t want = act.a - int64_t(r);
+          if (tape.back().first != want)
+            fail(ACKPT_EXECUTION_ERROR, "Reverse " + std::to_string(want) + " without taped state");
+          held[r] = tape.back().second;
+          states[want - lo] = dry ? nullptr : ptr(held[r]);
+          tape.pop_back();
+          ledger.drop_tape(E->S);
+        }
+        if (!dry) {
+          check_op(E->op.backward_many(E->op.ctx, offset + lo, int64_t(run), states, adj[a], adj[1 - a], s));
+          ++st.kernel_launches;
+        }
+        a = 1 - a;
+        st.backward_evals += int64_t(run);
+        for (size_t r = 0; r < run; ++r) release(held[r]);
+        idx += run - 1;
       } else if (act.op == ACKPT_REVERSE) {
         if (tape.empty() || tape.back().first != act.a)
           fail(ACKPT_EXECUTION_ERROR, "Reverse " + std::to_string(act.a) + " without taped state");
@@ -517,6 +576,11 @@ void run_impl(ackpt_engine* E, Mode mode, const void* initial_state, const void*
     r.multistage_backward();
   }
 
+  // Per-step runs end with the adjoint in adj[0] (seed parity); fused reverse
+  // runs swap once per launch, so the result may sit in the internal buffer.
+  if (mode != Mode::kForwardSweep && r.a != 0)
+    ACKPT_CUDA_CHECK(cudaMemcpyAsync(r.adj[0], r.adj[r.a], size_t(E->S), cudaMemcpyDeviceToDevice,
+                                     E->compute));
   ACKPT_CUDA_CHECK(cudaEventRecord(E->ev_end, E->compute));
   const auto t_enq = std::chrono::steady_clock::now();
   ACKPT_CUDA_CHECK(cudaEventSynchronize(E->ev_end));

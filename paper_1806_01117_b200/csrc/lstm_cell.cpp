@@ -78,6 +78,14 @@ int lstm_op_seed(void* ctx, const void* fin, void* adj, void* stream) {
 int lstm_op_advance(void* ctx, int64_t from, int64_t to, const void* in, void* out, void* stream) {
   return ackpt_lstm_advance(static_cast<ackpt_lstm*>(ctx), from, to, in, out, stream);
 }
+int lstm_op_forward_many(void* ctx, int64_t from, int64_t count, const void* in, void* const* outs,
+                         void* stream) {
+  return ackpt_lstm_forward_many(static_cast<ackpt_lstm*>(ctx), from, count, in, outs, stream);
+}
+int lstm_op_backward_many(void* ctx, int64_t from, int64_t count, const void* const* states,
+                          const void* ai, void* ao, void* stream) {
+  return ackpt_lstm_backward_many(static_cast<ackpt_lstm*>(ctx), from, count, states, ai, ao, stream);
+}
 
 }  // namespace ackpt
 
@@ -253,6 +261,52 @@ ACKPT_API int ackpt_lstm_backward(const ackpt_lstm* cell, int64_t step, const vo
   });
 }
 
+ACKPT_API int ackpt_lstm_forward_many(const ackpt_lstm* cell, int64_t from_step, int64_t count,
+                                      const void* state_in, void* const* states_out, void* stream) {
+  return ackpt::guard([&] {
+    if (count < 1 || count > ACKPT_MAX_FUSED) ackpt::fail(ACKPT_VALUE_ERROR, "count must be in [1, 64]");
+    if (from_step < 0 || from_step + count > cell->n) ackpt::fail(ACKPT_VALUE_ERROR, "steps out of range");
+    auto s = static_cast<cudaStream_t>(stream);
+    std::vector<const void*> all{state_in};
+    for (int64_t i = 0; i < count; ++i) all.push_back(states_out[i]);
+    bool fast = ackpt::f32_fast(cell, {});
+    for (const void* p : all) fast = fast && !(reinterpret_cast<uintptr_t>(p) & 7u);
+    if (fast) {
+      auto in = static_cast<const float*>(state_in);
+      auto outs = reinterpret_cast<float* const*>(states_out);
+      if (cell->d == 8) ackpt::f32_forward_many<8>(cell, from_step, int(count), in, outs, s);
+      else ackpt::f32_forward_many<4>(cell, from_step, int(count), in, outs, s);
+      ackpt::check_launch();
+      return;
+    }
+    const void* cur = state_in;  // per-step launches
+    for (int64_t i = 0; i < count; ++i) {
+      int rc = ackpt_lstm_forward(cell, from_step + i, cur, states_out[i], stream);
+      if (rc != ACKPT_OK) ackpt::fail(rc, ackpt_last_error());
+      cur = states_out[i];
+    }
+  });
+}
+
+ACKPT_API int ackpt_lstm_backward_many(const ackpt_lstm* cell, int64_t from_step, int64_t count,
+                                       const void* const* states, const void* adjoint_in,
+                                       void* adjoint_out, void* stream) {
+  return ackpt::guard([&] {
+    if (count < 1 || count > ACKPT_MAX_FUSED) ackpt::fail(ACKPT_VALUE_ERROR, "count must be in [1, 64]");
+    if (from_step < 0 || from_step + count > cell->n) ackpt::fail(ACKPT_VALUE_ERROR, "steps out of range");
+    bool fast = ackpt::f32_fast(cell, {adjoint_in, adjoint_out});
+    for (int64_t i = 0; i < count; ++i) fast = fast && !(reinterpret_cast<uintptr_t>(states[i]) & 7u);
+    if (!fast) ackpt::fail(ACKPT_VALUE_ERROR, "fused backward needs the fp32 d in {4, 8} fast path");
+    auto s = static_cast<cudaStream_t>(stream);
+    auto sp = reinterpret_cast<const float* const*>(states);
+    auto ai = static_cast<const float*>(adjoint_in);
+    auto ao = static_cast<float*>(adjoint_out);
+    if (cell->d == 8) ackpt::f32_backward_many<8>(cell, from_step, int(count), sp, ai, ao, s);
+    else ackpt::f32_backward_many<4>(cell, from_step, int(count), sp, ai, ao, s);
+    ackpt::check_launch();
+  });
+}
+
 ACKPT_API int ackpt_lstm_seed(const ackpt_lstm* cell, const void* final_state, void* adjoint_out,
                               void* stream) {
   return ackpt::guard([&] {
@@ -290,6 +344,9 @@ ACKPT_API int ackpt_lstm_operator(ackpt_lstm* cell, ackpt_operator* out) {
     out->advance = ackpt::lstm_op_advance;
     out->state_bytes = ackpt_lstm_state_bytes(cell);
     out->n_steps = cell->n;
+    const bool fused = cell->dtype == ACKPT_F32 && (cell->d == 4 || cell->d == 8) && !(cell->B & 1);
+    out->forward_many = fused ? ackpt::lstm_op_forward_many : nullptr;
+    out->backward_many = fused ? ackpt::lstm_op_backward_many : nullptr;
   });
 }
 

@@ -46,6 +46,13 @@ void f32_backward(const ackpt_lstm* c, int64_t step, const float* st, const floa
 template <int D>
 void f32_advance(const ackpt_lstm* c, int64_t from, int64_t to, const float* in, float* out,
                  cudaStream_t s);
+// Temporal fusion: a TapeForward run / a Reverse run in one launch (count <= 64).
+template <int D>
+void f32_forward_many(const ackpt_lstm* c, int64_t from, int count, const float* in,
+                      float* const* outs, cudaStream_t s);
+template <int D>
+void f32_backward_many(const ackpt_lstm* c, int64_t from, int count, const float* const* states,
+                       const float* adj_in, float* adj_out, cudaStream_t s);
 // Occupancy variants (MINB resident 256-thread CTAs per SM).
 template <int D, int MINB>
 void f32_forward_v(const ackpt_lstm* c, int64_t step, const float* in, float* out, cudaStream_t s);

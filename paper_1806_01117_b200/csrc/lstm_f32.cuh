@@ -150,7 +150,139 @@ __global__ void __launch_bounds__(256, 2)
   for (int j = 0; j < D; ++j) st2(out + b0 + int64_t(D + j) * B, c[j]);
 }
 
+// Scaled input projections of step k from the device table (uniform loads).
+template <int D>
+__device__ __forceinline__ void load_xbs(const float* __restrict__ xbs_all, int64_t k, float (&xbs)[4][D]) {
+  const float4* src = reinterpret_cast<const float4*>(xbs_all + k * 4 * D);
+#pragma unroll
+  for (int v = 0; v < D; ++v) {
+    const float4 x = __ldg(src + v);
+    xbs[(4 * v) / D][(4 * v) % D] = x.x;
+    xbs[(4 * v + 1) / D][(4 * v + 1) % D] = x.y;
+    xbs[(4 * v + 2) / D][(4 * v + 2) % D] = x.z;
+    xbs[(4 * v + 3) / D][(4 * v + 3) % D] = x.w;
+  }
+}
+
+struct StatePtrs {
+  const float* p[ACKPT_MAX_FUSED];
+};
+struct OutPtrs {
+  float* p[ACKPT_MAX_FUSED];
+};
+
+// Fused TapeForward: steps [from, from+count), the state after each step
+// stored to outs.p[i]; the state itself never leaves registers, so a step
+// costs S of HBM writes instead of 2S.  Bit-identical to per-step launches.
+template <int D>
+__global__ void __launch_bounds__(256, 2)
+    tape_kernel(const float* __restrict__ in, int64_t B, const float* __restrict__ xbs_all,
+                int64_t from, int count, const __grid_constant__ AdvParams<D> p,
+                const __grid_constant__ OutPtrs outs) {
+  const int64_t b0 = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) * 2;
+  if (b0 >= B) return;
+  float2 h[D], c[D], hn[D];
+#pragma unroll
+  for (int j = 0; j < D; ++j) h[j] = ld2(in + b0 + int64_t(j) * B);
+#pragma unroll
+  for (int j = 0; j < D; ++j) c[j] = ld2(in + b0 + int64_t(D + j) * B);
+  for (int i = 0; i < count; ++i) {
+    float xbs[4][D];
+    load_xbs<D>(xbs_all, from + i, xbs);
+#pragma unroll
+    for (int j = 0; j < D; ++j) {
+      float2 af, ai, ao, ag;
+      preacts<D>(p.ws, xbs, h, j, af, ai, ao, ag);
+      hn[j] = fwd_unit(af, ai, ao, ag, c[j]);
+    }
+    float* dst = outs.p[i] + b0;
+#pragma unroll
+    for (int j = 0; j < D; ++j) {
+      h[j] = hn[j];
+      st2(dst + int64_t(j) * B, hn[j]);
+    }
+#pragma unroll
+    for (int j = 0; j < D; ++j) st2(dst + int64_t(D + j) * B, c[j]);
+  }
+}
+
+// Fused run of Reverse actions: steps from+count-1 down to from; the adjoint
+// stays in registers, each step reads only its taped state (S instead of 3S
+// of HBM traffic).  Bit-identical to per-step launches.
+template <int D>
+__global__ void __launch_bounds__(256, 2)
+    rev_kernel(const float* __restrict__ adj_in, float* __restrict__ adj_out, int64_t B,
+               const float* __restrict__ xbs_all, int64_t from, int count,
+               const __grid_constant__ AdvParams<D> p, const __grid_constant__ StatePtrs states) {
+  const int64_t b0 = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) * 2;
+  if (b0 >= B) return;
+  float2 dh[D], dc[D];
+#pragma unroll
+  for (int j = 0; j < D; ++j) dh[j] = ld2(adj_in + b0 + int64_t(j) * B);
+#pragma unroll
+  for (int j = 0; j < D; ++j) dc[j] = ld2(adj_in + b0 + int64_t(D + j) * B);
+  for (int i = count - 1; i >= 0; --i) {
+    const float* xs = states.p[i] + b0;
+    float2 h[D], c[D];
+#pragma unroll
+    for (int j = 0; j < D; ++j) h[j] = ld2(xs + int64_t(j) * B);
+#pragma unroll
+    for (int j = 0; j < D; ++j) c[j] = ld2(xs + int64_t(D + j) * B);
+    float xbs[4][D];
+    load_xbs<D>(xbs_all, from + i, xbs);
+    float2 acc[D];
+#pragma unroll
+    for (int m = 0; m < D; ++m) acc[m] = bc(0.0f);
+#pragma unroll
+    for (int j = 0; j < D; ++j) {
+      float2 af, ai, ao, ag, daf, dai, dao, dag;
+      preacts<D>(p.ws, xbs, h, j, af, ai, ao, ag);
+      bwd_unit(af, ai, ao, ag, c[j], dh[j], dc[j], daf, dai, dao, dag, dc[j]);
+#pragma unroll
+      for (int m = 0; m < D; ++m) {
+        acc[m] = fma2(bc(p.ws[0][j][m]), daf, acc[m]);
+        acc[m] = fma2(bc(p.ws[1][j][m]), dai, acc[m]);
+        acc[m] = fma2(bc(p.ws[2][j][m]), dao, acc[m]);
+        acc[m] = fma2(bc(p.ws[3][j][m]), dag, acc[m]);
+      }
+    }
+#pragma unroll
+    for (int m = 0; m < D; ++m) dh[m] = acc[m];
+  }
+#pragma unroll
+  for (int j = 0; j < D; ++j) st2(adj_out + b0 + int64_t(j) * B, dh[j]);
+#pragma unroll
+  for (int j = 0; j < D; ++j) st2(adj_out + b0 + int64_t(D + j) * B, dc[j]);
+}
+
 }  // namespace f32k
+
+template <int D>
+f32k::AdvParams<D> adv_params(const ackpt_lstm* c) {
+  f32k::AdvParams<D> p;
+  f32m::ScaledParams<D> sp;
+  f32m::fill_scaled<D>(c, -1, sp);
+  std::memcpy(p.ws, sp.ws, sizeof(p.ws));
+  return p;
+}
+
+template <int D>
+void f32_forward_many(const ackpt_lstm* c, int64_t from, int count, const float* in,
+                      float* const* outs, cudaStream_t s) {
+  f32k::OutPtrs o;
+  for (int i = 0; i < count; ++i) o.p[i] = outs[i];
+  f32k::tape_kernel<D><<<blocks_for(c->B / 2, 256), 256, 0, s>>>(
+      in, c->B, static_cast<const float*>(c->d_xbs), from, count, adv_params<D>(c), o);
+}
+
+template <int D>
+void f32_backward_many(const ackpt_lstm* c, int64_t from, int count, const float* const* states,
+                       const float* adj_in, float* adj_out, cudaStream_t s) {
+  f32k::StatePtrs sp;
+  for (int i = 0; i < count; ++i) sp.p[i] = states[i];
+  f32k::rev_kernel<D><<<blocks_for(c->B / 2, 256), 256, 0, s>>>(
+      adj_in, adj_out, c->B, static_cast<const float*>(c->d_xbs), from, count, adv_params<D>(c), sp);
+}
 
 template <int D, int MINB>
 void f32_forward_v(const ackpt_lstm* c, int64_t step, const float* in, float* out, cudaStream_t s) {
@@ -199,6 +331,10 @@ void f32_advance(const ackpt_lstm* c, int64_t from, int64_t to, const float* in,
                                cudaStream_t);                                                 \
   template void f32_forward_v<D, 3>(const ackpt_lstm*, int64_t, const float*, float*,         \
                                     cudaStream_t);                                            \
+  template void f32_forward_many<D>(const ackpt_lstm*, int64_t, int, const float*,            \
+                                    float* const*, cudaStream_t);                             \
+  template void f32_backward_many<D>(const ackpt_lstm*, int64_t, int, const float* const*,    \
+                                     const float*, float*, cudaStream_t);                     \
   template void f32_backward_v<D, 3>(const ackpt_lstm*, int64_t, const float*, const float*,  \
                                      float*, cudaStream_t);                                   \
   }

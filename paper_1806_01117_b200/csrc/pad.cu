@@ -74,6 +74,8 @@ ACKPT_API int ackpt_pad_operator_create(const ackpt_operator* base, double forwa
     out->backward = ackpt::pad_backward;
     out->seed = base->seed ? ackpt::pad_seed : nullptr;
     out->advance = nullptr;  // padding is per step
+    out->forward_many = nullptr;
+    out->backward_many = nullptr;
   });
 }
 

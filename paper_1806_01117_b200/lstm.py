@@ -188,6 +188,25 @@ class DeviceCell:
         N.check(N.lib.ackpt_lstm_advance(self.handle, from_step, to_step, x.data_ptr(), out.data_ptr(), _stream()))
         return out
 
+    def forward_many(self, from_step: int, count: int, state) -> list:
+        """Fused TapeForward: the states after steps from_step .. from_step+count-1."""
+        x = self._tensor(state)
+        outs = [torch.empty_like(x) for _ in range(count)]
+        ptrs = (C.c_void_p * count)(*[o.data_ptr() for o in outs])
+        N.check(N.lib.ackpt_lstm_forward_many(self.handle, from_step, count, x.data_ptr(), ptrs, _stream()))
+        return outs
+
+    def backward_many(self, from_step: int, states: list, adjoint) -> torch.Tensor:
+        """Fused Reverse run over steps from_step+len(states)-1 .. from_step;
+        states[i] is the state of step from_step+i."""
+        xs = [self._tensor(s) for s in states]
+        a = self._tensor(adjoint)
+        out = torch.empty_like(a)
+        ptrs = (C.c_void_p * len(xs))(*[x.data_ptr() for x in xs])
+        N.check(N.lib.ackpt_lstm_backward_many(self.handle, from_step, len(xs), ptrs, a.data_ptr(),
+                                               out.data_ptr(), _stream()))
+        return out
+
     def backward(self, step: int, state, adjoint) -> torch.Tensor:
         x = self._tensor(state)
         a = self._tensor(adjoint)

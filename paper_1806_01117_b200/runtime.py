@@ -196,7 +196,8 @@ class _CallbackOperator:
             N.BACKWARD_FN(guard(bwd)),
             N.SEED_FN(guard(seed)) if callable(ops.adjoint_seed) else N.SEED_FN(),
         )
-        self.op = N.Operator(None, self._fns[0], self._fns[1], self._fns[2], N.ADVANCE_FN(), S, ops.n_steps)
+        self.op = N.Operator(None, self._fns[0], self._fns[1], self._fns[2], N.ADVANCE_FN(), S, ops.n_steps,
+                             N.FORWARD_MANY_FN(), N.BACKWARD_MANY_FN())
 
     def raise_pending(self) -> None:
         if self.error is not None:

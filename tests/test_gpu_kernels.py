@@ -114,6 +114,26 @@ def test_fused_advance_equals_step_chain(P, d, batch, dtype):
     assert torch.equal(fused, chain)
 
 
+@pytest.mark.parametrize("d,batch", [(8, 4096), (4, 512), (8, 1002)])
+def test_fused_tape_and_reverse_equal_step_chains(P, d, batch):
+    cell, _ = _cells(P, d, 70, 22)
+    x = torch.from_numpy(_states(d, 9, batch).astype(np.float32)).cuda()
+    a = torch.from_numpy(_states(d, 10, batch).astype(np.float32)).cuda()
+    dc = P.device_cell(cell, batch, "f32")
+    outs = dc.forward_many(3, 64, x)
+    chain, states = x, [x]
+    for k in range(3, 67):
+        chain = dc.forward(k, chain)
+        states.append(chain)
+    for got, want in zip(outs, states[1:]):
+        assert torch.equal(got, want)
+    fused = dc.backward_many(3, states[:64], a)
+    adj = a
+    for k in range(66, 2, -1):
+        adj = dc.backward(k, states[k - 3], adj)
+    assert torch.equal(fused, adj)
+
+
 def test_c2_shape_kernels_on_sampled_rows(P):
     # BASELINE config 2 shape: d=8, B=2^20 fp32 -> 64 MiB states
     d, batch = 8, 1 << 20
