@@ -48,12 +48,14 @@ def parse_args(argv=None):
     p.add_argument("--batch", type=int, default=1 << 20, help="sequences per GPU")
     p.add_argument("--memory-ratio", type=float, default=0.1)
     p.add_argument("--interval", type=int, default=0, help="0: calibrate")
-    p.add_argument("--fuse", action="store_true", help="fused Advance launches")
+    p.add_argument("--per-step", dest="fuse", action="store_false",
+                   help="headline = the reference's per-step operator contract (default: temporally fused "
+                        "launches; same schedule, counters and bits)")
     p.add_argument("--no-revolve", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
     p.add_argument("--full-n", type=int, default=1000, help="n of the measured FullStorage run")
-    p.add_argument("--no-fused", action="store_true")
+    p.add_argument("--no-other-mode", action="store_true")
     return p.parse_args(argv)
 
 
@@ -238,6 +240,36 @@ def kernel_chain_times(dc, state0, chain=64):
     return out[0], out[1]
 
 
+def fused_kernel_times(dc, state0, steps=64):
+    """Per-step durations of the fused launches (64 steps each): advance
+    (state in registers), tape (every output stored), reverse (adjoint in
+    registers, taped states read), plus their algorithmic bytes per launch."""
+    import torch
+
+    S = state0.numel() * state0.element_size()
+    states = dc.forward_many(0, steps, state0)
+    adj = dc.seed(states[-1])
+    out = {}
+    for kind in ("adv", "tape", "rev"):
+        for rep in range(2):
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            if kind == "adv":
+                dc.advance(0, steps, state0)
+            elif kind == "tape":
+                dc.forward_many(0, steps, state0)
+            else:
+                dc.backward_many(0, [state0] + states[:-1], adj)
+            e1.record()
+            torch.cuda.synchronize()
+        out[kind] = e0.elapsed_time(e1) * 1e-3 / steps
+    out["adv_bytes"] = 2 * S
+    out["tape_bytes"] = (steps + 1) * S
+    out["rev_bytes"] = (steps + 2) * S
+    return out
+
+
 def workload_config(args, interval, slots) -> dict:
     return {
         "workload": "BASELINE config 2: 1 GPU, 64 MiB fp32 state, n=10^4, memory ratio 0.1, "
@@ -248,7 +280,8 @@ def workload_config(args, interval, slots) -> dict:
         "state_bytes_per_gpu": 2 * args.d * args.batch * 4,
         "strategy": f"Multistage(slots={slots}, interval={interval})",
         "memory_ratio": args.memory_ratio,
-        "fused_advance": bool(args.fuse),
+        "execution": "temporally fused launches (Advance / TapeForward / Reverse runs)" if args.fuse
+                     else "per-step operator launches (reference contract)",
         "l2": "inputs larger than L2: every pass cycles >= I+2 distinct 64 MiB buffers (126 MB L2)",
         "parallelism": f"batch-sharded x{args.gpus}, identical schedule per rank, no collective in the timed region",
     }
@@ -335,21 +368,26 @@ def main(argv=None) -> None:
     # (event pairs inside the pass would perturb it: each completion flushes
     # the dirty L2 lines the next step reuses) ---
     t_fwd, t_bwd = kernel_chain_times(ops.native, state0, chain=64)
+    fk = fused_kernel_times(ops.native, state0, steps=64)
 
     # --- store-all (FullStorage) measured at the largest n kept affordable in
-    # HBM next to the other pools; T_inf = n x its per-step time ---
+    # HBM next to the other pools; T_inf = n x its per-step time, in both the
+    # per-step and the fused execution mode ---
     n_full = min(args.n, args.full_n)
     full_ops = lstm.operator_pair(lstm.random_cell(args.d, n_full, 0), args.batch, "f32")
-    pkg.execute(pkg.FullStorage(), full_ops, state0)
-    _, fst = pkg.execute(pkg.FullStorage(), full_ops, state0)
-    t_store_all_step = fst.wall_seconds / n_full
-    t_inf = args.n * t_store_all_step
+    t_store_all = {}
+    for mode in (False, True):
+        pkg.execute(pkg.FullStorage(), full_ops, state0, fuse=mode)
+        _, fst = pkg.execute(pkg.FullStorage(), full_ops, state0, fuse=mode)
+        t_store_all["fused" if mode else "per_step"] = fst.wall_seconds / n_full
+    t_inf = args.n * t_store_all["fused" if args.fuse else "per_step"]
+    t_inf_per_step = args.n * t_store_all["per_step"]
     t_inf_kernels = args.n * (t_fwd + t_bwd)
     overhead = (ms_per_step * 1e-3) / t_inf
     del full_ops
     torch.cuda.empty_cache()
 
-    # --- roofline: dominant kernel + whole pass ---
+    # --- roofline: dominant kernel of the headline pass + whole pass ---
     peaks = {}
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
@@ -358,43 +396,55 @@ def main(argv=None) -> None:
         pass
     hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
     peak_src = "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback 6.65 TB/s (B200_PROFILING.md)"
-    fwd_time_share = last.forward_evals * t_fwd
-    bwd_time_share = last.backward_evals * t_bwd
-    dominant = "lstm_fwd (K1)" if fwd_time_share >= bwd_time_share else "lstm_bwd (K2)"
-    bytes_dom = 2 * S if dominant.startswith("lstm_fwd") else 3 * S
-    t_dom = t_fwd if dominant.startswith("lstm_fwd") else t_bwd
+    if args.fuse:
+        # per step of the pass: n sweep steps (fused advance), n taped steps, n reverse steps
+        shares = {"lstm_rev_fused (K2f)": (args.n * fk["rev"], fk["rev_bytes"], fk["rev"] * 64),
+                  "lstm_tape_fused (K1t)": (args.n * fk["tape"], fk["tape_bytes"], fk["tape"] * 64),
+                  "lstm_adv_fused (K1f)": (args.n * fk["adv"], fk["adv_bytes"], fk["adv"] * 64)}
+    else:
+        shares = {"lstm_fwd (K1)": (last.forward_evals * t_fwd, 2 * S, t_fwd),
+                  "lstm_bwd (K2)": (last.backward_evals * t_bwd, 3 * S, t_bwd)}
+    dominant = max(shares, key=lambda k: shares[k][0])
+    _, bytes_dom, t_dom = shares[dominant]
     achieved = bytes_dom / t_dom / 1e9
     traffic = None
     tfile = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tfile):
         with open(tfile) as fh:
-            traffic = json.load(fh).get("fwd" if dominant.startswith("lstm_fwd") else "bwd")
+            traffic = json.load(fh).get(dominant.split()[0])
     link_gbs = S / t_t / 1e9
-    hbm_bytes = last.forward_evals * 2 * S + last.backward_evals * 3 * S
+    if args.fuse:  # algorithmic HBM bytes of the fused pass
+        hbm_bytes = int(args.n * S * (2 / 64 + 1 + 1) + last.backward_evals * S)
+    else:
+        hbm_bytes = last.forward_evals * 2 * S + last.backward_evals * 3 * S
     link_bytes = (last.stores_issued + last.prefetches_issued) * S
     pass_roofline = max(hbm_bytes / (hbm_peak * 1e9), link_bytes / (link_gbs * 1e9))
 
-    # --- fused Advance launches (same schedule, same counters, bit-identical) ---
-    fused = None
-    if not args.fuse and not args.no_fused:
-        ft_a, _, ft_t = pkg.calibrate(ops, backend, 5, state0, fuse=True)
-        f_interval = pkg.interval_length(ft_t, ft_a)
-        f_strategy = pkg.Multistage(slots, f_interval)
+    # --- the other execution mode (same schedule, same counters, bit-identical) ---
+    other = None
+    if not args.no_other_mode:
+        mode = not args.fuse
+        ot_a, _, ot_t = pkg.calibrate(ops, backend, 5, state0, fuse=mode)
+        o_interval = args.interval or pkg.interval_length(ot_t, ot_a)
+        o_strategy = pkg.Multistage(slots, o_interval)
         for _ in range(2):
-            f_adj, _ = pkg.execute(f_strategy, ops, state0, backend, fuse=True)
+            o_adj, _ = pkg.execute(o_strategy, ops, state0, backend, fuse=mode)
         torch.cuda.synchronize()
         g0 = torch.cuda.Event(enable_timing=True)
         g1 = torch.cuda.Event(enable_timing=True)
         g0.record()
         for _ in range(args.steps):
-            f_adj, fst2 = pkg.execute(f_strategy, ops, state0, backend, fuse=True)
+            o_adj, ost = pkg.execute(o_strategy, ops, state0, backend, fuse=mode)
         g1.record()
         torch.cuda.synchronize()
-        f_el = g0.elapsed_time(g1) * 1e-3 / args.steps
-        fused = {"interval": f_interval, "ms_per_step": f_el * 1e3, "steps_per_s": world * args.n / f_el,
-                 "overhead_vs_store_all": f_el / t_inf, "t_a_fused_us": ft_a * 1e6,
-                 "forward_evals": fst2.forward_evals, "stall_seconds": fst2.stall_seconds,
-                 "adjoint_bit_identical_to_unfused": bool(torch.equal(f_adj, adj))}
+        o_el = g0.elapsed_time(g1) * 1e-3 / args.steps
+        o_inf = args.n * t_store_all["fused" if mode else "per_step"]
+        other = {"mode": "fused" if mode else "per_step", "interval": o_interval,
+                 "ms_per_step": o_el * 1e3, "steps_per_s": world * args.n / o_el,
+                 "overhead_vs_store_all": o_el / o_inf, "overhead_vs_per_step_store_all": o_el / t_inf_per_step,
+                 "calibrated_t_a_us": ot_a * 1e6, "forward_evals": ost.forward_evals,
+                 "stall_seconds": ost.stall_seconds, "kernel_launches": ost.device["kernel_launches"],
+                 "adjoint_bit_identical_to_headline": bool(torch.equal(o_adj, adj))}
 
     # --- Revolve(s) at the same memory ratio, for comparison ---
     revolve = None
@@ -485,8 +535,12 @@ def main(argv=None) -> None:
             "roofline": {"kernel": dominant, "bound": "hbm", "achieved": achieved, "peak": hbm_peak,
                          "unit": "GB/s", "frac": achieved / hbm_peak, "traffic": traffic,
                          "algorithmic_bytes_per_launch": bytes_dom, "avg_launch_us": t_dom * 1e6,
-                         "timing": "CUDA events around 64 back-to-back launches", "peak_source": peak_src},
-            "fused": fused,
+                         "timing": "CUDA events around back-to-back launches of the same kernel",
+                         "peak_source": peak_src},
+            "other_mode": other,
+            "fused_kernels_us_per_step": {k: fk[k] * 1e6 for k in ("adv", "tape", "rev")},
+            "store_all_us_per_step": {k: v * 1e6 for k, v in t_store_all.items()},
+            "overhead_vs_per_step_store_all": (ms_per_step * 1e-3) / t_inf_per_step,
             "revolve": revolve,
             "e2e": e2e,
             "cpu_baseline": cpu,
