@@ -450,8 +450,8 @@ def main(argv=None) -> None:
     revolve = None
     if not args.no_revolve:
         try:
-            pkg.execute(pkg.Revolve(slots), ops, state0)
-            _, rst = pkg.execute(pkg.Revolve(slots), ops, state0)
+            pkg.execute(pkg.Revolve(slots), ops, state0, fuse=args.fuse)
+            _, rst = pkg.execute(pkg.Revolve(slots), ops, state0, fuse=args.fuse)
             revolve = {
                 "slots": slots,
                 "wall_seconds": rst.wall_seconds,
