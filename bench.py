@@ -307,6 +307,7 @@ def main(argv=None) -> None:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
     import paper_1806_01117_b200 as pkg
+    import paper_1806_01117_b200.distributed as D
     import paper_1806_01117_b200.lstm as lstm
 
     dev = torch.device("cuda", local)
@@ -320,11 +321,8 @@ def main(argv=None) -> None:
 
     # --- calibration (outside the timed window, runtime.py:359-361) ---
     t_a, t_b, t_t = pkg.calibrate(ops, backend, 5, state0, fuse=args.fuse)
-    interval = args.interval or pkg.interval_length(t_t, t_a)
-    if world > 1:  # identical schedule on every rank
-        t = torch.tensor([interval], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        interval = int(t.item())
+    # identical schedule on every rank: the largest calibrated interval
+    interval = D.agree_interval(args.interval or pkg.interval_length(t_t, t_a))
     strategy = pkg.Multistage(slots, interval)
 
     def run_once():
@@ -352,12 +350,7 @@ def main(argv=None) -> None:
     e1.record(stream)
     torch.cuda.synchronize()
     host_elapsed = time.perf_counter() - h0
-    elapsed = e0.elapsed_time(e1) * 1e-3
-    if world > 1:
-        dist.barrier()
-        t = torch.tensor([elapsed], device=dev, dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        elapsed = float(t.item())
+    elapsed = D.max_over_ranks(e0.elapsed_time(e1) * 1e-3)
     clock = clocks.stop()
     ms_per_step = elapsed / args.steps * 1e3
     value = world * args.n * args.steps / elapsed
@@ -425,7 +418,7 @@ def main(argv=None) -> None:
     if not args.no_other_mode:
         mode = not args.fuse
         ot_a, _, ot_t = pkg.calibrate(ops, backend, 5, state0, fuse=mode)
-        o_interval = args.interval or pkg.interval_length(ot_t, ot_a)
+        o_interval = D.agree_interval(args.interval or pkg.interval_length(ot_t, ot_a))
         o_strategy = pkg.Multistage(slots, o_interval)
         for _ in range(2):
             o_adj, _ = pkg.execute(o_strategy, ops, state0, backend, fuse=mode)
@@ -480,11 +473,7 @@ def main(argv=None) -> None:
             host_out.copy_(adj_dev)
         g1.record()
         torch.cuda.synchronize()
-        e2e_elapsed = g0.elapsed_time(g1) * 1e-3
-        if world > 1:
-            t = torch.tensor([e2e_elapsed], device=dev, dtype=torch.float64)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            e2e_elapsed = float(t.item())
+        e2e_elapsed = D.max_over_ranks(g0.elapsed_time(g1) * 1e-3)
         e2e = {"value": world * args.n * args.steps / e2e_elapsed, "unit": "steps/s",
                "h2d_bytes_per_step": S, "d2h_bytes_per_step": S,
                "ms_per_step": e2e_elapsed / args.steps * 1e3}

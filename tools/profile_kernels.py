@@ -24,6 +24,7 @@ def main():
     ap.add_argument("--d", type=int, default=8)
     ap.add_argument("--batch", type=int, default=1 << 20)
     ap.add_argument("--fused", type=int, default=0)
+    ap.add_argument("--fused-only", type=int, default=0, help="only the fused adv/tape/rev launches (for ncu)")
     args = ap.parse_args()
     cell = lstm.random_cell(args.d, max(args.steps, 2), 0)
     dc = lstm.device_cell(cell, args.batch, "f32")
@@ -34,6 +35,17 @@ def main():
     adj = [torch.empty_like(x) for _ in range(2)]
     bufs[0].copy_(x)
     out = {}
+    if args.fused_only:
+        L = min(64, args.steps)
+        states = dc.forward_many(0, L, x)
+        a0 = dc.seed(states[-1])
+        for _ in range(3):
+            dc.advance(0, L, x)
+            dc.forward_many(0, L, x)
+            dc.backward_many(0, [x] + states[:-1], a0)
+        torch.cuda.synchronize()
+        print(json.dumps({"fused_only": True, "steps": L}))
+        return
     for name in ("fwd", "bwd"):
         for _ in range(3):  # warm-up
             dc.forward(0, bufs[0])
