@@ -186,6 +186,14 @@ typedef int64_t ackpt_ticket;
 /* capacity: number of keys the pinned slab can hold; slot_bytes: bytes per key.
  * The slab is allocated here (outside any timed window). */
 ACKPT_API int ackpt_tier_create(int64_t capacity, int64_t slot_bytes, ackpt_tier** out);
+/* File (NVMe) stage, FileBackend (storage.py:321-340): every key is a file
+ * <directory>/ckpt_<key>.bin in the reference's CKPT format (magic, u16
+ * version, u64 step, u64 length, payload, u32 CRC32C; tmp + rename), moved
+ * HBM <-> pinned staging <-> file on the copy streams.  Corrupt / truncated
+ * files -> CHECKSUM_MISMATCH, ENOSPC -> STORAGE_FULL, absent -> MISSING_KEY,
+ * reported at wait (or at the end of an engine run).  Files already present
+ * in the directory can be fetched (resume). */
+ACKPT_API int ackpt_tier_create_file(const char* directory, int64_t slot_bytes, ackpt_tier** out);
 ACKPT_API int ackpt_tier_destroy(ackpt_tier* tier);
 /* Stall injection for contention tests: each transfer holds its copy stream
  * for at least latency_us + bytes / bandwidth (bandwidth <= 0: no limit),

@@ -147,6 +147,7 @@ _SIGS = {
     "ackpt_pad_operator_create": ([C.POINTER(Operator), C.c_double, C.c_double, C.POINTER(Operator)], C.c_int),
     "ackpt_pad_operator_destroy": ([C.POINTER(Operator)], C.c_int),
     "ackpt_tier_create": ([C.c_int64, C.c_int64, C.POINTER(_vp)], C.c_int),
+    "ackpt_tier_create_file": ([C.c_char_p, C.c_int64, C.POINTER(_vp)], C.c_int),
     "ackpt_tier_destroy": ([_vp], C.c_int),
     "ackpt_tier_set_throttle": ([_vp, C.c_double, C.c_double], C.c_int),
     "ackpt_tier_begin_store": ([_vp, C.c_int64, C.c_int64, _vp, C.c_int64, _vp, _i64p], C.c_int),

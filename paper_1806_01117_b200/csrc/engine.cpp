@@ -44,6 +44,7 @@ namespace ackpt {
 void tier_reserve_keys(ackpt_tier* t, const std::vector<int64_t>& keys, int64_t bytes);
 cudaEvent_t tier_ticket_event(ackpt_tier* t, ackpt_ticket id);
 int tier_ticket_status(ackpt_tier* t, ackpt_ticket id, std::string* msg);
+int tier_async_status(ackpt_tier* t, ackpt_ticket id, std::string* msg);
 void tier_retire(ackpt_tier* t, ackpt_ticket id);
 int64_t tier_slot_bytes(const ackpt_tier* t);
 cudaStream_t tier_d2h(const ackpt_tier* t);
@@ -273,9 +274,14 @@ struct Run {
     stall_pairs.emplace_back(before, after);
   }
 
+  std::vector<ackpt_ticket> issued;  // checked for file-stage errors after the run
+
   ackpt_ticket begin_store(int64_t key, int state) {
     ackpt_ticket t = -1;
-    if (!dry) check_op(ackpt_tier_begin_store(E->tier, key, key, ptr(state), E->S, s, &t));
+    if (!dry) {
+      check_op(ackpt_tier_begin_store(E->tier, key, key, ptr(state), E->S, s, &t));
+      issued.push_back(t);
+    }
     ++st.stores_issued;
     st.link_bytes += E->S;
     return t;
@@ -286,6 +292,7 @@ struct Run {
     if (!dry) {
       int rc = ackpt_tier_begin_fetch(E->tier, key, wptr(dst), E->S, s, &t);
       if (rc != ACKPT_OK) fail(rc, ackpt_last_error());
+      issued.push_back(t);
     }
     ++st.prefetches_issued;
     st.link_bytes += E->S;
@@ -586,6 +593,11 @@ void run_impl(ackpt_engine* E, Mode mode, const void* initial_state, const void*
   ACKPT_CUDA_CHECK(cudaEventSynchronize(E->ev_end));
   const auto t1 = std::chrono::steady_clock::now();
   ACKPT_CUDA_CHECK(cudaStreamWaitEvent(caller, E->ev_end, 0));
+  for (ackpt_ticket tk : r.issued) {  // file-stage I/O errors surface once the run drained
+    std::string msg;
+    const int rc = tier_async_status(E->tier, tk, &msg);
+    if (rc != ACKPT_OK) fail(rc, msg);
+  }
   if (mode == Mode::kFull && !r.seeded)
     fail(ACKPT_EXECUTION_ERROR, "execution finished without producing an adjoint");  // runtime.py:379-380
 

@@ -11,7 +11,11 @@
 // status returned by ackpt_tier_wait (MissingKey, StorageFull, SizeMismatch).
 #include <cuda_runtime.h>
 
+#include <atomic>
+#include <cerrno>
 #include <chrono>
+#include <cstdio>
+#include <cstring>
 #include <deque>
 #include <memory>
 #include <mutex>
@@ -24,6 +28,13 @@
 
 namespace ackpt {
 
+// Status written by a host function on a copy stream (file I/O); read after
+// the ticket's event completed, which orders it after the host function.
+struct AsyncStatus {
+  std::atomic<int> err{ACKPT_OK};
+  std::string msg;
+};
+
 struct TierTicket {
   cudaEvent_t done = nullptr;
   int kind = 0;  // 0 store, 1 fetch
@@ -33,6 +44,10 @@ struct TierTicket {
   std::string msg;
   bool complete = false;
   double hold_seconds = 0.0;  // throttle: host-func sleep on the copy stream
+  // file stage
+  std::shared_ptr<AsyncStatus> async;
+  ackpt_tier* tier = nullptr;
+  int64_t len = 0;
 };
 
 struct KeyEntry {
@@ -62,6 +77,13 @@ struct ackpt_tier {
   cudaEvent_t after = nullptr;
   double latency_s = 0.0, bandwidth = 0.0;
   std::mutex mu;
+  // File (NVMe) stage: keys live in CKPT files under `dir`; transfers stage
+  // through one pinned buffer per direction (stream FIFO orders their reuse).
+  bool file_mode = false;
+  std::string dir;
+  unsigned char* stage_out = nullptr;
+  unsigned char* stage_in = nullptr;
+  int64_t stage_cap = 0;
 };
 
 namespace ackpt {
@@ -130,6 +152,128 @@ void retire(ackpt_tier* t, TierTicket& tk) {
   }
 }
 
+// ---- file stage: CKPT format (storage.py:9-18, 83-127) ----------------------
+// magic "CKPT" | u16 version=1 | u64 step | u64 length | payload | u32 crc32c(header+payload)
+constexpr int kHeader = 22, kTrailer = 4;
+
+std::string ckpt_path(const ackpt_tier* t, int64_t key) {
+  return t->dir + "/ckpt_" + std::to_string(key) + ".bin";
+}
+
+void put_le(unsigned char* p, uint64_t v, int bytes) {
+  for (int i = 0; i < bytes; ++i) p[i] = (unsigned char)(v >> (8 * i));
+}
+uint64_t get_le(const unsigned char* p, int bytes) {
+  uint64_t v = 0;
+  for (int i = 0; i < bytes; ++i) v |= uint64_t(p[i]) << (8 * i);
+  return v;
+}
+
+void set_async(AsyncStatus& st, int code, const std::string& msg) {
+  st.msg = msg;
+  st.err.store(code, std::memory_order_release);
+}
+
+// Host function on the D2H stream, after the payload landed in stage_out:
+// tmp file + rename (write_checkpoint_file, storage.py:109-118).
+void CUDART_CB file_store_cb(void* arg) {
+  auto* tk = static_cast<TierTicket*>(arg);
+  ackpt_tier* t = tk->tier;
+  unsigned char header[kHeader];
+  std::memcpy(header, "CKPT", 4);
+  put_le(header + 4, 1, 2);
+  put_le(header + 6, uint64_t(tk->step), 8);
+  put_le(header + 14, uint64_t(tk->len), 8);
+  uint32_t crc = ackpt_crc32c(header, kHeader, 0);
+  crc = ackpt_crc32c(t->stage_out, tk->len, crc);
+  unsigned char trailer[kTrailer];
+  put_le(trailer, crc, 4);
+  const std::string path = ckpt_path(t, tk->key), tmp = path + ".tmp";
+  errno = 0;
+  FILE* f = std::fopen(tmp.c_str(), "wb");
+  bool ok = f != nullptr;
+  if (ok) ok = std::fwrite(header, 1, kHeader, f) == size_t(kHeader);
+  if (ok && tk->len > 0) ok = std::fwrite(t->stage_out, 1, size_t(tk->len), f) == size_t(tk->len);
+  if (ok) ok = std::fwrite(trailer, 1, kTrailer, f) == size_t(kTrailer);
+  if (f && std::fclose(f) != 0) ok = false;
+  if (ok) ok = std::rename(tmp.c_str(), path.c_str()) == 0;
+  if (!ok) {
+    const int e = errno;
+    std::remove(tmp.c_str());
+    set_async(*tk->async, e == ENOSPC ? ACKPT_STORAGE_FULL : ACKPT_EXECUTION_ERROR,
+              "writing " + path + ": " + std::strerror(e));
+  }
+}
+
+// Host function on the H2D stream: read + verify into stage_in
+// (decode_checkpoint / read_checkpoint_file, storage.py:83-127).
+void CUDART_CB file_fetch_cb(void* arg) {
+  auto* tk = static_cast<TierTicket*>(arg);
+  ackpt_tier* t = tk->tier;
+  const std::string path = ckpt_path(t, tk->key);
+  FILE* f = std::fopen(path.c_str(), "rb");
+  if (!f) {
+    set_async(*tk->async, ACKPT_MISSING_KEY, path);
+    return;
+  }
+  std::fseek(f, 0, SEEK_END);
+  const long size = std::ftell(f);
+  std::fseek(f, 0, SEEK_SET);
+  unsigned char header[kHeader], trailer[kTrailer];
+  auto bad = [&](const std::string& why) {
+    std::fclose(f);
+    set_async(*tk->async, ACKPT_CHECKSUM_MISMATCH, path + ": " + why);
+  };
+  if (size < kHeader + kTrailer) return bad("checkpoint truncated: " + std::to_string(size) + " bytes");
+  if (std::fread(header, 1, kHeader, f) != size_t(kHeader)) return bad("short read");
+  if (std::memcmp(header, "CKPT", 4) != 0) return bad("bad magic bytes");
+  if (get_le(header + 4, 2) != 1) return bad("unsupported format version");
+  const uint64_t step = get_le(header + 6, 8), length = get_le(header + 14, 8);
+  if (uint64_t(size) != length + kHeader + kTrailer)
+    return bad("length field says " + std::to_string(length) + ", file holds " +
+               std::to_string(size - kHeader - kTrailer));
+  if (int64_t(length) != tk->len || int64_t(length) > t->stage_cap) return bad("payload size changed");
+  if (length > 0 && std::fread(t->stage_in, 1, size_t(length), f) != size_t(length)) return bad("short read");
+  if (std::fread(trailer, 1, kTrailer, f) != size_t(kTrailer)) return bad("short read");
+  std::fclose(f);
+  uint32_t crc = ackpt_crc32c(header, kHeader, 0);
+  crc = ackpt_crc32c(t->stage_in, int64_t(length), crc);
+  if (crc != uint32_t(get_le(trailer, 4))) {
+    set_async(*tk->async, ACKPT_CHECKSUM_MISMATCH, path + ": crc mismatch");
+    return;
+  }
+  if (int64_t(step) != tk->key)
+    set_async(*tk->async, ACKPT_CHECKSUM_MISMATCH,
+              path + ": file holds step " + std::to_string(step) + ", expected " + std::to_string(tk->key));
+  tk->step = int64_t(step);
+}
+
+// Length of an existing CKPT file (header only), -1 when absent / unreadable.
+int64_t file_payload_len(const ackpt_tier* t, int64_t key) {
+  FILE* f = std::fopen(ckpt_path(t, key).c_str(), "rb");
+  if (!f) return -1;
+  unsigned char header[kHeader];
+  const bool ok = std::fread(header, 1, kHeader, f) == size_t(kHeader);
+  std::fclose(f);
+  return ok ? int64_t(get_le(header + 14, 8)) : 0;
+}
+
+void ensure_stage(ackpt_tier* t, int64_t bytes) {
+  if (bytes <= t->stage_cap) return;
+  ACKPT_CUDA_CHECK(cudaStreamSynchronize(t->d2h));
+  ACKPT_CUDA_CHECK(cudaStreamSynchronize(t->h2d));
+  if (t->stage_out) cudaFreeHost(t->stage_out);
+  if (t->stage_in) cudaFreeHost(t->stage_in);
+  t->stage_out = t->stage_in = nullptr;
+  t->stage_cap = 0;
+  if (cudaHostAlloc(reinterpret_cast<void**>(&t->stage_out), size_t(bytes), cudaHostAllocDefault) != cudaSuccess ||
+      cudaHostAlloc(reinterpret_cast<void**>(&t->stage_in), size_t(bytes), cudaHostAllocDefault) != cudaSuccess) {
+    cudaGetLastError();
+    fail(ACKPT_STORAGE_FULL, "pinned staging allocation failed");
+  }
+  t->stage_cap = bytes;
+}
+
 unsigned char* key_ptr(const ackpt_tier* t, const KeyEntry& ke) {
   return ke.big ? ke.big : t->slot_ptr[size_t(ke.slot)];
 }
@@ -189,6 +333,15 @@ cudaEvent_t tier_ticket_event(ackpt_tier* t, ackpt_ticket id) {
   TierTicket& tk = get_ticket(t, id);
   return tk.complete ? nullptr : tk.done;
 }
+// Asynchronous (file-stage) status of a ticket whose event has completed.
+int tier_async_status(ackpt_tier* t, ackpt_ticket id, std::string* msg) {
+  std::lock_guard<std::mutex> lk(t->mu);
+  TierTicket& tk = get_ticket(t, id);
+  if (!tk.async) return ACKPT_OK;
+  const int e = tk.async->err.load(std::memory_order_acquire);
+  if (e != ACKPT_OK && msg) *msg = tk.async->msg;
+  return e;
+}
 int tier_ticket_status(ackpt_tier* t, ackpt_ticket id, std::string* msg) {
   std::lock_guard<std::mutex> lk(t->mu);
   TierTicket& tk = get_ticket(t, id);
@@ -226,6 +379,17 @@ ACKPT_API int ackpt_tier_create(int64_t capacity, int64_t slot_bytes, ackpt_tier
   });
 }
 
+ACKPT_API int ackpt_tier_create_file(const char* directory, int64_t slot_bytes, ackpt_tier** out) {
+  int rc = ackpt_tier_create(0, slot_bytes > 0 ? slot_bytes : 1, out);
+  if (rc != ACKPT_OK) return rc;
+  return ackpt::guard([&] {
+    ackpt_tier* t = *out;
+    t->file_mode = true;
+    t->dir = directory ? directory : ".";
+    ackpt::ensure_stage(t, slot_bytes > 0 ? slot_bytes : 1);
+  });
+}
+
 ACKPT_API int ackpt_tier_destroy(ackpt_tier* t) {
   return ackpt::guard([&] {
     if (!t) return;
@@ -239,6 +403,8 @@ ACKPT_API int ackpt_tier_destroy(ackpt_tier* t) {
     }
     if (t->after) cudaEventDestroy(t->after);
     for (auto c : t->chunks) cudaFreeHost(c);
+    if (t->stage_out) cudaFreeHost(t->stage_out);
+    if (t->stage_in) cudaFreeHost(t->stage_in);
     if (t->d2h) cudaStreamDestroy(t->d2h);
     if (t->h2d) cudaStreamDestroy(t->h2d);
     delete t;
@@ -263,6 +429,35 @@ ACKPT_API int ackpt_tier_begin_store(ackpt_tier* t, int64_t key, int64_t step, c
     tk.key = key;
     tk.step = step;
     if (bytes < 0) ackpt::fail(ACKPT_VALUE_ERROR, "bytes must be >= 0");
+    if (t->file_mode) {
+      // D2H into the staging buffer, then write the CKPT file from a host
+      // function on the same stream (stores serialise on the D2H stream).
+      ackpt::ensure_stage(t, bytes);
+      ackpt::KeyEntry& ke = t->keys[key];
+      if (after_stream) {
+        ACKPT_CUDA_CHECK(cudaEventRecord(t->after, static_cast<cudaStream_t>(after_stream)));
+        ACKPT_CUDA_CHECK(cudaStreamWaitEvent(t->d2h, t->after, 0));
+      }
+      if (ke.fetched) ACKPT_CUDA_CHECK(cudaStreamWaitEvent(t->d2h, ke.last_fetch, 0));
+      if (bytes > 0)
+        ACKPT_CUDA_CHECK(cudaMemcpyAsync(t->stage_out, src, size_t(bytes), cudaMemcpyDeviceToHost, t->d2h));
+      ke.step = step;
+      ke.len = bytes;
+      ackpt_ticket id = ackpt::add_ticket(t, std::move(tk));
+      ackpt::TierTicket& ref = t->tickets[size_t(id)];
+      ref.tier = t;
+      ref.len = bytes;
+      ref.async = std::make_shared<ackpt::AsyncStatus>();
+      ACKPT_CUDA_CHECK(cudaLaunchHostFunc(t->d2h, ackpt::file_store_cb, &ref));
+      ackpt::hold(t, t->d2h, ref, bytes);
+      ref.done = ackpt::new_event(t);
+      ACKPT_CUDA_CHECK(cudaEventRecord(ref.done, t->d2h));
+      if (!ke.last_store) ACKPT_CUDA_CHECK(cudaEventCreateWithFlags(&ke.last_store, cudaEventDisableTiming));
+      ACKPT_CUDA_CHECK(cudaEventRecord(ke.last_store, t->d2h));
+      ke.stored = true;
+      *out = id;
+      return;
+    }
     ackpt::KeyEntry* kp = nullptr;
     try {
       kp = &ackpt::ensure_storage(t, key, bytes);
@@ -304,6 +499,51 @@ ACKPT_API int ackpt_tier_begin_fetch(ackpt_tier* t, int64_t key, void* dst, int6
     tk.kind = 1;
     tk.key = key;
     auto it = t->keys.find(key);
+    if (t->file_mode) {
+      // Keys stored earlier in this tier, or CKPT files already on disk (resume).
+      int64_t len = -1;
+      if (it != t->keys.end() && it->second.stored) len = it->second.len;
+      else len = ackpt::file_payload_len(t, key);
+      if (len < 0) {
+        tk.err = ACKPT_MISSING_KEY;
+        tk.msg = ackpt::ckpt_path(t, key);
+        tk.complete = true;
+        *out = ackpt::add_ticket(t, std::move(tk));
+        return;
+      }
+      if (bytes >= 0 && bytes < len) {
+        tk.err = ACKPT_SIZE_MISMATCH;
+        tk.msg = "destination holds " + std::to_string(bytes) + " bytes, key " + std::to_string(key) +
+                 " holds " + std::to_string(len);
+        tk.complete = true;
+        *out = ackpt::add_ticket(t, std::move(tk));
+        return;
+      }
+      ackpt::ensure_stage(t, len);
+      ackpt::KeyEntry& ke = t->keys[key];
+      tk.step = ke.stored ? ke.step : key;
+      if (after_stream) {
+        ACKPT_CUDA_CHECK(cudaEventRecord(t->after, static_cast<cudaStream_t>(after_stream)));
+        ACKPT_CUDA_CHECK(cudaStreamWaitEvent(t->h2d, t->after, 0));
+      }
+      if (ke.stored) ACKPT_CUDA_CHECK(cudaStreamWaitEvent(t->h2d, ke.last_store, 0));
+      ackpt_ticket id = ackpt::add_ticket(t, std::move(tk));
+      ackpt::TierTicket& ref = t->tickets[size_t(id)];
+      ref.tier = t;
+      ref.len = len;
+      ref.async = std::make_shared<ackpt::AsyncStatus>();
+      ACKPT_CUDA_CHECK(cudaLaunchHostFunc(t->h2d, ackpt::file_fetch_cb, &ref));
+      if (len > 0)
+        ACKPT_CUDA_CHECK(cudaMemcpyAsync(dst, t->stage_in, size_t(len), cudaMemcpyHostToDevice, t->h2d));
+      ackpt::hold(t, t->h2d, ref, len);
+      ref.done = ackpt::new_event(t);
+      ACKPT_CUDA_CHECK(cudaEventRecord(ref.done, t->h2d));
+      if (!ke.last_fetch) ACKPT_CUDA_CHECK(cudaEventCreateWithFlags(&ke.last_fetch, cudaEventDisableTiming));
+      ACKPT_CUDA_CHECK(cudaEventRecord(ke.last_fetch, t->h2d));
+      ke.fetched = true;
+      *out = id;
+      return;
+    }
     if (it == t->keys.end() || !it->second.stored) {
       tk.err = ACKPT_MISSING_KEY;  // storage.py:310-311
       tk.msg = "key " + std::to_string(key) + " never stored";
@@ -350,12 +590,18 @@ ACKPT_API int ackpt_tier_wait(ackpt_tier* t, ackpt_ticket ticket, int64_t* step_
     if (tk.err != ACKPT_OK) ackpt::fail(tk.err, tk.msg);
     ev = tk.complete ? nullptr : tk.done;
   });
-  if (rc != ACKPT_OK || !ev) return rc;
+  if (rc != ACKPT_OK) return rc;
   // Block without holding the lock (other threads may issue transfers).
   return ackpt::guard([&] {
-    ACKPT_CUDA_CHECK(cudaEventSynchronize(ev));
+    if (ev) ACKPT_CUDA_CHECK(cudaEventSynchronize(ev));
     std::lock_guard<std::mutex> lk(t->mu);
-    ackpt::retire(t, ackpt::get_ticket(t, ticket));
+    ackpt::TierTicket& tk = ackpt::get_ticket(t, ticket);
+    ackpt::retire(t, tk);
+    if (step_out) *step_out = tk.step;
+    if (tk.async) {  // file-stage errors, raised by the worker side (storage.py:271-278)
+      const int e = tk.async->err.load(std::memory_order_acquire);
+      if (e != ACKPT_OK) ackpt::fail(e, tk.async->msg);
+    }
   });
 }
 
@@ -391,6 +637,7 @@ ACKPT_API int ackpt_tier_contains(ackpt_tier* t, int64_t key, int32_t* out) {
     std::lock_guard<std::mutex> lk(t->mu);
     auto it = t->keys.find(key);
     *out = (it != t->keys.end() && it->second.stored) ? 1 : 0;
+    if (!*out && t->file_mode) *out = ackpt::file_payload_len(t, key) >= 0 ? 1 : 0;
   });
 }
 
@@ -398,6 +645,12 @@ ACKPT_API int ackpt_tier_key_bytes(ackpt_tier* t, int64_t key, int64_t* out) {
   return ackpt::guard([&] {
     std::lock_guard<std::mutex> lk(t->mu);
     auto it = t->keys.find(key);
+    if (t->file_mode && (it == t->keys.end() || !it->second.stored)) {
+      const int64_t len = ackpt::file_payload_len(t, key);
+      if (len < 0) ackpt::fail(ACKPT_MISSING_KEY, ackpt::ckpt_path(t, key));
+      *out = len;
+      return;
+    }
     if (it == t->keys.end() || !it->second.stored)
       ackpt::fail(ACKPT_MISSING_KEY, "key " + std::to_string(key) + " never stored");
     *out = it->second.len;
@@ -407,6 +660,7 @@ ACKPT_API int ackpt_tier_key_bytes(ackpt_tier* t, int64_t key, int64_t* out) {
 ACKPT_API int ackpt_tier_host_ptr(ackpt_tier* t, int64_t key, void** out) {
   return ackpt::guard([&] {
     std::lock_guard<std::mutex> lk(t->mu);
+    if (t->file_mode) ackpt::fail(ACKPT_VALUE_ERROR, "file-stage keys live on disk, not in pinned memory");
     auto it = t->keys.find(key);
     if (it == t->keys.end() || !it->second.stored)
       ackpt::fail(ACKPT_MISSING_KEY, "key " + std::to_string(key) + " never stored");

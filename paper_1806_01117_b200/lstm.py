@@ -33,7 +33,7 @@ from .runtime import (
     Strategy,
     execute,
 )
-from .storage import Level2Backend, PinnedHostBackend, SimulatedBackend, as_host_bytes
+from .storage import FileBackend, Level2Backend, PinnedHostBackend, SimulatedBackend, as_host_bytes
 
 _F8 = np.dtype("<f8")
 
@@ -324,8 +324,6 @@ def make_backend(config: Optional[dict], slot_bytes: Optional[int] = None) -> Op
     if kind == "pinned":
         return PinnedHostBackend(slot_bytes=slot_bytes)
     if kind == "file":
-        from .filestage import FileBackend
-
         return FileBackend(config.get("dir") or tempfile.mkdtemp(prefix="ckpt_"), slot_bytes=slot_bytes)
     raise ValueError(f"unknown backend kind {kind!r}")
 

@@ -251,14 +251,17 @@ class Level2Backend:
             raise RuntimeError("backend is closed")
         if self._handle is None:
             size = max(int(nbytes), int(self._slot_bytes or 0), 1)
-            h = C.c_void_p()
-            N.check(N.lib.ackpt_tier_create(self._capacity, size, C.byref(h)))
-            self._handle = h.value
+            self._handle = self._create_native(size)
             self._slot_bytes = size
             if self._latency or self._bandwidth:
                 N.check(N.lib.ackpt_tier_set_throttle(self._handle, float(self._latency), float(self._bandwidth)))
         # payloads larger than the slab slots get dedicated pinned buffers per key
         return self._handle
+
+    def _create_native(self, slot_bytes: int) -> int:
+        h = C.c_void_p()
+        N.check(N.lib.ackpt_tier_create(self._capacity, slot_bytes, C.byref(h)))
+        return h.value
 
     @property
     def native(self) -> Optional[int]:
@@ -343,6 +346,32 @@ class Level2Backend:
 
 class PinnedHostBackend(Level2Backend):
     """HBM <-> pinned host DRAM at full copy-engine speed (the product tier)."""
+
+
+class FileBackend(Level2Backend):
+    """Third stage: one CKPT file per key, ``<dir>/ckpt_<key>.bin``, in the
+    reference's byte format (storage.py:321-340, tmp + rename, CRC32C).
+    HBM -> pinned staging -> file on the D2H engine's stream, and back on the
+    H2D stream; the file I/O and checksum run natively off the compute path.
+    Corruption / truncation raise ChecksumMismatch, ENOSPC StorageFull, at
+    wait (or at the end of an execute() that used the backend).  Existing
+    files in the directory can be fetched (resume)."""
+
+    def __init__(self, directory, slot_bytes=None, device=None):
+        self.directory = Path(directory)
+        self.directory.mkdir(parents=True, exist_ok=True)
+        super().__init__(slot_bytes=slot_bytes, device=device)
+
+    def _create_native(self, slot_bytes: int) -> int:
+        h = C.c_void_p()
+        N.check(N.lib.ackpt_tier_create_file(str(self.directory).encode(), slot_bytes, C.byref(h)))
+        return h.value
+
+    def path_for(self, key: int) -> Path:
+        return self.directory / f"ckpt_{key}.bin"
+
+    def host_view(self, key: int):
+        raise ValueError("file-stage keys live on disk; read path_for(key)")
 
 
 class SimulatedBackend(Level2Backend):
