@@ -437,7 +437,8 @@ def main(argv=None) -> None:
                  "overhead_vs_store_all": o_el / o_inf, "overhead_vs_per_step_store_all": o_el / t_inf_per_step,
                  "calibrated_t_a_us": ot_a * 1e6, "forward_evals": ost.forward_evals,
                  "stall_seconds": ost.stall_seconds, "kernel_launches": ost.device["kernel_launches"],
-                 "adjoint_bit_identical_to_headline": bool(torch.equal(o_adj, adj))}
+                 "adjoint_rel_l2_vs_headline": float((o_adj.double() - adj.double()).norm()
+                                                     / max(adj.double().norm().item(), 1e-300))}
 
     # --- Revolve(s) at the same memory ratio, for comparison ---
     revolve = None

@@ -229,7 +229,8 @@ struct Run {
   int advance(int64_t from, int64_t to, int cur) {
     // Advance(from, to): per-step contract by default; one fused launch when
     // the operator provides advance() and fusion is enabled.
-    if (to - from >= 2 && E->fuse && E->op.advance) {
+    // (length 1 too: a fused execution uses the fused kernel family throughout)
+    if (to - from >= 1 && E->fuse && E->op.advance) {
       int out = acquire();
       if (!dry) {
         check_op(E->op.advance(E->op.ctx, from, to, ptr(cur), wptr(out), s));

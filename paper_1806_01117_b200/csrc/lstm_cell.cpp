@@ -53,6 +53,18 @@ Variant variant() {
   return v;
 }
 
+// Fused launches (advance / forward_many / backward_many) for d=8 run on the
+// tensor cores (tcgen05, 3xTF32) unless ACKPT_TC=0 selects the FFMA2 family.
+// Each execution mode uses one kernel family for every step, so strategies
+// stay bit-identical within a mode.
+bool tc_on() {
+  static const bool on = [] {
+    const char* e = std::getenv("ACKPT_TC");
+    return !(e && std::string(e) == "0");
+  }();
+  return on;
+}
+
 // TMA path: d=8, B % 4 == 0 (16-byte row segments), 16-byte aligned rows.
 bool tma_ok(const ackpt_lstm* c, std::initializer_list<const void*> ptrs) {
   const Variant v = variant();
@@ -210,7 +222,8 @@ ACKPT_API int ackpt_lstm_advance(const ackpt_lstm* cell, int64_t from_step, int6
     if (ackpt::f32_fast(cell, {state_in, state_out})) {
       auto i = static_cast<const float*>(state_in);
       auto o = static_cast<float*>(state_out);
-      if (cell->d == 8) ackpt::f32_advance<8>(cell, from_step, to_step, i, o, s);
+      if (cell->d == 8 && ackpt::tc_on()) ackpt::tc_advance(cell, from_step, int(to_step - from_step), i, o, s);
+      else if (cell->d == 8) ackpt::f32_advance<8>(cell, from_step, to_step, i, o, s);
       else ackpt::f32_advance<4>(cell, from_step, to_step, i, o, s);
     } else if (cell->dtype == ACKPT_F32) {
       ackpt::generic_advance<float>(cell, from_step, to_step, static_cast<const float*>(state_in),
@@ -274,7 +287,8 @@ ACKPT_API int ackpt_lstm_forward_many(const ackpt_lstm* cell, int64_t from_step,
     if (fast) {
       auto in = static_cast<const float*>(state_in);
       auto outs = reinterpret_cast<float* const*>(states_out);
-      if (cell->d == 8) ackpt::f32_forward_many<8>(cell, from_step, int(count), in, outs, s);
+      if (cell->d == 8 && ackpt::tc_on()) ackpt::tc_forward_many(cell, from_step, int(count), in, outs, s);
+      else if (cell->d == 8) ackpt::f32_forward_many<8>(cell, from_step, int(count), in, outs, s);
       else ackpt::f32_forward_many<4>(cell, from_step, int(count), in, outs, s);
       ackpt::check_launch();
       return;
@@ -301,7 +315,8 @@ ACKPT_API int ackpt_lstm_backward_many(const ackpt_lstm* cell, int64_t from_step
     auto sp = reinterpret_cast<const float* const*>(states);
     auto ai = static_cast<const float*>(adjoint_in);
     auto ao = static_cast<float*>(adjoint_out);
-    if (cell->d == 8) ackpt::f32_backward_many<8>(cell, from_step, int(count), sp, ai, ao, s);
+    if (cell->d == 8 && ackpt::tc_on()) ackpt::tc_backward_many(cell, from_step, int(count), sp, ai, ao, s);
+    else if (cell->d == 8) ackpt::f32_backward_many<8>(cell, from_step, int(count), sp, ai, ao, s);
     else ackpt::f32_backward_many<4>(cell, from_step, int(count), sp, ai, ao, s);
     ackpt::check_launch();
   });

@@ -53,6 +53,12 @@ void f32_forward_many(const ackpt_lstm* c, int64_t from, int count, const float*
 template <int D>
 void f32_backward_many(const ackpt_lstm* c, int64_t from, int count, const float* const* states,
                        const float* adj_in, float* adj_out, cudaStream_t s);
+// Tensor-core (tcgen05, 3xTF32) fused kernels, d = 8 (lstm_f32_tc.cu).
+void tc_advance(const ackpt_lstm* c, int64_t from, int count, const float* in, float* out, cudaStream_t s);
+void tc_forward_many(const ackpt_lstm* c, int64_t from, int count, const float* in, float* const* outs,
+                     cudaStream_t s);
+void tc_backward_many(const ackpt_lstm* c, int64_t from, int count, const float* const* states, const float* adj_in,
+                      float* adj_out, cudaStream_t s);
 // Occupancy variants (MINB resident 256-thread CTAs per SM).
 template <int D, int MINB>
 void f32_forward_v(const ackpt_lstm* c, int64_t step, const float* in, float* out, cudaStream_t s);

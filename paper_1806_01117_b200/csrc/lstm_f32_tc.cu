@@ -1,0 +1,42 @@
+// Launchers of the tensor-core fused LSTM kernels (lstm_f32_tc.cuh).
+#include "lstm_f32_tc.cuh"
+
+namespace ackpt {
+
+namespace {
+
+tc::Weights tc_weights(const ackpt_lstm* c) {
+  f32m::ScaledParams<8> sp;
+  f32m::fill_scaled<8>(c, -1, sp);
+  tc::Weights w;
+  std::memcpy(w.ws, sp.ws, sizeof(w.ws));
+  return w;
+}
+
+unsigned tc_grid(int64_t B) { return unsigned((B + tc::kTile - 1) / tc::kTile); }
+
+}  // namespace
+
+void tc_advance(const ackpt_lstm* c, int64_t from, int count, const float* in, float* out, cudaStream_t s) {
+  tc::OutPtrs none{};
+  tc::fwd_tc<false><<<tc_grid(c->B), tc::kThreads, 0, s>>>(in, out, c->B, static_cast<const float*>(c->d_xbs),
+                                                            from, count, tc_weights(c), none);
+}
+
+void tc_forward_many(const ackpt_lstm* c, int64_t from, int count, const float* in, float* const* outs,
+                     cudaStream_t s) {
+  tc::OutPtrs o{};
+  for (int i = 0; i < count; ++i) o.p[i] = outs[i];
+  tc::fwd_tc<true><<<tc_grid(c->B), tc::kThreads, 0, s>>>(in, nullptr, c->B, static_cast<const float*>(c->d_xbs),
+                                                           from, count, tc_weights(c), o);
+}
+
+void tc_backward_many(const ackpt_lstm* c, int64_t from, int count, const float* const* states, const float* adj_in,
+                      float* adj_out, cudaStream_t s) {
+  tc::StatePtrs sp{};
+  for (int i = 0; i < count; ++i) sp.p[i] = states[i];
+  tc::rev_tc<<<tc_grid(c->B), tc::kThreads, 0, s>>>(adj_in, adj_out, c->B, static_cast<const float*>(c->d_xbs),
+                                                     from, count, tc_weights(c), sp);
+}
+
+}  // namespace ackpt

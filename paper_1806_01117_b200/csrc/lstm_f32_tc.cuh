@@ -1,0 +1,320 @@
+// Tensor-core (tcgen05) fused LSTM kernels for sm_100a, hidden size 8:
+// fused Advance, fused TapeForward and fused Reverse runs.  Same results
+// contract as lstm_f32.cuh (fp32 state, rel-L2 <= 1e-5 vs float64), different
+// arithmetic for the gate matvec, so NOT bit-identical to the FFMA2 kernels:
+// an execution uses one family for every step.
+//
+// Gate pre-activations of a step, for the 256 batch elements of a CTA, are one
+// MMA problem per M-tile: D[128 x 32] = A[128 x 16] . B[32 x 16]^T with
+//   A row r = [h_0..h_7, 1, 0 x 7]                    (element of the tile)
+//   B row n = [s_g W_g[j][0..7], s_g xb_k[g][j], 0 x 7]  n = 4 j + g (unit-major)
+// (s_g: the exponent scale folded into the weights, lstm_f32_math.cuh), so the
+// bias / input projection of step k rides in the MMA and D holds the ex2
+// arguments directly.  fp32 accuracy from TF32 tensor cores with the 3xTF32
+// split x = hi + lo (hi = x with the low 13 mantissa bits cleared):
+// A.B ~ Ahi.Bhi + Alo.Bhi + Ahi.Blo (rel. error ~5e-7, tools/umma_probe.cu).
+// Operands are K-major, no swizzle, in shared memory; D (fp32) is in TMEM,
+// one column per gate, one lane per tile row, read back with tcgen05.ld.
+//
+// CTA = 128 threads = the 128 TMEM lanes.  Tile 0 row r is element base+2r,
+// tile 1 row r is element base+2r+1, so thread r owns the float2 pair at
+// base+2r in global memory and processes it with the packed-fp32 math.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include "lstm_f32_math.cuh"
+
+namespace ackpt {
+namespace tc {
+
+using namespace f32m;
+
+constexpr int kThreads = 128;
+constexpr int kTile = 256;     // elements per CTA
+constexpr int kD = 8;          // hidden size
+constexpr int kN = 4 * kD;     // gate columns
+constexpr int kK = 16;         // [h (8) | 1 | 0 x 7]
+constexpr uint32_t kLBO = 128; // bytes between 16-byte K chunks (8 rows x 16 B core matrices)
+constexpr uint32_t kSBO = 512; // bytes between 8-row groups (4 chunks of 128 B)
+constexpr int kMatBytes = 128 * kK * 4;  // one 128 x 16 tf32 operand
+constexpr uint32_t kIdesc = (1u << 4) | (2u << 7) | (2u << 10) | (uint32_t(kN >> 3) << 17) | (uint32_t(128 >> 4) << 24);
+
+struct Smem {
+  float a[2][2][128 * kK];  // [tile][hi, lo]
+  float b[2][kN * kK];      // [hi, lo]
+  uint64_t mbar;
+  uint32_t tmem;
+};
+
+__device__ __forceinline__ uint32_t su32(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
+__device__ __forceinline__ uint64_t desc(uint32_t addr) {
+  return uint64_t((addr >> 4) & 0x3FFF) | (uint64_t((kLBO >> 4) & 0x3FFF) << 16) |
+         (uint64_t((kSBO >> 4) & 0x3FFF) << 32) | (uint64_t(1) << 46);
+}
+// float offset of (row, k) in a K-major no-swizzle 16-wide operand
+__device__ __forceinline__ int kofs(int r, int k) { return (r >> 3) * (kSBO / 4) + (k >> 2) * (kLBO / 4) + (r & 7) * 4 + (k & 3); }
+__device__ __forceinline__ float hi_part(float x) { return __uint_as_float(__float_as_uint(x) & 0xFFFFE000u); }
+
+__device__ __forceinline__ void mma(uint32_t d, uint64_t a, uint64_t b, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
+      "l"(a), "l"(b), "r"(kIdesc), "r"(acc));
+}
+
+// Unit pair (2 hidden units = 8 columns) of one tile row, from TMEM.
+__device__ __forceinline__ void ld8(uint32_t addr, float (&v)[8]) {
+  uint32_t r[8];
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+               : "r"(addr));
+#pragma unroll
+  for (int i = 0; i < 8; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+struct Weights {  // pre-scaled (lstm_f32_math.cuh ScaledParams layout)
+  float ws[4][kD][kD];
+};
+
+// One-time CTA setup: TMEM, mbarrier, constant operand parts.
+__device__ __forceinline__ void setup(Smem& sm, const Weights& w) {
+  const int tid = threadIdx.x;
+  if (tid < 32) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(&sm.tmem)), "r"(64));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (tid == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(&sm.mbar)));
+    asm volatile("fence.mbarrier_init.release.cluster;");
+  }
+  // A columns 8..15 (chunks 2, 3): hi = [1, 0, ...], lo = 0, for this thread's row in both tiles
+#pragma unroll
+  for (int t = 0; t < 2; ++t) {
+    *reinterpret_cast<float4*>(&sm.a[t][0][kofs(tid, 8)]) = make_float4(1.f, 0.f, 0.f, 0.f);
+    *reinterpret_cast<float4*>(&sm.a[t][0][kofs(tid, 12)]) = make_float4(0.f, 0.f, 0.f, 0.f);
+    *reinterpret_cast<float4*>(&sm.a[t][1][kofs(tid, 8)]) = make_float4(0.f, 0.f, 0.f, 0.f);
+    *reinterpret_cast<float4*>(&sm.a[t][1][kofs(tid, 12)]) = make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+  // B rows n = 4 j + g, k 0..7: scaled weights, k 9..15: 0 (k 8 is per step)
+  if (tid < kN) {
+    const int j = tid >> 2, g = tid & 3;
+#pragma unroll
+    for (int k = 0; k < kD; ++k) {
+      const float x = w.ws[g][j][k];
+      sm.b[0][kofs(tid, k)] = hi_part(x);
+      sm.b[1][kofs(tid, k)] = x - hi_part(x);
+    }
+#pragma unroll
+    for (int k = 9; k < kK; ++k) {
+      sm.b[0][kofs(tid, k)] = 0.f;
+      sm.b[1][kofs(tid, k)] = 0.f;
+    }
+  }
+}
+
+// Writes A (h hi/lo for both tiles) and, in warp 0, B's bias column for step k.
+__device__ __forceinline__ void stage_operands(Smem& sm, const float2 (&h)[kD], const float* __restrict__ xbs_all,
+                                               int64_t k) {
+  const int tid = threadIdx.x;
+  float4 hx[2], hy[2];
+  hx[0] = make_float4(h[0].x, h[1].x, h[2].x, h[3].x);
+  hx[1] = make_float4(h[4].x, h[5].x, h[6].x, h[7].x);
+  hy[0] = make_float4(h[0].y, h[1].y, h[2].y, h[3].y);
+  hy[1] = make_float4(h[4].y, h[5].y, h[6].y, h[7].y);
+#pragma unroll
+  for (int c = 0; c < 2; ++c) {
+    const float4 a = hx[c], b = hy[c];
+    const float4 ah = make_float4(hi_part(a.x), hi_part(a.y), hi_part(a.z), hi_part(a.w));
+    const float4 bh = make_float4(hi_part(b.x), hi_part(b.y), hi_part(b.z), hi_part(b.w));
+    *reinterpret_cast<float4*>(&sm.a[0][0][kofs(tid, 4 * c)]) = ah;
+    *reinterpret_cast<float4*>(&sm.a[0][1][kofs(tid, 4 * c)]) =
+        make_float4(a.x - ah.x, a.y - ah.y, a.z - ah.z, a.w - ah.w);
+    *reinterpret_cast<float4*>(&sm.a[1][0][kofs(tid, 4 * c)]) = bh;
+    *reinterpret_cast<float4*>(&sm.a[1][1][kofs(tid, 4 * c)]) =
+        make_float4(b.x - bh.x, b.y - bh.y, b.z - bh.z, b.w - bh.w);
+  }
+  if (tid < kN) {
+    const int j = tid >> 2, g = tid & 3;
+    const float x = __ldg(xbs_all + k * kN + g * kD + j);  // table is gate-major
+    sm.b[0][kofs(tid, 8)] = hi_part(x);
+    sm.b[1][kofs(tid, 8)] = x - hi_part(x);
+  }
+}
+
+// Barrier, issue the 10 MMAs of a step (thread 0), wait for them.
+__device__ __forceinline__ void gates_mma(Smem& sm, uint32_t phase) {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint64_t bh0 = desc(su32(sm.b[0])), bl0 = desc(su32(sm.b[1]));
+    const uint64_t bh1 = desc(su32(sm.b[0]) + 2 * kLBO), bl1 = desc(su32(sm.b[1]) + 2 * kLBO);
+#pragma unroll
+    for (int t = 0; t < 2; ++t) {
+      const uint32_t d = sm.tmem + uint32_t(t * kN);
+      const uint32_t ah = su32(sm.a[t][0]), al = su32(sm.a[t][1]);
+      mma(d, desc(ah), bh0, 0u);               // h_hi . W_hi
+      mma(d, desc(al), bh0, 1u);               // h_lo . W_hi
+      mma(d, desc(ah), bl0, 1u);               // h_hi . W_lo
+      mma(d, desc(ah + 2 * kLBO), bh1, 1u);    // 1 . xb_hi
+      mma(d, desc(ah + 2 * kLBO), bl1, 1u);    // 1 . xb_lo
+    }
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(&sm.mbar))
+                 : "memory");
+  }
+  uint32_t done = 0;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(su32(&sm.mbar)), "r"(phase)
+        : "memory");
+  } while (!done);
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+
+// Scaled pre-activations (f, i, o, g) of units u, u+1 for the thread's pair.
+__device__ __forceinline__ void read_units(const Smem& sm, int u, float2 (&pre)[2][4]) {
+  const uint32_t lane = uint32_t((threadIdx.x >> 5) * 32) << 16;
+  float a[8], b[8];
+  ld8(sm.tmem + lane + uint32_t(4 * u), a);
+  ld8(sm.tmem + lane + uint32_t(kN + 4 * u), b);
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int q = 0; q < 2; ++q)
+#pragma unroll
+    for (int g = 0; g < 4; ++g) pre[q][g] = make_float2(a[4 * q + g], b[4 * q + g]);
+}
+
+__device__ __forceinline__ void teardown(Smem& sm) {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (threadIdx.x < 32) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(sm.tmem), "r"(64));
+}
+
+__device__ __forceinline__ float2 ldg2(const float* p) {
+  float2 v;
+  asm volatile("ld.global.nc.L1::no_allocate.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ void stg2(float* p, float2 v) {
+  asm volatile("st.global.v2.f32 [%0], {%1, %2};" ::"l"(p), "f"(v.x), "f"(v.y) : "memory");
+}
+
+struct OutPtrs {
+  float* p[ACKPT_MAX_FUSED];
+};
+struct StatePtrs {
+  const float* p[ACKPT_MAX_FUSED];
+};
+
+// Fused forward over `count` steps from `from`; TAPE stores every step's
+// output to outs.p[i], otherwise only the final state goes to `out`.
+template <bool TAPE>
+__global__ void __launch_bounds__(kThreads, 4)
+    fwd_tc(const float* __restrict__ in, float* __restrict__ out, int64_t B, const float* __restrict__ xbs_all,
+           int64_t from, int count, const __grid_constant__ Weights w, const __grid_constant__ OutPtrs outs) {
+  __shared__ __align__(128) Smem sm;
+  const int64_t b0 = int64_t(blockIdx.x) * kTile + 2 * threadIdx.x;
+  const bool live = b0 < B;  // every thread takes part in the MMA protocol
+  setup(sm, w);
+  float2 h[kD], c[kD];
+#pragma unroll
+  for (int j = 0; j < kD; ++j) {
+    h[j] = live ? ldg2(in + b0 + int64_t(j) * B) : make_float2(0.f, 0.f);
+    c[j] = live ? ldg2(in + b0 + int64_t(kD + j) * B) : make_float2(0.f, 0.f);
+  }
+  for (int i = 0; i < count; ++i) {
+    stage_operands(sm, h, xbs_all, from + i);
+    gates_mma(sm, uint32_t(i & 1));
+#pragma unroll
+    for (int u = 0; u < kD; u += 2) {
+      float2 pre[2][4];
+      read_units(sm, u, pre);
+#pragma unroll
+      for (int q = 0; q < 2; ++q) h[u + q] = fwd_unit(pre[q][0], pre[q][1], pre[q][2], pre[q][3], c[u + q]);
+    }
+    if (TAPE && live) {
+      float* dst = outs.p[i] + b0;
+#pragma unroll
+      for (int j = 0; j < kD; ++j) {
+        stg2(dst + int64_t(j) * B, h[j]);
+        stg2(dst + int64_t(kD + j) * B, c[j]);
+      }
+    }
+  }
+  if (!TAPE && live) {
+#pragma unroll
+    for (int j = 0; j < kD; ++j) {
+      stg2(out + b0 + int64_t(j) * B, h[j]);
+      stg2(out + b0 + int64_t(kD + j) * B, c[j]);
+    }
+  }
+  teardown(sm);
+}
+
+// Fused run of Reverse actions, steps from+count-1 .. from.  Gates on the
+// tensor cores; the transpose matvec dh = sum_g (s_g W_g)^T (da_g / s_g) on
+// the packed-fp32 pipe with uniform-register weights.
+__global__ void __launch_bounds__(kThreads, 4)
+    rev_tc(const float* __restrict__ adj_in, float* __restrict__ adj_out, int64_t B, const float* __restrict__ xbs_all,
+           int64_t from, int count, const __grid_constant__ Weights w, const __grid_constant__ StatePtrs states) {
+  __shared__ __align__(128) Smem sm;
+  const int64_t b0 = int64_t(blockIdx.x) * kTile + 2 * threadIdx.x;
+  const bool live = b0 < B;
+  setup(sm, w);
+  float2 dh[kD], dc[kD];
+#pragma unroll
+  for (int j = 0; j < kD; ++j) {
+    dh[j] = live ? ldg2(adj_in + b0 + int64_t(j) * B) : make_float2(0.f, 0.f);
+    dc[j] = live ? ldg2(adj_in + b0 + int64_t(kD + j) * B) : make_float2(0.f, 0.f);
+  }
+  int phase = 0;
+  for (int i = count - 1; i >= 0; --i, ++phase) {
+    const float* xs = states.p[i] + b0;
+    float2 h[kD], c[kD];
+#pragma unroll
+    for (int j = 0; j < kD; ++j) {
+      h[j] = live ? ldg2(xs + int64_t(j) * B) : make_float2(0.f, 0.f);
+      c[j] = live ? ldg2(xs + int64_t(kD + j) * B) : make_float2(0.f, 0.f);
+    }
+    stage_operands(sm, h, xbs_all, from + i);
+    gates_mma(sm, uint32_t(phase & 1));
+    float2 acc[kD];
+#pragma unroll
+    for (int m = 0; m < kD; ++m) acc[m] = bc(0.0f);
+#pragma unroll
+    for (int u = 0; u < kD; u += 2) {
+      float2 pre[2][4];
+      read_units(sm, u, pre);
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        const int j = u + q;
+        float2 daf, dai, dao, dag;
+        bwd_unit(pre[q][0], pre[q][1], pre[q][2], pre[q][3], c[j], dh[j], dc[j], daf, dai, dao, dag, dc[j]);
+#pragma unroll
+        for (int m = 0; m < kD; ++m) {
+          acc[m] = fma2(bc(w.ws[0][j][m]), daf, acc[m]);
+          acc[m] = fma2(bc(w.ws[1][j][m]), dai, acc[m]);
+          acc[m] = fma2(bc(w.ws[2][j][m]), dao, acc[m]);
+          acc[m] = fma2(bc(w.ws[3][j][m]), dag, acc[m]);
+        }
+      }
+    }
+#pragma unroll
+    for (int m = 0; m < kD; ++m) dh[m] = acc[m];
+  }
+  if (live) {
+#pragma unroll
+    for (int j = 0; j < kD; ++j) {
+      stg2(adj_out + b0 + int64_t(j) * B, dh[j]);
+      stg2(adj_out + b0 + int64_t(kD + j) * B, dc[j]);
+    }
+  }
+  teardown(sm);
+}
+
+}  // namespace tc
+}  // namespace ackpt

@@ -100,38 +100,60 @@ def test_seed_and_loss(P):
         assert L.rel_l2(losses, L.loss(ocell, x.astype(npdt).astype(np.float64))) <= tol
 
 
+def _tensor_core_family(d, batch, dtype):
+    # fused d=8 fp32 launches (even batch) run on tcgen05 with the 3xTF32 split
+    return d == 8 and dtype == "f32" and batch % 2 == 0
+
+
 @pytest.mark.parametrize("d,batch,dtype", [(8, 4096, "f32"), (4, 512, "f32"), (8, 7, "f32"), (6, 64, "f64")])
-def test_fused_advance_equals_step_chain(P, d, batch, dtype):
+def test_fused_advance(P, d, batch, dtype):
     cell, ocell = _cells(P, d, 12, 21)
     npdt = np.float64 if dtype == "f64" else np.float32
     x = torch.from_numpy(_states(d, 8, batch).astype(npdt)).cuda()
     dc = P.device_cell(cell, batch, dtype)
-    chain = x
-    for k in range(2, 11):
-        chain = dc.forward(k, chain)
     fused = dc.advance(2, 11, x)
-    # identical arithmetic per step: bit-identical results
-    assert torch.equal(fused, chain)
+    if _tensor_core_family(d, batch, dtype):
+        ref = x.double().cpu().numpy()
+        for k in range(2, 11):
+            ref = L.forward_step(ocell, k, ref)
+        assert L.rel_l2(fused.cpu().numpy(), ref) <= F32_TOL
+        # same family: the fused tape's last output is the fused advance, bit for bit
+        assert torch.equal(dc.forward_many(2, 9, x)[-1], fused)
+    else:
+        chain = x
+        for k in range(2, 11):
+            chain = dc.forward(k, chain)
+        assert torch.equal(fused, chain)  # identical arithmetic per step
 
 
-@pytest.mark.parametrize("d,batch", [(8, 4096), (4, 512), (8, 1002)])
-def test_fused_tape_and_reverse_equal_step_chains(P, d, batch):
-    cell, _ = _cells(P, d, 70, 22)
+@pytest.mark.parametrize("d,batch", [(8, 4096), (4, 512), (8, 1002), (8, 300)])
+def test_fused_tape_and_reverse(P, d, batch):
+    cell, ocell = _cells(P, d, 70, 22)
     x = torch.from_numpy(_states(d, 9, batch).astype(np.float32)).cuda()
     a = torch.from_numpy(_states(d, 10, batch).astype(np.float32)).cuda()
     dc = P.device_cell(cell, batch, "f32")
     outs = dc.forward_many(3, 64, x)
-    chain, states = x, [x]
-    for k in range(3, 67):
-        chain = dc.forward(k, chain)
-        states.append(chain)
-    for got, want in zip(outs, states[1:]):
-        assert torch.equal(got, want)
-    fused = dc.backward_many(3, states[:64], a)
-    adj = a
-    for k in range(66, 2, -1):
-        adj = dc.backward(k, states[k - 3], adj)
-    assert torch.equal(fused, adj)
+    states = [x] + outs[:-1]  # input state of steps 3..66
+    fused = dc.backward_many(3, states, a)
+    if _tensor_core_family(d, batch, "f32"):
+        ref = x.double().cpu().numpy()
+        for i, k in enumerate(range(3, 67)):
+            ref = L.forward_step(ocell, k, ref)
+            assert L.rel_l2(outs[i].cpu().numpy(), ref) <= F32_TOL, (k, L.rel_l2(outs[i].cpu().numpy(), ref))
+        adj = a.double().cpu().numpy()
+        for i, k in reversed(list(enumerate(range(3, 67)))):
+            adj = L.backward_step(ocell, k, states[i].double().cpu().numpy(), adj)
+        assert L.rel_l2(fused.cpu().numpy(), adj) <= F32_TOL
+        assert torch.equal(dc.advance(3, 67, x), outs[-1])
+    else:
+        chain = x
+        for k in range(3, 67):
+            chain = dc.forward(k, chain)
+            assert torch.equal(outs[k - 3], chain)
+        adj = a
+        for k in range(66, 2, -1):
+            adj = dc.backward(k, states[k - 3], adj)
+        assert torch.equal(fused, adj)
 
 
 def test_c2_shape_kernels_on_sampled_rows(P):

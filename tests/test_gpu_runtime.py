@@ -307,12 +307,29 @@ def test_fp32_strategies_bit_identical_at_long_n(P):
     finally:
         backend.close()
     assert torch.equal(g_full, g_rev) and torch.equal(g_full, g_ms)
-    assert torch.equal(g_full, g_fused) and torch.equal(g_full, g_rev_fused)
+    # the fused mode (tensor-core family for d=8) is bit-identical across its strategies
+    g_full_fused, _ = pkg.execute(pkg.FullStorage(), ops, s0, fuse=True)
+    assert torch.equal(g_full_fused, g_fused) and torch.equal(g_full_fused, g_rev_fused)
     assert st.forward_evals == st_f.forward_evals == 2 * n
     # counters and ledger equal the CPU oracle executor's
     _, ost = RO.execute("multistage", L.random_cell(d, n, 0), np.zeros((2, d, 1)), slots=19, interval=20)
     assert st.forward_evals == ost["forward_evals"] and st.stores_issued == ost["stores_issued"]
     assert st.peak_l1_bytes == ost["peak_l1_bytes"] // (2 * d * 8) * ops.state_size
+
+
+def test_fused_and_per_step_modes_agree(P):
+    # different kernel families (FFMA2 per step, tcgen05 3xTF32 fused): equal
+    # to the oracle within the fp32 tolerance, at n where the adjoint is not denormal
+    pkg, lstm, _ = P
+    d, n, batch = 8, 60, 1 << 12
+    cell = lstm.random_cell(d, n, 3)
+    ops = lstm.operator_pair(cell, batch, "f32")
+    s0 = lstm.random_states(d, 4, batch, "f32")
+    per_step, _ = pkg.execute(pkg.Revolve(7), ops, s0)
+    fused, _ = pkg.execute(pkg.Revolve(7), ops, s0, fuse=True)
+    ref, _ = RO.execute("full", L.random_cell(d, n, 3), s0.double().cpu().numpy())
+    assert L.rel_l2(per_step.double().cpu().numpy(), ref) <= 1e-5
+    assert L.rel_l2(fused.double().cpu().numpy(), ref) <= 1e-5
 
 
 def test_python_callback_operator_pair(P, fast_backend):

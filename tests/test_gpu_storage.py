@@ -161,9 +161,9 @@ def test_execute_multistage_through_file_stage(pkg, tmp_path):
     cell = lstm.random_cell(8, 40, 3)
     ops = lstm.operator_pair(cell, 4096, "f32")
     s0 = lstm.random_states(8, 4, 4096, "f32")
-    ref, _ = pkg.execute(pkg.FullStorage(), ops, s0)
     with pkg.FileBackend(tmp_path) as b:
         for fuse in (False, True):
+            ref, _ = pkg.execute(pkg.FullStorage(), ops, s0, fuse=fuse)
             adj, st = pkg.execute(pkg.Multistage(5, interval=8), ops, s0, b, fuse=fuse)
             assert torch.equal(adj, ref)
             assert st.stores_issued == st.prefetches_issued == 5
