@@ -86,6 +86,72 @@ __device__ __forceinline__ float2 tanh2(float2 x) {
   return fma2(rcp2(y), bc(-2.0f), bc(1.0f));
 }
 
+// ---- Newton-Raphson variants (tensor-core family) ------------------------
+// With the matvec on the tensor cores the FMA pipe idles while MUFU (16/clk/SM)
+// saturates, so reciprocals move to the FMA pipe: a bit-trick seed (<= 12 %
+// error) and three Newton steps r <- r (2 - y r) reach ~1 ulp for any normal
+// y >= 1 (the only arguments here).
+__device__ __forceinline__ float2 rcp2_nr(float2 y) {
+  float2 r = make_float2(__int_as_float(0x7EF311C3 - __float_as_int(y.x)),
+                         __int_as_float(0x7EF311C3 - __float_as_int(y.y)));
+#pragma unroll
+  for (int it = 0; it < 3; ++it) r = mul2(r, fma2(neg(y), r, bc(2.0f)));
+  return r;
+}
+
+__device__ __forceinline__ void activate_nr(float2 tf, float2 ti, float2 to, float2 tg, float2& f, float2& i,
+                                            float2& o, float2& g) {
+  const float2 one = bc(1.0f);
+  const float2 yf = add2(ex2_2(tf), one), yi = add2(ex2_2(ti), one);
+  const float2 yo = add2(ex2_2(to), one), yg = add2(ex2_2(tg), one);
+  const float2 p12 = mul2(yf, yi), p34 = mul2(yo, yg);
+  const float2 P = mul2(p12, p34);
+  if (__builtin_expect(P.x <= 3.0e38f && P.y <= 3.0e38f, 1)) {
+    const float2 r = rcp2_nr(P);
+    const float2 q34 = mul2(r, p34), q12 = mul2(r, p12);
+    f = mul2(q34, yi);
+    i = mul2(q34, yf);
+    o = mul2(q12, yg);
+    g = fma2(mul2(q12, yo), bc(-2.0f), one);
+  } else {
+    f = rcp2(yf);
+    i = rcp2(yi);
+    o = rcp2(yo);
+    g = fma2(rcp2(yg), bc(-2.0f), one);
+  }
+}
+
+// tanh with the exponent argument clamped at 64 so 1 + 2^t stays finite for
+// the Newton reciprocal (tanh rounds to 1.0f long before).
+__device__ __forceinline__ float2 tanh2_nr(float2 x) {
+  const float2 t = mul2(x, bc(2.0f * kL2e));
+  const float2 y = add2(make_float2(ex2(fminf(t.x, 64.0f)), ex2(fminf(t.y, 64.0f))), bc(1.0f));
+  return fma2(rcp2_nr(y), bc(-2.0f), bc(1.0f));
+}
+
+__device__ __forceinline__ float2 fwd_unit_nr(float2 af, float2 ai, float2 ao, float2 ag, float2& c) {
+  float2 f, ig, o, g;
+  activate_nr(af, ai, ao, ag, f, ig, o, g);
+  c = fma2(f, c, mul2(ig, g));
+  return mul2(o, tanh2_nr(c));
+}
+
+__device__ __forceinline__ void bwd_unit_nr(float2 af, float2 ai, float2 ao, float2 ag, float2 c, float2 dhn,
+                                            float2 dcn, float2& daf, float2& dai, float2& dao, float2& dag,
+                                            float2& dck) {
+  float2 f, ig, o, g;
+  activate_nr(af, ai, ao, ag, f, ig, o, g);
+  const float2 cn = fma2(f, c, mul2(ig, g));
+  const float2 t = tanh2_nr(cn);
+  const float2 dco = fma2(mul2(dhn, o), fma2(neg(t), t, bc(1.0f)), dcn);
+  const float2 dcs = mul2(dco, bc(-kLn2));
+  daf = mul2(mul2(dcs, c), fma2(neg(f), f, f));
+  dai = mul2(mul2(dcs, g), fma2(neg(ig), ig, ig));
+  dao = mul2(mul2(dhn, mul2(t, bc(-kLn2))), fma2(neg(o), o, o));
+  dag = mul2(mul2(dco, mul2(ig, bc(0.5f * kLn2))), fma2(neg(g), g, bc(1.0f)));
+  dck = mul2(dco, f);
+}
+
 // Weights pre-scaled per gate (see file comment).
 template <int D>
 struct ScaledParams {

@@ -234,7 +234,7 @@ __global__ void __launch_bounds__(kThreads, 4)
       float2 pre[2][4];
       read_units(sm, u, pre);
 #pragma unroll
-      for (int q = 0; q < 2; ++q) h[u + q] = fwd_unit(pre[q][0], pre[q][1], pre[q][2], pre[q][3], c[u + q]);
+      for (int q = 0; q < 2; ++q) h[u + q] = fwd_unit_nr(pre[q][0], pre[q][1], pre[q][2], pre[q][3], c[u + q]);
     }
     if (TAPE && live) {
       float* dst = outs.p[i] + b0;
@@ -293,7 +293,7 @@ __global__ void __launch_bounds__(kThreads, 4)
       for (int q = 0; q < 2; ++q) {
         const int j = u + q;
         float2 daf, dai, dao, dag;
-        bwd_unit(pre[q][0], pre[q][1], pre[q][2], pre[q][3], c[j], dh[j], dc[j], daf, dai, dao, dag, dc[j]);
+        bwd_unit_nr(pre[q][0], pre[q][1], pre[q][2], pre[q][3], c[j], dh[j], dc[j], daf, dai, dao, dag, dc[j]);
 #pragma unroll
         for (int m = 0; m < kD; ++m) {
           acc[m] = fma2(bc(w.ws[0][j][m]), daf, acc[m]);
