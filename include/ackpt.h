@@ -171,6 +171,13 @@ typedef struct ackpt_operator {
 /* Fills *out with the built-in LSTM operator bound to cell. */
 ACKPT_API int ackpt_lstm_operator(ackpt_lstm* cell, ackpt_operator* out);
 
+/* Kernel family of the fused d=8 fp32 launches (advance / forward_many /
+ * backward_many): 0 = packed FFMA2 (default), 1 = tcgen05 tensor cores with
+ * the 3xTF32 split.  Families differ in rounding (both within the fp32
+ * tolerance); switch only between executions.  Env ACKPT_TC=1 sets 1. */
+ACKPT_API int ackpt_set_fused_family(int32_t family);
+ACKPT_API int32_t ackpt_get_fused_family(void);
+
 /* Latency injection (test support, pkg/tests/test_runtime.py:33-52 pad_operators):
  * *out wraps base so each forward / backward call first holds the stream for
  * the given seconds with a device-side delay kernel.  Release with

@@ -144,6 +144,8 @@ _SIGS = {
     "ackpt_lstm_seed": ([_vp, _vp, _vp, _vp], C.c_int),
     "ackpt_lstm_loss": ([_vp, _vp, _vp, _vp], C.c_int),
     "ackpt_lstm_operator": ([_vp, C.POINTER(Operator)], C.c_int),
+    "ackpt_set_fused_family": ([C.c_int32], C.c_int),
+    "ackpt_get_fused_family": ([], C.c_int32),
     "ackpt_pad_operator_create": ([C.POINTER(Operator), C.c_double, C.c_double, C.POINTER(Operator)], C.c_int),
     "ackpt_pad_operator_destroy": ([C.POINTER(Operator)], C.c_int),
     "ackpt_tier_create": ([C.c_int64, C.c_int64, C.POINTER(_vp)], C.c_int),

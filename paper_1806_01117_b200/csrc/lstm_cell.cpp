@@ -2,6 +2,7 @@
 #include "lstm_cell.h"
 
 #include <algorithm>
+#include <atomic>
 #include <cstdlib>
 #include <cstring>
 #include <memory>
@@ -54,15 +55,20 @@ Variant variant() {
 }
 
 // Fused launches (advance / forward_many / backward_many) for d=8 run on the
-// tensor cores (tcgen05, 3xTF32) unless ACKPT_TC=0 selects the FFMA2 family.
+// packed-FFMA2 family by default; ACKPT_TC=1 selects the tensor-core family
+// (tcgen05, 3xTF32).  Measured at the C2 shape the tcgen05 kernels are not
+// faster yet (MUFU-bound activations, exposed MMA latency).
 // Each execution mode uses one kernel family for every step, so strategies
 // stay bit-identical within a mode.
+std::atomic<int> g_family{-1};  // -1: not yet read from the environment
 bool tc_on() {
-  static const bool on = [] {
+  int f = g_family.load(std::memory_order_relaxed);
+  if (f < 0) {
     const char* e = std::getenv("ACKPT_TC");
-    return !(e && std::string(e) == "0");
-  }();
-  return on;
+    f = (e && std::string(e) == "1") ? 1 : 0;
+    g_family.store(f, std::memory_order_relaxed);
+  }
+  return f == 1;
 }
 
 // TMA path: d=8, B % 4 == 0 (16-byte row segments), 16-byte aligned rows.
@@ -349,6 +355,15 @@ ACKPT_API int ackpt_lstm_loss(const ackpt_lstm* cell, const void* final_state, v
     ackpt::check_launch();
   });
 }
+
+ACKPT_API int ackpt_set_fused_family(int32_t family) {
+  return ackpt::guard([&] {
+    if (family != 0 && family != 1) ackpt::fail(ACKPT_VALUE_ERROR, "family must be 0 (ffma2) or 1 (tcgen05)");
+    ackpt::g_family.store(family);
+  });
+}
+
+ACKPT_API int32_t ackpt_get_fused_family(void) { return ackpt::tc_on() ? 1 : 0; }
 
 ACKPT_API int ackpt_lstm_operator(ackpt_lstm* cell, ackpt_operator* out) {
   return ackpt::guard([&] {

@@ -231,6 +231,17 @@ def _stream() -> int:
     return torch.cuda.current_stream().cuda_stream
 
 
+def set_kernel_family(name: str) -> None:
+    """Kernel family of the fused d=8 fp32 launches: "ffma2" (packed fp32
+    FMA, default) or "tcgen05" (tensor cores, 3xTF32).  Both meet the fp32
+    tolerance; they round differently, so switch only between executions."""
+    N.check(N.lib.ackpt_set_fused_family({"ffma2": 0, "tcgen05": 1}[name]))
+
+
+def kernel_family() -> str:
+    return "tcgen05" if N.lib.ackpt_get_fused_family() == 1 else "ffma2"
+
+
 def device_cell(cell: LstmCell, batch: int = 1, dtype="f64") -> DeviceCell:
     key = (int(batch), _torch_dtype(dtype))
     dc = cell._device.get(key)

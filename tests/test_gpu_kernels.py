@@ -100,19 +100,27 @@ def test_seed_and_loss(P):
         assert L.rel_l2(losses, L.loss(ocell, x.astype(npdt).astype(np.float64))) <= tol
 
 
-def _tensor_core_family(d, batch, dtype):
+@pytest.fixture(params=["ffma2", "tcgen05"])
+def family(request, P):
+    before = P.kernel_family()
+    P.set_kernel_family(request.param)
+    yield request.param
+    P.set_kernel_family(before)
+
+
+def _tensor_core_family(P, d, batch, dtype):
     # fused d=8 fp32 launches (even batch) run on tcgen05 with the 3xTF32 split
-    return d == 8 and dtype == "f32" and batch % 2 == 0
+    return P.kernel_family() == "tcgen05" and d == 8 and dtype == "f32" and batch % 2 == 0
 
 
 @pytest.mark.parametrize("d,batch,dtype", [(8, 4096, "f32"), (4, 512, "f32"), (8, 7, "f32"), (6, 64, "f64")])
-def test_fused_advance(P, d, batch, dtype):
+def test_fused_advance(P, family, d, batch, dtype):
     cell, ocell = _cells(P, d, 12, 21)
     npdt = np.float64 if dtype == "f64" else np.float32
     x = torch.from_numpy(_states(d, 8, batch).astype(npdt)).cuda()
     dc = P.device_cell(cell, batch, dtype)
     fused = dc.advance(2, 11, x)
-    if _tensor_core_family(d, batch, dtype):
+    if _tensor_core_family(P, d, batch, dtype):
         ref = x.double().cpu().numpy()
         for k in range(2, 11):
             ref = L.forward_step(ocell, k, ref)
@@ -127,7 +135,7 @@ def test_fused_advance(P, d, batch, dtype):
 
 
 @pytest.mark.parametrize("d,batch", [(8, 4096), (4, 512), (8, 1002), (8, 300)])
-def test_fused_tape_and_reverse(P, d, batch):
+def test_fused_tape_and_reverse(P, family, d, batch):
     cell, ocell = _cells(P, d, 70, 22)
     x = torch.from_numpy(_states(d, 9, batch).astype(np.float32)).cuda()
     a = torch.from_numpy(_states(d, 10, batch).astype(np.float32)).cuda()
@@ -135,7 +143,7 @@ def test_fused_tape_and_reverse(P, d, batch):
     outs = dc.forward_many(3, 64, x)
     states = [x] + outs[:-1]  # input state of steps 3..66
     fused = dc.backward_many(3, states, a)
-    if _tensor_core_family(d, batch, "f32"):
+    if _tensor_core_family(P, d, batch, "f32"):
         ref = x.double().cpu().numpy()
         for i, k in enumerate(range(3, 67)):
             ref = L.forward_step(ocell, k, ref)

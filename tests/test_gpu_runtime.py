@@ -326,10 +326,20 @@ def test_fused_and_per_step_modes_agree(P):
     ops = lstm.operator_pair(cell, batch, "f32")
     s0 = lstm.random_states(d, 4, batch, "f32")
     per_step, _ = pkg.execute(pkg.Revolve(7), ops, s0)
-    fused, _ = pkg.execute(pkg.Revolve(7), ops, s0, fuse=True)
     ref, _ = RO.execute("full", L.random_cell(d, n, 3), s0.double().cpu().numpy())
     assert L.rel_l2(per_step.double().cpu().numpy(), ref) <= 1e-5
-    assert L.rel_l2(fused.double().cpu().numpy(), ref) <= 1e-5
+    before = lstm.kernel_family()
+    try:
+        for fam in ("ffma2", "tcgen05"):
+            lstm.set_kernel_family(fam)
+            fused, _ = pkg.execute(pkg.Revolve(7), ops, s0, fuse=True)
+            full_fused, _ = pkg.execute(pkg.FullStorage(), ops, s0, fuse=True)
+            with pkg.PinnedHostBackend() as b:
+                ms_fused, _ = pkg.execute(pkg.Multistage(7, interval=8), ops, s0, b, fuse=True)
+            assert torch.equal(fused, full_fused) and torch.equal(fused, ms_fused), fam
+            assert L.rel_l2(fused.double().cpu().numpy(), ref) <= 1e-5, fam
+    finally:
+        lstm.set_kernel_family(before)
 
 
 def test_python_callback_operator_pair(P, fast_backend):
