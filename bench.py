@@ -56,6 +56,8 @@ def parse_args(argv=None):
     p.add_argument("--no-cpu", action="store_true")
     p.add_argument("--full-n", type=int, default=1000, help="n of the measured FullStorage run")
     p.add_argument("--no-other-mode", action="store_true")
+    p.add_argument("--family", choices=["ffma2", "tcgen05", "mixed"], default="mixed",
+                   help="kernel family of the fused d=8 launches (lstm.set_kernel_family)")
     return p.parse_args(argv)
 
 
@@ -282,6 +284,7 @@ def workload_config(args, interval, slots) -> dict:
         "memory_ratio": args.memory_ratio,
         "execution": "temporally fused launches (Advance / TapeForward / Reverse runs)" if args.fuse
                      else "per-step operator launches (reference contract)",
+        "kernel_family": args.family if args.fuse else "ffma2 (per-step kernels)",
         "l2": "inputs larger than L2: every pass cycles >= I+2 distinct 64 MiB buffers (126 MB L2)",
         "parallelism": f"batch-sharded x{args.gpus}, identical schedule per rank, no collective in the timed region",
     }
@@ -310,6 +313,7 @@ def main(argv=None) -> None:
     import paper_1806_01117_b200.distributed as D
     import paper_1806_01117_b200.lstm as lstm
 
+    lstm.set_kernel_family(args.family)
     dev = torch.device("cuda", local)
     cell = lstm.random_cell(args.d, args.n, 0)
     ops = lstm.operator_pair(cell, args.batch, "f32")

@@ -54,22 +54,23 @@ Variant variant() {
   return v;
 }
 
-// Fused launches (advance / forward_many / backward_many) for d=8 run on the
-// packed-FFMA2 family by default; ACKPT_TC=1 selects the tensor-core family
-// (tcgen05, 3xTF32).  Measured at the C2 shape the tcgen05 kernels are not
-// faster yet (MUFU-bound activations, exposed MMA latency).
-// Each execution mode uses one kernel family for every step, so strategies
-// stay bit-identical within a mode.
+// Fused launches (advance / forward_many / backward_many) for d=8 pick a
+// kernel family: 0 packed FFMA2, 1 tcgen05 for all three, 2 "mixed" (default)
+// = tcgen05 forward launches (advance, forward_many) + FFMA2 reverse runs, the
+// fastest measured at the C2 shape.  Env ACKPT_TC=0/1/2 presets.  Families round differently (each within the
+// fp32 tolerance); within one family the strategies stay bit-identical.
 std::atomic<int> g_family{-1};  // -1: not yet read from the environment
-bool tc_on() {
+int family() {
   int f = g_family.load(std::memory_order_relaxed);
   if (f < 0) {
     const char* e = std::getenv("ACKPT_TC");
-    f = (e && std::string(e) == "1") ? 1 : 0;
+    f = !e ? 2 : std::string(e) == "0" ? 0 : std::string(e) == "1" ? 1 : 2;
     g_family.store(f, std::memory_order_relaxed);
   }
-  return f == 1;
+  return f;
 }
+bool tc_fwd_on() { return family() != 0; }
+bool tc_bwd_on() { return family() == 1; }
 
 // TMA path: d=8, B % 4 == 0 (16-byte row segments), 16-byte aligned rows.
 bool tma_ok(const ackpt_lstm* c, std::initializer_list<const void*> ptrs) {
@@ -228,7 +229,7 @@ ACKPT_API int ackpt_lstm_advance(const ackpt_lstm* cell, int64_t from_step, int6
     if (ackpt::f32_fast(cell, {state_in, state_out})) {
       auto i = static_cast<const float*>(state_in);
       auto o = static_cast<float*>(state_out);
-      if (cell->d == 8 && ackpt::tc_on()) ackpt::tc_advance(cell, from_step, int(to_step - from_step), i, o, s);
+      if (cell->d == 8 && ackpt::tc_fwd_on()) ackpt::tc_advance(cell, from_step, int(to_step - from_step), i, o, s);
       else if (cell->d == 8) ackpt::f32_advance<8>(cell, from_step, to_step, i, o, s);
       else ackpt::f32_advance<4>(cell, from_step, to_step, i, o, s);
     } else if (cell->dtype == ACKPT_F32) {
@@ -293,7 +294,7 @@ ACKPT_API int ackpt_lstm_forward_many(const ackpt_lstm* cell, int64_t from_step,
     if (fast) {
       auto in = static_cast<const float*>(state_in);
       auto outs = reinterpret_cast<float* const*>(states_out);
-      if (cell->d == 8 && ackpt::tc_on()) ackpt::tc_forward_many(cell, from_step, int(count), in, outs, s);
+      if (cell->d == 8 && ackpt::tc_fwd_on()) ackpt::tc_forward_many(cell, from_step, int(count), in, outs, s);
       else if (cell->d == 8) ackpt::f32_forward_many<8>(cell, from_step, int(count), in, outs, s);
       else ackpt::f32_forward_many<4>(cell, from_step, int(count), in, outs, s);
       ackpt::check_launch();
@@ -321,7 +322,7 @@ ACKPT_API int ackpt_lstm_backward_many(const ackpt_lstm* cell, int64_t from_step
     auto sp = reinterpret_cast<const float* const*>(states);
     auto ai = static_cast<const float*>(adjoint_in);
     auto ao = static_cast<float*>(adjoint_out);
-    if (cell->d == 8 && ackpt::tc_on()) ackpt::tc_backward_many(cell, from_step, int(count), sp, ai, ao, s);
+    if (cell->d == 8 && ackpt::tc_bwd_on()) ackpt::tc_backward_many(cell, from_step, int(count), sp, ai, ao, s);
     else if (cell->d == 8) ackpt::f32_backward_many<8>(cell, from_step, int(count), sp, ai, ao, s);
     else ackpt::f32_backward_many<4>(cell, from_step, int(count), sp, ai, ao, s);
     ackpt::check_launch();
@@ -358,12 +359,12 @@ ACKPT_API int ackpt_lstm_loss(const ackpt_lstm* cell, const void* final_state, v
 
 ACKPT_API int ackpt_set_fused_family(int32_t family) {
   return ackpt::guard([&] {
-    if (family != 0 && family != 1) ackpt::fail(ACKPT_VALUE_ERROR, "family must be 0 (ffma2) or 1 (tcgen05)");
+    if (family < 0 || family > 2) ackpt::fail(ACKPT_VALUE_ERROR, "family must be 0 (ffma2), 1 (tcgen05) or 2 (mixed)");
     ackpt::g_family.store(family);
   });
 }
 
-ACKPT_API int32_t ackpt_get_fused_family(void) { return ackpt::tc_on() ? 1 : 0; }
+ACKPT_API int32_t ackpt_get_fused_family(void) { return ackpt::family(); }
 
 ACKPT_API int ackpt_lstm_operator(ackpt_lstm* cell, ackpt_operator* out) {
   return ackpt::guard([&] {

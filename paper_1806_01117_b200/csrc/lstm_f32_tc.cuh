@@ -34,15 +34,18 @@ constexpr int kThreads = 128;
 constexpr int kTile = 256;     // elements per CTA
 constexpr int kD = 8;          // hidden size
 constexpr int kN = 4 * kD;     // gate columns
-constexpr int kK = 16;         // [h (8) | 1 | 0 x 7]
-constexpr uint32_t kLBO = 128; // bytes between 16-byte K chunks (8 rows x 16 B core matrices)
-constexpr uint32_t kSBO = 512; // bytes between 8-row groups (4 chunks of 128 B)
-constexpr int kMatBytes = 128 * kK * 4;  // one 128 x 16 tf32 operand
+constexpr int kK = 8;          // one MMA K step
+constexpr uint32_t kLBO = 128; // bytes between the two 16-byte K chunks (8 rows x 16 B core matrices)
+constexpr uint32_t kSBO = 256; // bytes between 8-row groups
 constexpr uint32_t kIdesc = (1u << 4) | (2u << 7) | (2u << 10) | (uint32_t(kN >> 3) << 17) | (uint32_t(128 >> 4) << 24);
 
+// 24 KB: h operands per tile (hi, lo), one constant bias operand A1 = [1, 0 x 7]
+// shared by both tiles, the weights (hi, lo) and the step's bias column (hi, lo).
 struct Smem {
   float a[2][2][128 * kK];  // [tile][hi, lo]
-  float b[2][kN * kK];      // [hi, lo]
+  float a1[128 * kK];       // rows [1, 0, ..., 0]
+  float bw[2][kN * kK];     // [hi, lo] scaled W rows n = 4 j + g
+  float bb[2][kN * kK];     // [hi, lo] column 0 = scaled xb_k, rest 0
   uint64_t mbar;
   uint32_t tmem;
 };
@@ -88,34 +91,32 @@ __device__ __forceinline__ void setup(Smem& sm, const Weights& w) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(&sm.mbar)));
     asm volatile("fence.mbarrier_init.release.cluster;");
   }
-  // A columns 8..15 (chunks 2, 3): hi = [1, 0, ...], lo = 0, for this thread's row in both tiles
-#pragma unroll
-  for (int t = 0; t < 2; ++t) {
-    *reinterpret_cast<float4*>(&sm.a[t][0][kofs(tid, 8)]) = make_float4(1.f, 0.f, 0.f, 0.f);
-    *reinterpret_cast<float4*>(&sm.a[t][0][kofs(tid, 12)]) = make_float4(0.f, 0.f, 0.f, 0.f);
-    *reinterpret_cast<float4*>(&sm.a[t][1][kofs(tid, 8)]) = make_float4(0.f, 0.f, 0.f, 0.f);
-    *reinterpret_cast<float4*>(&sm.a[t][1][kofs(tid, 12)]) = make_float4(0.f, 0.f, 0.f, 0.f);
-  }
-  // B rows n = 4 j + g, k 0..7: scaled weights, k 9..15: 0 (k 8 is per step)
+  // bias operand row of this thread: [1, 0, ..., 0]
+  *reinterpret_cast<float4*>(&sm.a1[kofs(tid, 0)]) = make_float4(1.f, 0.f, 0.f, 0.f);
+  *reinterpret_cast<float4*>(&sm.a1[kofs(tid, 4)]) = make_float4(0.f, 0.f, 0.f, 0.f);
+  // weight rows n = 4 j + g (scaled, split), bias rows zero but for column 0 (per step)
   if (tid < kN) {
     const int j = tid >> 2, g = tid & 3;
 #pragma unroll
     for (int k = 0; k < kD; ++k) {
       const float x = w.ws[g][j][k];
-      sm.b[0][kofs(tid, k)] = hi_part(x);
-      sm.b[1][kofs(tid, k)] = x - hi_part(x);
-    }
-#pragma unroll
-    for (int k = 9; k < kK; ++k) {
-      sm.b[0][kofs(tid, k)] = 0.f;
-      sm.b[1][kofs(tid, k)] = 0.f;
+      sm.bw[0][kofs(tid, k)] = hi_part(x);
+      sm.bw[1][kofs(tid, k)] = x - hi_part(x);
+      sm.bb[0][kofs(tid, k)] = 0.f;
+      sm.bb[1][kofs(tid, k)] = 0.f;
     }
   }
 }
 
-// Writes A (h hi/lo for both tiles) and, in warp 0, B's bias column for step k.
-__device__ __forceinline__ void stage_operands(Smem& sm, const float2 (&h)[kD], const float* __restrict__ xbs_all,
-                                               int64_t k) {
+// Scaled bias of step k for B row n = tid (threads < kN), loaded one step ahead.
+__device__ __forceinline__ float load_bias(const float* __restrict__ xbs_all, int64_t k) {
+  const int tid = threadIdx.x;
+  if (tid >= kN) return 0.f;
+  return __ldg(xbs_all + k * kN + (tid & 3) * kD + (tid >> 2));  // table is gate-major
+}
+
+// Writes A (h hi/lo for both tiles) and, in warp 0, B's bias column (x from load_bias).
+__device__ __forceinline__ void stage_operands(Smem& sm, const float2 (&h)[kD], float x) {
   const int tid = threadIdx.x;
   float4 hx[2], hy[2];
   hx[0] = make_float4(h[0].x, h[1].x, h[2].x, h[3].x);
@@ -135,10 +136,8 @@ __device__ __forceinline__ void stage_operands(Smem& sm, const float2 (&h)[kD], 
         make_float4(b.x - bh.x, b.y - bh.y, b.z - bh.z, b.w - bh.w);
   }
   if (tid < kN) {
-    const int j = tid >> 2, g = tid & 3;
-    const float x = __ldg(xbs_all + k * kN + g * kD + j);  // table is gate-major
-    sm.b[0][kofs(tid, 8)] = hi_part(x);
-    sm.b[1][kofs(tid, 8)] = x - hi_part(x);
+    sm.bb[0][kofs(tid, 0)] = hi_part(x);
+    sm.bb[1][kofs(tid, 0)] = x - hi_part(x);
   }
 }
 
@@ -149,17 +148,17 @@ __device__ __forceinline__ void gates_mma(Smem& sm, uint32_t phase) {
   __syncthreads();
   if (threadIdx.x == 0) {
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    const uint64_t bh0 = desc(su32(sm.b[0])), bl0 = desc(su32(sm.b[1]));
-    const uint64_t bh1 = desc(su32(sm.b[0]) + 2 * kLBO), bl1 = desc(su32(sm.b[1]) + 2 * kLBO);
+    const uint64_t wh = desc(su32(sm.bw[0])), wl = desc(su32(sm.bw[1]));
+    const uint64_t xh = desc(su32(sm.bb[0])), xl = desc(su32(sm.bb[1])), one = desc(su32(sm.a1));
 #pragma unroll
     for (int t = 0; t < 2; ++t) {
       const uint32_t d = sm.tmem + uint32_t(t * kN);
-      const uint32_t ah = su32(sm.a[t][0]), al = su32(sm.a[t][1]);
-      mma(d, desc(ah), bh0, 0u);               // h_hi . W_hi
-      mma(d, desc(al), bh0, 1u);               // h_lo . W_hi
-      mma(d, desc(ah), bl0, 1u);               // h_hi . W_lo
-      mma(d, desc(ah + 2 * kLBO), bh1, 1u);    // 1 . xb_hi
-      mma(d, desc(ah + 2 * kLBO), bl1, 1u);    // 1 . xb_lo
+      const uint64_t ah = desc(su32(sm.a[t][0])), al = desc(su32(sm.a[t][1]));
+      mma(d, ah, wh, 0u);   // h_hi . W_hi
+      mma(d, al, wh, 1u);   // h_lo . W_hi
+      mma(d, ah, wl, 1u);   // h_hi . W_lo
+      mma(d, one, xh, 1u);  // 1 . xb_hi
+      mma(d, one, xl, 1u);  // 1 . xb_lo
     }
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(&sm.mbar))
                  : "memory");
@@ -213,7 +212,7 @@ struct StatePtrs {
 // Fused forward over `count` steps from `from`; TAPE stores every step's
 // output to outs.p[i], otherwise only the final state goes to `out`.
 template <bool TAPE>
-__global__ void __launch_bounds__(kThreads, 4)
+__global__ void __launch_bounds__(kThreads, 8)
     fwd_tc(const float* __restrict__ in, float* __restrict__ out, int64_t B, const float* __restrict__ xbs_all,
            int64_t from, int count, const __grid_constant__ Weights w, const __grid_constant__ OutPtrs outs) {
   __shared__ __align__(128) Smem sm;
@@ -226,8 +225,10 @@ __global__ void __launch_bounds__(kThreads, 4)
     h[j] = live ? ldg2(in + b0 + int64_t(j) * B) : make_float2(0.f, 0.f);
     c[j] = live ? ldg2(in + b0 + int64_t(kD + j) * B) : make_float2(0.f, 0.f);
   }
+  float xb = load_bias(xbs_all, from);
   for (int i = 0; i < count; ++i) {
-    stage_operands(sm, h, xbs_all, from + i);
+    stage_operands(sm, h, xb);
+    if (i + 1 < count) xb = load_bias(xbs_all, from + i + 1);
     gates_mma(sm, uint32_t(i & 1));
 #pragma unroll
     for (int u = 0; u < kD; u += 2) {
@@ -272,6 +273,7 @@ __global__ void __launch_bounds__(kThreads, 4)
     dc[j] = live ? ldg2(adj_in + b0 + int64_t(kD + j) * B) : make_float2(0.f, 0.f);
   }
   int phase = 0;
+  float xb = load_bias(xbs_all, from + count - 1);
   for (int i = count - 1; i >= 0; --i, ++phase) {
     const float* xs = states.p[i] + b0;
     float2 h[kD], c[kD];
@@ -280,7 +282,8 @@ __global__ void __launch_bounds__(kThreads, 4)
       h[j] = live ? ldg2(xs + int64_t(j) * B) : make_float2(0.f, 0.f);
       c[j] = live ? ldg2(xs + int64_t(kD + j) * B) : make_float2(0.f, 0.f);
     }
-    stage_operands(sm, h, xbs_all, from + i);
+    stage_operands(sm, h, xb);
+    if (i > 0) xb = load_bias(xbs_all, from + i - 1);
     gates_mma(sm, uint32_t(phase & 1));
     float2 acc[kD];
 #pragma unroll

@@ -233,13 +233,17 @@ def _stream() -> int:
 
 def set_kernel_family(name: str) -> None:
     """Kernel family of the fused d=8 fp32 launches: "ffma2" (packed fp32
-    FMA, default) or "tcgen05" (tensor cores, 3xTF32).  Both meet the fp32
+    FMA), "tcgen05" (tensor cores, 3xTF32) or "mixed" (default: tcgen05
+    advance / forward_many, ffma2 backward_many).  All meet the fp32
     tolerance; they round differently, so switch only between executions."""
-    N.check(N.lib.ackpt_set_fused_family({"ffma2": 0, "tcgen05": 1}[name]))
+    N.check(N.lib.ackpt_set_fused_family(KERNEL_FAMILIES.index(name)))
+
+
+KERNEL_FAMILIES = ("ffma2", "tcgen05", "mixed")
 
 
 def kernel_family() -> str:
-    return "tcgen05" if N.lib.ackpt_get_fused_family() == 1 else "ffma2"
+    return KERNEL_FAMILIES[N.lib.ackpt_get_fused_family()]
 
 
 def device_cell(cell: LstmCell, batch: int = 1, dtype="f64") -> DeviceCell:

@@ -330,7 +330,7 @@ def test_fused_and_per_step_modes_agree(P):
     assert L.rel_l2(per_step.double().cpu().numpy(), ref) <= 1e-5
     before = lstm.kernel_family()
     try:
-        for fam in ("ffma2", "tcgen05"):
+        for fam in lstm.KERNEL_FAMILIES:
             lstm.set_kernel_family(fam)
             fused, _ = pkg.execute(pkg.Revolve(7), ops, s0, fuse=True)
             full_fused, _ = pkg.execute(pkg.FullStorage(), ops, s0, fuse=True)
