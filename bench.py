@@ -233,16 +233,16 @@ def kernel_chain_times(dc, state0, chain=64):
             e0.record()
             for k in range(chain):
                 if kind == "fwd":
-                    bufs[(k + 1) % 6] = dc.forward(k % dc.cell.n_steps, bufs[k % 6])
+                    bufs[(k + 1) % 6] = dc.forward(k % dc.n_steps, bufs[k % 6])
                 else:
-                    adj[(k + 1) % 2] = dc.backward(k % dc.cell.n_steps, bufs[k % 6], adj[k % 2])
+                    adj[(k + 1) % 2] = dc.backward(k % dc.n_steps, bufs[k % 6], adj[k % 2])
             e1.record()
             torch.cuda.synchronize()
         out.append(e0.elapsed_time(e1) * 1e-3 / chain)
     return out[0], out[1]
 
 
-def fused_kernel_times(dc, state0, steps=64):
+def fused_kernel_times(dc, state0, steps=64, reps=5):
     """Per-step durations of the fused launches (64 steps each): advance
     (state in registers), tape (every output stored), reverse (adjoint in
     registers, taped states read), plus their algorithmic bytes per launch."""
@@ -253,7 +253,8 @@ def fused_kernel_times(dc, state0, steps=64):
     adj = dc.seed(states[-1])
     out = {}
     for kind in ("adv", "tape", "rev"):
-        for rep in range(2):
+        times = []
+        for rep in range(reps + 1):  # first launch is a warm-up
             torch.cuda.synchronize()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record()
@@ -265,7 +266,9 @@ def fused_kernel_times(dc, state0, steps=64):
                 dc.backward_many(0, [state0] + states[:-1], adj)
             e1.record()
             torch.cuda.synchronize()
-        out[kind] = e0.elapsed_time(e1) * 1e-3 / steps
+            if rep:
+                times.append(e0.elapsed_time(e1) * 1e-3 / steps)
+        out[kind] = sorted(times)[len(times) // 2]  # median
     out["adv_bytes"] = 2 * S
     out["tape_bytes"] = (steps + 1) * S
     out["rev_bytes"] = (steps + 2) * S

@@ -57,6 +57,12 @@ int64_t interval_length_exact(double t_t, double t_a);
 // Save, the index of the last Load reading that write, or -1.
 void slot_read_liveness(const std::vector<Action>& actions, std::vector<int64_t>& last_read);
 
+// CRC32C helpers (crc32c.cpp).  raw = unconditioned register (no xor in/out).
+uint32_t crc32c_raw(const void* data, int64_t len, uint32_t reg);
+uint32_t crc32c_shift(uint32_t reg, int64_t len);  // as if len zero bytes followed
+uint32_t crc32c_parallel(const void* data, int64_t len, uint32_t crc, int threads);
+int io_threads(int64_t len);  // worker threads for a len-byte host I/O job
+
 }  // namespace ackpt
 
 #define ACKPT_CUDA_CHECK(expr)                                                        \

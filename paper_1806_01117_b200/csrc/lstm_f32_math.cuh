@@ -44,6 +44,11 @@ __device__ __forceinline__ float2 add2(float2 a, float2 b) {
   asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r.u) : "l"(x.u), "l"(y.u));
   return r.f;
 }
+__device__ __forceinline__ float2 sub2(float2 a, float2 b) {
+  P2 x{a}, y{b}, r;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r.u) : "l"(x.u), "l"(y.u));
+  return r.f;
+}
 __device__ __forceinline__ float2 bc(float s) { return make_float2(s, s); }
 __device__ __forceinline__ float2 neg(float2 a) { return make_float2(-a.x, -a.y); }
 __device__ __forceinline__ float ex2(float x) {

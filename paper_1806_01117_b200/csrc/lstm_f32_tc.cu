@@ -1,6 +1,9 @@
 // Launchers of the tensor-core fused LSTM kernels (lstm_f32_tc.cuh).
 #include "lstm_f32_tc.cuh"
 
+#include <cstdint>
+#include <cstdlib>
+
 namespace ackpt {
 
 namespace {
@@ -35,8 +38,14 @@ void tc_backward_many(const ackpt_lstm* c, int64_t from, int count, const float*
                       float* adj_out, cudaStream_t s) {
   tc::StatePtrs sp{};
   for (int i = 0; i < count; ++i) sp.p[i] = states[i];
-  tc::rev_tc<<<tc_grid(c->B), tc::kThreads, 0, s>>>(adj_in, adj_out, c->B, static_cast<const float*>(c->d_xbs),
-                                                     from, count, tc_weights(c), sp);
+  bool pf = c->B % 4 == 0 && std::getenv("ACKPT_TC_NO_PF") == nullptr;
+  for (int i = 0; i < count; ++i) pf = pf && !(reinterpret_cast<uintptr_t>(states[i]) & 15u);
+  if (pf)
+    tc::rev_tc<true><<<tc_grid(c->B), tc::kThreads, 0, s>>>(
+        adj_in, adj_out, c->B, static_cast<const float*>(c->d_xbs), from, count, tc_weights(c), sp);
+  else
+    tc::rev_tc<false><<<tc_grid(c->B), tc::kThreads, 0, s>>>(
+        adj_in, adj_out, c->B, static_cast<const float*>(c->d_xbs), from, count, tc_weights(c), sp);
 }
 
 }  // namespace ackpt

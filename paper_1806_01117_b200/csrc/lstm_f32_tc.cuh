@@ -128,12 +128,15 @@ __device__ __forceinline__ void stage_operands(Smem& sm, const float2 (&h)[kD], 
     const float4 a = hx[c], b = hy[c];
     const float4 ah = make_float4(hi_part(a.x), hi_part(a.y), hi_part(a.z), hi_part(a.w));
     const float4 bh = make_float4(hi_part(b.x), hi_part(b.y), hi_part(b.z), hi_part(b.w));
+    // lo = x - hi, packed two at a time (every FMA-pipe instruction costs 2 cycles)
+    const float2 a01 = sub2(make_float2(a.x, a.y), make_float2(ah.x, ah.y));
+    const float2 a23 = sub2(make_float2(a.z, a.w), make_float2(ah.z, ah.w));
+    const float2 b01 = sub2(make_float2(b.x, b.y), make_float2(bh.x, bh.y));
+    const float2 b23 = sub2(make_float2(b.z, b.w), make_float2(bh.z, bh.w));
     *reinterpret_cast<float4*>(&sm.a[0][0][kofs(tid, 4 * c)]) = ah;
-    *reinterpret_cast<float4*>(&sm.a[0][1][kofs(tid, 4 * c)]) =
-        make_float4(a.x - ah.x, a.y - ah.y, a.z - ah.z, a.w - ah.w);
+    *reinterpret_cast<float4*>(&sm.a[0][1][kofs(tid, 4 * c)]) = make_float4(a01.x, a01.y, a23.x, a23.y);
     *reinterpret_cast<float4*>(&sm.a[1][0][kofs(tid, 4 * c)]) = bh;
-    *reinterpret_cast<float4*>(&sm.a[1][1][kofs(tid, 4 * c)]) =
-        make_float4(b.x - bh.x, b.y - bh.y, b.z - bh.z, b.w - bh.w);
+    *reinterpret_cast<float4*>(&sm.a[1][1][kofs(tid, 4 * c)]) = make_float4(b01.x, b01.y, b23.x, b23.y);
   }
   if (tid < kN) {
     sm.bb[0][kofs(tid, 0)] = hi_part(x);
@@ -141,8 +144,21 @@ __device__ __forceinline__ void stage_operands(Smem& sm, const float2 (&h)[kD], 
   }
 }
 
-// Barrier, issue the 10 MMAs of a step (thread 0), wait for them.
-__device__ __forceinline__ void gates_mma(Smem& sm, uint32_t phase) {
+__device__ __forceinline__ void mbar_wait(const uint64_t* bar, uint32_t phase) {
+  uint32_t done = 0;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(su32(bar)), "r"(phase)
+        : "memory");
+  } while (!done);
+}
+
+// Barrier, then thread 0 issues the 10 MMAs of a step and commits them to
+// sm.mbar.  Every thread's shared-memory reads and writes of the step so far
+// are complete (and visible to the async proxy) when this returns.
+__device__ __forceinline__ void gates_issue(Smem& sm) {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
@@ -163,15 +179,17 @@ __device__ __forceinline__ void gates_mma(Smem& sm, uint32_t phase) {
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(&sm.mbar))
                  : "memory");
   }
-  uint32_t done = 0;
-  do {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
-        : "=r"(done)
-        : "r"(su32(&sm.mbar)), "r"(phase)
-        : "memory");
-  } while (!done);
+}
+
+__device__ __forceinline__ void gates_wait(Smem& sm, uint32_t phase) {
+  mbar_wait(&sm.mbar, phase);
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+
+// Barrier, issue the 10 MMAs of a step (thread 0), wait for them.
+__device__ __forceinline__ void gates_mma(Smem& sm, uint32_t phase) {
+  gates_issue(sm);
+  gates_wait(sm, phase);
 }
 
 // Scaled pre-activations (f, i, o, g) of units u, u+1 for the thread's pair.
@@ -256,16 +274,54 @@ __global__ void __launch_bounds__(kThreads, 8)
   teardown(sm);
 }
 
+// Reverse-run shared memory: the gate operands plus one staging buffer for
+// the taped state of the next step (16 rows of the CTA's 256 elements).
+struct RevSmem {
+  Smem g;
+  float st[2 * kD][kTile];
+  uint64_t mbar_st;
+};
+
+// Thread 0: the CTA's 16 row segments of `state` into sm.st with
+// cp.async.bulk, completing on sm.mbar_st.
+__device__ __forceinline__ void stage_state(RevSmem& sm, const float* state, int64_t B, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(&sm.mbar_st)),
+               "r"(bytes * uint32_t(2 * kD))
+               : "memory");
+  const float* src = state + int64_t(blockIdx.x) * kTile;
+#pragma unroll 1
+  for (int j = 0; j < 2 * kD; ++j)
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     su32(sm.st[j])),
+                 "l"(src + int64_t(j) * B), "r"(bytes), "r"(su32(&sm.mbar_st))
+                 : "memory");
+}
+
 // Fused run of Reverse actions, steps from+count-1 .. from.  Gates on the
 // tensor cores; the transpose matvec dh = sum_g (s_g W_g)^T (da_g / s_g) on
-// the packed-fp32 pipe with uniform-register weights.
+// the packed-fp32 pipe with uniform-register weights.  PF (B % 4 == 0, 16-byte
+// aligned states): the taped state of step i-1 streams into shared memory by
+// cp.async.bulk while step i computes, instead of a dependent load at the top
+// of every step.
+template <bool PF>
 __global__ void __launch_bounds__(kThreads, 4)
     rev_tc(const float* __restrict__ adj_in, float* __restrict__ adj_out, int64_t B, const float* __restrict__ xbs_all,
            int64_t from, int count, const __grid_constant__ Weights w, const __grid_constant__ StatePtrs states) {
-  __shared__ __align__(128) Smem sm;
+  __shared__ __align__(128) RevSmem rs;
+  Smem& sm = rs.g;
   const int64_t b0 = int64_t(blockIdx.x) * kTile + 2 * threadIdx.x;
   const bool live = b0 < B;
+  const int64_t rem = B - int64_t(blockIdx.x) * kTile;
+  const uint32_t seg = uint32_t(rem < kTile ? rem : kTile) * 4u;
   setup(sm, w);
+  if (PF) {
+    if (threadIdx.x == 0) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(&rs.mbar_st)));
+      asm volatile("fence.mbarrier_init.release.cluster;");
+      stage_state(rs, states.p[count - 1], B, seg);
+    }
+    __syncthreads();
+  }
   float2 dh[kD], dc[kD];
 #pragma unroll
   for (int j = 0; j < kD; ++j) {
@@ -275,16 +331,27 @@ __global__ void __launch_bounds__(kThreads, 4)
   int phase = 0;
   float xb = load_bias(xbs_all, from + count - 1);
   for (int i = count - 1; i >= 0; --i, ++phase) {
-    const float* xs = states.p[i] + b0;
     float2 h[kD], c[kD];
+    if (PF) {
+      mbar_wait(&rs.mbar_st, uint32_t(phase & 1));
 #pragma unroll
-    for (int j = 0; j < kD; ++j) {
-      h[j] = live ? ldg2(xs + int64_t(j) * B) : make_float2(0.f, 0.f);
-      c[j] = live ? ldg2(xs + int64_t(kD + j) * B) : make_float2(0.f, 0.f);
+      for (int j = 0; j < kD; ++j) {
+        h[j] = *reinterpret_cast<const float2*>(&rs.st[j][2 * threadIdx.x]);
+        c[j] = *reinterpret_cast<const float2*>(&rs.st[kD + j][2 * threadIdx.x]);
+      }
+    } else {
+      const float* xs = states.p[i] + b0;
+#pragma unroll
+      for (int j = 0; j < kD; ++j) {
+        h[j] = live ? ldg2(xs + int64_t(j) * B) : make_float2(0.f, 0.f);
+        c[j] = live ? ldg2(xs + int64_t(kD + j) * B) : make_float2(0.f, 0.f);
+      }
     }
     stage_operands(sm, h, xb);
     if (i > 0) xb = load_bias(xbs_all, from + i - 1);
-    gates_mma(sm, uint32_t(phase & 1));
+    gates_issue(sm);  // after its barrier every thread has read rs.st
+    if (PF && i > 0 && threadIdx.x == 0) stage_state(rs, states.p[i - 1], B, seg);
+    gates_wait(sm, uint32_t(phase & 1));
     float2 acc[kD];
 #pragma unroll
     for (int m = 0; m < kD; ++m) acc[m] = bc(0.0f);
@@ -296,7 +363,7 @@ __global__ void __launch_bounds__(kThreads, 4)
       for (int q = 0; q < 2; ++q) {
         const int j = u + q;
         float2 daf, dai, dao, dag;
-        bwd_unit_nr(pre[q][0], pre[q][1], pre[q][2], pre[q][3], c[j], dh[j], dc[j], daf, dai, dao, dag, dc[j]);
+        bwd_unit(pre[q][0], pre[q][1], pre[q][2], pre[q][3], c[j], dh[j], dc[j], daf, dai, dao, dag, dc[j]);
 #pragma unroll
         for (int m = 0; m < kD; ++m) {
           acc[m] = fma2(bc(w.ws[0][j][m]), daf, acc[m]);

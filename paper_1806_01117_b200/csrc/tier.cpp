@@ -10,7 +10,11 @@
 // Worker exceptions surfaced at wait() (storage.py:271-278) map to a ticket
 // status returned by ackpt_tier_wait (MissingKey, StorageFull, SizeMismatch).
 #include <cuda_runtime.h>
+#include <fcntl.h>
+#include <sys/stat.h>
+#include <unistd.h>
 
+#include <algorithm>
 #include <atomic>
 #include <cerrno>
 #include <chrono>
@@ -174,6 +178,46 @@ void set_async(AsyncStatus& st, int code, const std::string& msg) {
   st.err.store(code, std::memory_order_release);
 }
 
+// Payload I/O split over worker threads: slice i of the payload is
+// checksummed (raw CRC register from 0) and written / read at file offset
+// kHeader + lo by its own thread with pwrite / pread, then the slices' CRCs
+// are merged in order (crc32c.cpp).  Returns the raw register after
+// `reg` (header CRC) and the payload, or sets `err` to the first errno.
+uint32_t payload_io(int fd, unsigned char* buf, int64_t len, uint32_t reg, bool write, int& err) {
+  const int threads = io_threads(len);
+  const int64_t chunk = ((len + threads - 1) / threads + 4095) & ~int64_t(4095);
+  std::vector<uint32_t> part(size_t(threads), 0);
+  std::vector<int> errs(size_t(threads), 0);
+  auto work = [&](int i) {
+    const int64_t lo = int64_t(i) * chunk, hi = std::min(len, lo + chunk);
+    if (write) part[size_t(i)] = crc32c_raw(buf + lo, hi - lo, 0);
+    for (int64_t off = lo; off < hi;) {
+      const ssize_t r = write ? ::pwrite(fd, buf + off, size_t(hi - off), off_t(kHeader + off))
+                              : ::pread(fd, buf + off, size_t(hi - off), off_t(kHeader + off));
+      if (r < 0 && errno == EINTR) continue;
+      if (r <= 0) {
+        errs[size_t(i)] = r < 0 ? errno : EIO;
+        return;
+      }
+      off += r;
+    }
+    if (!write) part[size_t(i)] = crc32c_raw(buf + lo, hi - lo, 0);
+  };
+  std::vector<std::thread> pool;
+  int used = 0;
+  for (int i = 0; i < threads && int64_t(i) * chunk < len; ++i, ++used)
+    if (i > 0) pool.emplace_back(work, i);
+  if (used > 0) work(0);
+  for (auto& th : pool) th.join();
+  err = 0;
+  for (int i = 0; i < used; ++i) {
+    if (errs[size_t(i)] && !err) err = errs[size_t(i)];
+    const int64_t lo = int64_t(i) * chunk, hi = std::min(len, lo + chunk);
+    reg = crc32c_shift(reg, hi - lo) ^ part[size_t(i)];
+  }
+  return reg;
+}
+
 // Host function on the D2H stream, after the payload landed in stage_out:
 // tmp file + rename (write_checkpoint_file, storage.py:109-118).
 void CUDART_CB file_store_cb(void* arg) {
@@ -184,25 +228,24 @@ void CUDART_CB file_store_cb(void* arg) {
   put_le(header + 4, 1, 2);
   put_le(header + 6, uint64_t(tk->step), 8);
   put_le(header + 14, uint64_t(tk->len), 8);
-  uint32_t crc = ackpt_crc32c(header, kHeader, 0);
-  crc = ackpt_crc32c(t->stage_out, tk->len, crc);
-  unsigned char trailer[kTrailer];
-  put_le(trailer, crc, 4);
   const std::string path = ckpt_path(t, tk->key), tmp = path + ".tmp";
-  errno = 0;
-  FILE* f = std::fopen(tmp.c_str(), "wb");
-  bool ok = f != nullptr;
-  if (ok) ok = std::fwrite(header, 1, kHeader, f) == size_t(kHeader);
-  if (ok && tk->len > 0) ok = std::fwrite(t->stage_out, 1, size_t(tk->len), f) == size_t(tk->len);
-  if (ok) ok = std::fwrite(trailer, 1, kTrailer, f) == size_t(kTrailer);
-  if (f && std::fclose(f) != 0) ok = false;
-  if (ok) ok = std::rename(tmp.c_str(), path.c_str()) == 0;
-  if (!ok) {
-    const int e = errno;
+  auto failed = [&](int e) {
     std::remove(tmp.c_str());
     set_async(*tk->async, e == ENOSPC ? ACKPT_STORAGE_FULL : ACKPT_EXECUTION_ERROR,
               "writing " + path + ": " + std::strerror(e));
-  }
+  };
+  const int fd = ::open(tmp.c_str(), O_WRONLY | O_CREAT | O_TRUNC | O_CLOEXEC, 0644);
+  if (fd < 0) return failed(errno);
+  int err = 0;
+  uint32_t reg = crc32c_raw(header, kHeader, 0xFFFFFFFFu);
+  if (::pwrite(fd, header, kHeader, 0) != kHeader) err = errno ? errno : EIO;
+  if (!err && tk->len > 0) reg = payload_io(fd, t->stage_out, tk->len, reg, true, err);
+  unsigned char trailer[kTrailer];
+  put_le(trailer, reg ^ 0xFFFFFFFFu, 4);
+  if (!err && ::pwrite(fd, trailer, kTrailer, off_t(kHeader + tk->len)) != kTrailer) err = errno ? errno : EIO;
+  if (::close(fd) != 0 && !err) err = errno;
+  if (!err && std::rename(tmp.c_str(), path.c_str()) != 0) err = errno;
+  if (err) failed(err);
 }
 
 // Host function on the H2D stream: read + verify into stage_in
@@ -211,21 +254,20 @@ void CUDART_CB file_fetch_cb(void* arg) {
   auto* tk = static_cast<TierTicket*>(arg);
   ackpt_tier* t = tk->tier;
   const std::string path = ckpt_path(t, tk->key);
-  FILE* f = std::fopen(path.c_str(), "rb");
-  if (!f) {
+  const int fd = ::open(path.c_str(), O_RDONLY | O_CLOEXEC);
+  if (fd < 0) {
     set_async(*tk->async, ACKPT_MISSING_KEY, path);
     return;
   }
-  std::fseek(f, 0, SEEK_END);
-  const long size = std::ftell(f);
-  std::fseek(f, 0, SEEK_SET);
+  struct stat sb;
+  const int64_t size = ::fstat(fd, &sb) == 0 ? int64_t(sb.st_size) : -1;
   unsigned char header[kHeader], trailer[kTrailer];
   auto bad = [&](const std::string& why) {
-    std::fclose(f);
+    ::close(fd);
     set_async(*tk->async, ACKPT_CHECKSUM_MISMATCH, path + ": " + why);
   };
   if (size < kHeader + kTrailer) return bad("checkpoint truncated: " + std::to_string(size) + " bytes");
-  if (std::fread(header, 1, kHeader, f) != size_t(kHeader)) return bad("short read");
+  if (::pread(fd, header, kHeader, 0) != kHeader) return bad("short read");
   if (std::memcmp(header, "CKPT", 4) != 0) return bad("bad magic bytes");
   if (get_le(header + 4, 2) != 1) return bad("unsupported format version");
   const uint64_t step = get_le(header + 6, 8), length = get_le(header + 14, 8);
@@ -233,12 +275,13 @@ void CUDART_CB file_fetch_cb(void* arg) {
     return bad("length field says " + std::to_string(length) + ", file holds " +
                std::to_string(size - kHeader - kTrailer));
   if (int64_t(length) != tk->len || int64_t(length) > t->stage_cap) return bad("payload size changed");
-  if (length > 0 && std::fread(t->stage_in, 1, size_t(length), f) != size_t(length)) return bad("short read");
-  if (std::fread(trailer, 1, kTrailer, f) != size_t(kTrailer)) return bad("short read");
-  std::fclose(f);
-  uint32_t crc = ackpt_crc32c(header, kHeader, 0);
-  crc = ackpt_crc32c(t->stage_in, int64_t(length), crc);
-  if (crc != uint32_t(get_le(trailer, 4))) {
+  int err = 0;
+  uint32_t reg = crc32c_raw(header, kHeader, 0xFFFFFFFFu);
+  if (length > 0) reg = payload_io(fd, t->stage_in, int64_t(length), reg, false, err);
+  if (err) return bad(std::string("short read: ") + std::strerror(err));
+  if (::pread(fd, trailer, kTrailer, off_t(kHeader + length)) != kTrailer) return bad("short read");
+  ::close(fd);
+  if ((reg ^ 0xFFFFFFFFu) != uint32_t(get_le(trailer, 4))) {
     set_async(*tk->async, ACKPT_CHECKSUM_MISMATCH, path + ": crc mismatch");
     return;
   }

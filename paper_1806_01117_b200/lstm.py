@@ -132,7 +132,9 @@ class DeviceCell:
     """The cell uploaded to the GPU for one (batch, dtype): native ackpt_lstm."""
 
     def __init__(self, cell: LstmCell, batch: int, dtype):
-        self.cell = cell
+        # no reference back to `cell`: the cell caches this object (cell._device),
+        # and a cycle would keep the engine's HBM pool alive until a GC round
+        self.n_steps = cell.n_steps
         self.batch = int(batch)
         self.dtype = _torch_dtype(dtype)
         self.d = cell.hidden_size

@@ -158,9 +158,11 @@ class _CallbackOperator:
     bytes and may return tensors (any dtype, same byte size) or bytes."""
 
     def __init__(self, ops: OperatorPair):
-        self.ops = ops
+        # the callables only: no reference back to `ops`, which owns this object
+        forward_step, backward_step, adjoint_seed = ops.forward_step, ops.backward_step, ops.adjoint_seed
         S = ops.state_size
-        self.error: Optional[BaseException] = None
+        pending: list = []  # raised exception, shared with the closures (no self-cycle)
+        self._pending = pending
 
         def put(ptr: int, value) -> None:
             dst = _view(ptr, S)
@@ -177,19 +179,19 @@ class _CallbackOperator:
                         fn(*args[:-1])
                     return N.OK
                 except BaseException as exc:  # reported through the status code
-                    self.error = exc
+                    pending.append(exc)
                     return N.EXECUTION_ERROR
 
             return call
 
         def fwd(ctx, step, inp, out):
-            put(out, ops.forward_step(step, _view(inp, S)))
+            put(out, forward_step(step, _view(inp, S)))
 
         def bwd(ctx, step, state, adj_in, adj_out):
-            put(adj_out, ops.backward_step(step, _view(state, S), _view(adj_in, S)))
+            put(adj_out, backward_step(step, _view(state, S), _view(adj_in, S)))
 
         def seed(ctx, final, adj_out):
-            put(adj_out, ops.seed_for(_view(final, S)))
+            put(adj_out, adjoint_seed(_view(final, S)) if callable(adjoint_seed) else adjoint_seed)
 
         self._fns = (
             N.FORWARD_FN(guard(fwd)),
@@ -200,14 +202,20 @@ class _CallbackOperator:
                              N.FORWARD_MANY_FN(), N.BACKWARD_MANY_FN())
 
     def raise_pending(self) -> None:
-        if self.error is not None:
-            exc, self.error = self.error, None
+        if self._pending:
+            exc = self._pending[0]
+            self._pending.clear()
             raise exc
 
 
 class _Engine:
-    def __init__(self, op: N.Operator, owner):
-        self.owner = owner  # keeps callbacks / device cell alive
+    """Native engine (HBM slot pool, events, streams).  ``owner`` keeps the
+    operator's context alive; the engine itself is cached ON that context
+    (or on the OperatorPair for callbacks), never the other way round, so
+    dropping the operator pair frees the pool immediately by refcount."""
+
+    def __init__(self, op: N.Operator, owner=None):
+        self.owner = owner
         h = C.c_void_p()
         N.check(N.lib.ackpt_engine_create(C.byref(op), C.byref(h)))
         self.handle = h.value
@@ -220,24 +228,30 @@ class _Engine:
             pass
 
 
-_CALLBACK_ENGINES: dict = {}
-
-
 def _engine_for(ops: OperatorPair) -> tuple:
     """(engine, callback wrapper or None), cached per operator pair."""
     if ops.native is not None:
         eng = getattr(ops.native, "_engine", None)
         if eng is None:
-            eng = _Engine(ops.native.operator(), ops.native)
+            eng = _Engine(ops.native.operator())  # no back-reference: ops.native owns it
             ops.native._engine = eng
         return eng, None
-    key = id(ops)
-    hit = _CALLBACK_ENGINES.get(key)
-    if hit is None or hit[2] is not ops:
+    hit = ops.__dict__.get("_ackpt_engine")
+    if hit is None:
         cb = _CallbackOperator(ops)
-        hit = (_Engine(cb.op, cb), cb, ops)
-        _CALLBACK_ENGINES[key] = hit
-    return hit[0], hit[1]
+        hit = (_Engine(cb.op, cb), cb)
+        object.__setattr__(ops, "_ackpt_engine", hit)  # frozen dataclass: cache only
+    return hit
+
+
+def release(ops: OperatorPair) -> None:
+    """Free the engine (HBM slot pool, events) cached for ``ops`` now rather
+    than when ``ops`` is dropped."""
+    if ops.native is not None:
+        if getattr(ops.native, "_engine", None) is not None:
+            ops.native._engine = None
+    else:
+        ops.__dict__.pop("_ackpt_engine", None)
 
 
 class _PaddedNative:

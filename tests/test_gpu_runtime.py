@@ -363,3 +363,56 @@ def test_python_callback_operator_pair(P, fast_backend):
     assert st_got.forward_evals == st_want.forward_evals
     got_ms, _ = pkg.execute(pkg.Multistage(2, interval=4), ops, s0, fast_backend)
     assert got_ms == want
+
+
+def test_engine_pool_freed_with_operator_pair(P):
+    # the HBM slot pool lives in the engine cached on the operator; dropping
+    # the operator pair frees it by refcount (no cyclic-GC round needed)
+    import gc
+
+    pkg, lstm, _ = P
+    gc.disable()
+    try:
+        d, n, batch = 8, 40, 1 << 20  # 64 MiB states
+        torch.cuda.synchronize()
+        free0, _ = torch.cuda.mem_get_info()
+        ops = lstm.operator_pair(lstm.random_cell(d, n, 0), batch, "f32")
+        s0 = lstm.random_states(d, 1, batch, "f32")
+        pkg.execute(pkg.Revolve(20), ops, s0, fuse=True)
+        torch.cuda.synchronize()
+        held, _ = torch.cuda.mem_get_info()
+        assert free0 - held >= 20 * (64 << 20)  # pool of >= 20 slots
+        del ops
+        torch.cuda.synchronize()
+        free1, _ = torch.cuda.mem_get_info()
+        assert free1 - held >= 20 * (64 << 20)
+        # explicit release keeps the operator usable (the pool is re-created)
+        ops = lstm.operator_pair(lstm.random_cell(d, n, 0), batch, "f32")
+        a, _ = pkg.execute(pkg.Revolve(20), ops, s0, fuse=True)
+        pkg.release(ops)
+        b, _ = pkg.execute(pkg.Revolve(20), ops, s0, fuse=True)
+        assert torch.equal(a, b)
+    finally:
+        gc.enable()
+
+
+def test_callback_engine_not_leaked(P):
+    import weakref
+
+    pkg, lstm, _ = P
+    cell = lstm.random_cell(d=4, n=6, seed=2)
+    dc = lstm.device_cell(cell, 1, "f64")
+    ops = pkg.OperatorPair(
+        forward_step=lambda k, s: dc.forward(k, s.view(torch.float64)),
+        backward_step=lambda k, s, a: dc.backward(k, s.view(torch.float64), a.view(torch.float64)),
+        state_size=dc.state_bytes,
+        n_steps=6,
+        adjoint_seed=lambda fin: dc.seed(fin.view(torch.float64)),
+    )
+    s0 = lstm.random_state(4, 9)
+    ref, _ = pkg.execute(pkg.FullStorage(), lstm.operator_pair(cell), s0)
+    got, _ = pkg.execute(pkg.Revolve(2), ops, s0)
+    assert got == ref
+    eng = weakref.ref(ops.__dict__["_ackpt_engine"][0])
+    del ops
+    assert eng() is None

@@ -110,3 +110,18 @@ def test_payload_validation():
     with pytest.raises(ValueError):
         CheckpointPayload(-1, b"")
     assert CheckpointPayload(3, os.urandom(0)).data == b""
+
+
+@pytest.mark.parametrize("size", [12287, 12288, 12288 + 13, 100_003, (4 << 20) + 5, (16 << 20) - 1,
+                                  (16 << 20) + 7, (33 << 20) + 3])
+def test_crc32c_long_buffers_match_chained_short_calls(size):
+    # long buffers take the 3-way interleaved and multi-threaded paths; short
+    # calls (< 12 KiB each) take the single-chain path the golden vectors pin
+    import numpy as np
+
+    data = np.random.default_rng(size).integers(0, 256, size, dtype=np.uint8).tobytes()
+    want = 0x1234
+    for lo in range(0, size, 8000):
+        want = crc32c(data[lo:lo + 8000], want)
+    assert crc32c(data, 0x1234) == want
+    assert crc32c(b"123456789") == 0xE3069283
