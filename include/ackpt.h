@@ -296,6 +296,35 @@ ACKPT_API int ackpt_engine_calibrate(ackpt_engine* engine, ackpt_tier* tier, int
 /* Interval the last prepare chose. */
 ACKPT_API int64_t ackpt_engine_interval(const ackpt_engine* engine);
 
+/* ---- measured timeline (reporting parity with simulator.py:55-66) ----------
+ * With the timeline on, a run records every compute launch (per-step or
+ * fused, so one event may span several steps), every stall (compute-stream
+ * wait on a transfer, from/to = the step it happened at) and every transfer
+ * (copy-stream marks around the copy, plus file I/O for the file stage),
+ * in seconds since the run's start event.  Events come sorted by start. */
+enum {
+  ACKPT_EV_FORWARD = 0, /* "forward_compute" */
+  ACKPT_EV_BACKWARD = 1, /* "backward_compute" */
+  ACKPT_EV_STORE = 2,
+  ACKPT_EV_FETCH = 3,
+  ACKPT_EV_STALL = 4
+};
+enum { ACKPT_LANE_COMPUTE = 0, ACKPT_LANE_TRANSFER = 1 };
+typedef struct ackpt_timeline_event {
+  int32_t kind;
+  int32_t lane;
+  int64_t from_step;
+  int64_t to_step;
+  double start;
+  double end;
+} ackpt_timeline_event;
+/* Takes effect at the next prepare (adds two events per launch: a reporting
+ * mode, not for headline timing). */
+ACKPT_API int ackpt_engine_set_timeline(ackpt_engine* engine, int32_t on);
+/* Events of the last run: *len = count; the first min(cap, count) are copied. */
+ACKPT_API int ackpt_engine_timeline(const ackpt_engine* engine, ackpt_timeline_event* out, int64_t cap,
+                                    int64_t* len);
+
 /* ---- CRC32C (storage.py:49-68), hardware crc32 instruction when present ---- */
 ACKPT_API uint32_t ackpt_crc32c(const void* data, int64_t len, uint32_t crc);
 

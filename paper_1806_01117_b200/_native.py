@@ -84,6 +84,14 @@ class Stats(C.Structure):
     ]
 
 
+class TimelineEvent(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("lane", C.c_int32), ("from_step", C.c_int64), ("to_step", C.c_int64),
+                ("start", C.c_double), ("end", C.c_double)]
+
+
+EV_KINDS = ("forward_compute", "backward_compute", "store", "fetch", "stall")
+LANES = ("compute", "transfer")
+
 FORWARD_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p)
 BACKWARD_FN = C.CFUNCTYPE(
     C.c_int, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p
@@ -172,6 +180,8 @@ _SIGS = {
     "ackpt_engine_backward_sweep": ([_vp, _vp, _vp, C.POINTER(Stats), _vp], C.c_int),
     "ackpt_engine_calibrate": ([_vp, _vp, C.c_int64, _vp, _dp, _dp, _dp], C.c_int),
     "ackpt_engine_interval": ([_vp], C.c_int64),
+    "ackpt_engine_set_timeline": ([_vp, C.c_int32], C.c_int),
+    "ackpt_engine_timeline": ([_vp, C.POINTER(TimelineEvent), C.c_int64, _i64p], C.c_int),
     "ackpt_crc32c": ([_vp, C.c_int64, C.c_uint32], C.c_uint32),
 }
 

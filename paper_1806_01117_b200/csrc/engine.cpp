@@ -46,6 +46,8 @@ cudaEvent_t tier_ticket_event(ackpt_tier* t, ackpt_ticket id);
 int tier_ticket_status(ackpt_tier* t, ackpt_ticket id, std::string* msg);
 int tier_async_status(ackpt_tier* t, ackpt_ticket id, std::string* msg);
 void tier_retire(ackpt_tier* t, ackpt_ticket id);
+void tier_set_timing(ackpt_tier* t, bool on);
+bool tier_ticket_times(ackpt_tier* t, ackpt_ticket id, cudaEvent_t* t0, cudaEvent_t* t1);
 int64_t tier_slot_bytes(const ackpt_tier* t);
 cudaStream_t tier_d2h(const ackpt_tier* t);
 }  // namespace ackpt
@@ -81,6 +83,8 @@ struct ackpt_engine {
   int fuse = 0;
   int prefetch = -1;
   int64_t sample_every = 0;
+  int timeline = 0;                               // record a measured event timeline
+  std::vector<ackpt_timeline_event> timeline_out;  // of the last run
 };
 
 namespace ackpt {
@@ -135,6 +139,36 @@ struct Run {
   // timing events
   size_t next_ev = 0;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> stall_pairs;
+  // measured timeline (ackpt_engine_set_timeline): compute launches and
+  // stalls bracketed by events on the compute stream, transfers by the
+  // tier's marks on its copy streams
+  struct Span {
+    int32_t kind;
+    int64_t from, to;
+    cudaEvent_t e0, e1;
+  };
+  struct Xfer {
+    int32_t kind;
+    int64_t key;
+    ackpt_ticket id;
+  };
+  std::vector<Span> spans;
+  std::vector<Xfer> xfers;
+
+  // Runs `launch` (skipped in the dry run), bracketed by timeline events.
+  template <class F>
+  void span(int32_t kind, int64_t from, int64_t to, F&& launch) {
+    if (!E->timeline) {
+      if (!dry) launch();
+      return;
+    }
+    cudaEvent_t e0 = timing_event(), e1 = timing_event();
+    if (dry) return;
+    ACKPT_CUDA_CHECK(cudaEventRecord(e0, s));
+    launch();
+    ACKPT_CUDA_CHECK(cudaEventRecord(e1, s));
+    spans.push_back({kind, from, to, e0, e1});
+  }
 
   Run(ackpt_engine* e, bool d, cudaStream_t str) : E(e), dry(d), s(str) {
     if (!dry) {
@@ -174,7 +208,11 @@ struct Run {
       ++next_ev;
       return nullptr;
     }
-    if (next_ev >= E->timing.size()) fail(ACKPT_EXECUTION_ERROR, "timing-event pool exhausted");
+    if (next_ev >= E->timing.size()) {  // the dry run sized the pool; grow if a mode changed since
+      cudaEvent_t ev;
+      ACKPT_CUDA_CHECK(cudaEventCreate(&ev));
+      E->timing.push_back(ev);
+    }
     return E->timing[next_ev++];
   }
 
@@ -216,9 +254,11 @@ struct Run {
 
   int forward(int64_t step, int cur) {
     int out = acquire();
-    timed(fwd_calls, fwd_pairs, [&] {
-      check_op(E->op.forward(E->op.ctx, step, ptr(cur), wptr(out), s));
-      ++st.kernel_launches;
+    span(ACKPT_EV_FORWARD, step, step + 1, [&] {
+      timed(fwd_calls, fwd_pairs, [&] {
+        check_op(E->op.forward(E->op.ctx, step, ptr(cur), wptr(out), s));
+        ++st.kernel_launches;
+      });
     });
     release(cur);
     ++st.forward_evals;
@@ -232,10 +272,10 @@ struct Run {
     // (length 1 too: a fused execution uses the fused kernel family throughout)
     if (to - from >= 1 && E->fuse && E->op.advance) {
       int out = acquire();
-      if (!dry) {
+      span(ACKPT_EV_FORWARD, from, to, [&] {
         check_op(E->op.advance(E->op.ctx, from, to, ptr(cur), wptr(out), s));
         ++st.kernel_launches;
-      }
+      });
       release(cur);
       st.forward_evals += to - from;
       ++st.fused_advances;
@@ -249,16 +289,18 @@ struct Run {
   void backward(int64_t step, int state) {
     if (!seeded)
       fail(ACKPT_EXECUTION_ERROR, "Reverse " + std::to_string(step) + " before the adjoint was seeded");
-    timed(bwd_calls, bwd_pairs, [&] {
-      check_op(E->op.backward(E->op.ctx, step, ptr(state), adj[a], adj[1 - a], s));
-      ++st.kernel_launches;
+    span(ACKPT_EV_BACKWARD, step, step + 1, [&] {
+      timed(bwd_calls, bwd_pairs, [&] {
+        check_op(E->op.backward(E->op.ctx, step, ptr(state), adj[a], adj[1 - a], s));
+        ++st.kernel_launches;
+      });
     });
     a = 1 - a;
     ++st.backward_evals;
   }
 
   // -- transfers ------------------------------------------------------------
-  void wait_transfer(ackpt_ticket t) {
+  void wait_transfer(ackpt_ticket t, int64_t at_step) {
     // runtime.py:192-199.  Errors captured by the transfer surface here.
     if (dry) {
       next_ev += 2;
@@ -273,6 +315,7 @@ struct Run {
     if (done) ACKPT_CUDA_CHECK(cudaStreamWaitEvent(s, done, 0));
     ACKPT_CUDA_CHECK(cudaEventRecord(after, s));
     stall_pairs.emplace_back(before, after);
+    if (E->timeline) spans.push_back({ACKPT_EV_STALL, at_step, at_step, before, after});
   }
 
   std::vector<ackpt_ticket> issued;  // checked for file-stage errors after the run
@@ -282,6 +325,7 @@ struct Run {
     if (!dry) {
       check_op(ackpt_tier_begin_store(E->tier, key, key, ptr(state), E->S, s, &t));
       issued.push_back(t);
+      if (E->timeline) xfers.push_back({ACKPT_EV_STORE, key, t});
     }
     ++st.stores_issued;
     st.link_bytes += E->S;
@@ -294,6 +338,7 @@ struct Run {
       int rc = ackpt_tier_begin_fetch(E->tier, key, wptr(dst), E->S, s, &t);
       if (rc != ACKPT_OK) fail(rc, ackpt_last_error());
       issued.push_back(t);
+      if (E->timeline) xfers.push_back({ACKPT_EV_FETCH, key, t});
     }
     ++st.prefetches_issued;
     st.link_bytes += E->S;
@@ -342,10 +387,10 @@ struct Run {
               tape.emplace_back(rel + i + 1, ids[i]);
               ledger.add_tape(E->S);
             }
-            if (!dry) {
+            span(ACKPT_EV_FORWARD, offset + rel, offset + rel + cnt, [&] {
               check_op(E->op.forward_many(E->op.ctx, offset + rel, cnt, ptr(state), outs, s));
               ++st.kernel_launches;
-            }
+            });
             release(state);
             state = ids[cnt - 1];
             st.forward_evals += cnt;
@@ -412,10 +457,10 @@ struct Run {
           tape.pop_back();
           ledger.drop_tape(E->S);
         }
-        if (!dry) {
+        span(ACKPT_EV_BACKWARD, offset + lo, offset + lo + int64_t(run), [&] {
           check_op(E->op.backward_many(E->op.ctx, offset + lo, int64_t(run), states, adj[a], adj[1 - a], s));
           ++st.kernel_launches;
-        }
+        });
         a = 1 - a;
         st.backward_evals += int64_t(run);
         for (size_t r = 0; r < run; ++r) release(held[r]);
@@ -449,7 +494,7 @@ struct Run {
     for (size_t idx = 0; idx < bs.size(); ++idx) {
       const int64_t b = bs[idx];
       if (have) {
-        wait_transfer(ticket);
+        wait_transfer(ticket, b);
         ledger.drop_transfer(E->S);
         release(store_src);
       }
@@ -462,7 +507,7 @@ struct Run {
       state = advance(b, end, state);
     }
     if (have) {
-      wait_transfer(ticket);
+      wait_transfer(ticket, E->n);
       ledger.drop_transfer(E->S);
       release(store_src);
     }
@@ -487,7 +532,7 @@ struct Run {
       auto it = tickets.find(start);
       auto tk = it->second;
       tickets.erase(it);
-      wait_transfer(tk.first);
+      wait_transfer(tk.first, start);
       if (pf && jj > 0) issue(bs[jj - 1]);
       ledger.drop_transfer(E->S);  // fetched bytes go live
       const SegPlan& plan = E->seg_by_len.at(end - start);
@@ -628,6 +673,23 @@ void run_impl(ackpt_engine* E, Mode mode, const void* initial_state, const void*
   r.st.fwd_samples = int64_t(r.fwd_pairs.size());
   r.st.bwd_sample_seconds = sum_pairs(r.bwd_pairs);
   r.st.bwd_samples = int64_t(r.bwd_pairs.size());
+  E->timeline_out.clear();
+  if (E->timeline) {
+    auto since = [&](cudaEvent_t ev) {
+      float msv = 0.f;
+      ACKPT_CUDA_CHECK(cudaEventElapsedTime(&msv, E->ev_start, ev));
+      return double(msv) * 1e-3;
+    };
+    for (const auto& sp : r.spans)
+      E->timeline_out.push_back({sp.kind, ACKPT_LANE_COMPUTE, sp.from, sp.to, since(sp.e0), since(sp.e1)});
+    for (const auto& x : r.xfers) {
+      cudaEvent_t t0 = nullptr, t1 = nullptr;
+      if (tier_ticket_times(E->tier, x.id, &t0, &t1))
+        E->timeline_out.push_back({x.kind, ACKPT_LANE_TRANSFER, x.key, x.key, since(t0), since(t1)});
+    }
+    std::stable_sort(E->timeline_out.begin(), E->timeline_out.end(),
+                     [](const ackpt_timeline_event& a, const ackpt_timeline_event& b) { return a.start < b.start; });
+  }
   if (stats) *stats = r.st;
 }
 
@@ -726,6 +788,7 @@ ACKPT_API int ackpt_engine_prepare(ackpt_engine* E, int32_t strategy, int64_t sl
     } else {
       fail(ACKPT_VALUE_ERROR, "unknown strategy " + std::to_string(strategy));
     }
+    if (tier) tier_set_timing(tier, E->timeline != 0);
     // Dry run: sizes the HBM pool and the timing-event pool exactly.
     Run r(E, true, nullptr);
     r.adj[0] = r.adj[1] = nullptr;
@@ -752,6 +815,20 @@ ACKPT_API int ackpt_engine_set_kernel_sampling(ackpt_engine* e, int64_t every) {
   e->sample_every = every < 0 ? 0 : every;
   e->prepared = false;  // the timing-event pool is sized by the next prepare
   return ACKPT_OK;
+}
+
+ACKPT_API int ackpt_engine_set_timeline(ackpt_engine* e, int32_t on) {
+  e->timeline = on ? 1 : 0;
+  e->prepared = false;  // the event pool and the tier's marks are set by the next prepare
+  return ACKPT_OK;
+}
+
+ACKPT_API int ackpt_engine_timeline(const ackpt_engine* e, ackpt_timeline_event* out, int64_t cap, int64_t* len) {
+  return ackpt::guard([&] {
+    if (!e || !len) ackpt::fail(ACKPT_VALUE_ERROR, "engine and len are required");
+    *len = int64_t(e->timeline_out.size());
+    for (int64_t i = 0; i < std::min(cap, *len); ++i) out[i] = e->timeline_out[size_t(i)];
+  });
 }
 
 ACKPT_API int ackpt_engine_set_prefetch(ackpt_engine* e, int32_t prefetch) {

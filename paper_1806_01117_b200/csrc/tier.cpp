@@ -48,6 +48,7 @@ struct TierTicket {
   std::string msg;
   bool complete = false;
   double hold_seconds = 0.0;  // throttle: host-func sleep on the copy stream
+  cudaEvent_t t0 = nullptr, t1 = nullptr;  // timeline marks (copy start / done)
   // file stage
   std::shared_ptr<AsyncStatus> async;
   ackpt_tier* tier = nullptr;
@@ -77,6 +78,8 @@ struct ackpt_tier {
   std::deque<ackpt::TierTicket> tickets;
   std::vector<cudaEvent_t> event_pool;
   std::vector<cudaEvent_t> all_events;
+  bool timing = false;                   // record timeline marks around transfers
+  std::vector<cudaEvent_t> timing_pool;  // timing-enabled events (in all_events too)
   cudaStream_t d2h = nullptr, h2d = nullptr;
   cudaEvent_t after = nullptr;
   double latency_s = 0.0, bandwidth = 0.0;
@@ -102,6 +105,21 @@ cudaEvent_t new_event(ackpt_tier* t) {
   cudaEvent_t e;
   ACKPT_CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   t->all_events.push_back(e);
+  return e;
+}
+
+// Timeline mark on a copy stream (nullptr unless the engine asked for a timeline).
+cudaEvent_t mark(ackpt_tier* t, cudaStream_t s) {
+  if (!t->timing) return nullptr;
+  cudaEvent_t e;
+  if (!t->timing_pool.empty()) {
+    e = t->timing_pool.back();
+    t->timing_pool.pop_back();
+  } else {
+    ACKPT_CUDA_CHECK(cudaEventCreate(&e));
+    t->all_events.push_back(e);
+  }
+  ACKPT_CUDA_CHECK(cudaEventRecord(e, s));
   return e;
 }
 
@@ -154,6 +172,11 @@ void retire(ackpt_tier* t, TierTicket& tk) {
     t->event_pool.push_back(tk.done);
     tk.done = nullptr;
   }
+  for (cudaEvent_t* e : {&tk.t0, &tk.t1})
+    if (*e) {
+      t->timing_pool.push_back(*e);
+      *e = nullptr;
+    }
 }
 
 // ---- file stage: CKPT format (storage.py:9-18, 83-127) ----------------------
@@ -391,6 +414,18 @@ int tier_ticket_status(ackpt_tier* t, ackpt_ticket id, std::string* msg) {
   if (msg) *msg = tk.msg;
   return tk.err;
 }
+void tier_set_timing(ackpt_tier* t, bool on) {
+  std::lock_guard<std::mutex> lk(t->mu);
+  t->timing = on;
+}
+bool tier_ticket_times(ackpt_tier* t, ackpt_ticket id, cudaEvent_t* t0, cudaEvent_t* t1) {
+  std::lock_guard<std::mutex> lk(t->mu);
+  TierTicket& tk = get_ticket(t, id);
+  *t0 = tk.t0;
+  *t1 = tk.t1;
+  return tk.t0 && tk.t1;
+}
+
 void tier_retire(ackpt_tier* t, ackpt_ticket id) {
   std::lock_guard<std::mutex> lk(t->mu);
   retire(t, get_ticket(t, id));
@@ -482,6 +517,7 @@ ACKPT_API int ackpt_tier_begin_store(ackpt_tier* t, int64_t key, int64_t step, c
         ACKPT_CUDA_CHECK(cudaStreamWaitEvent(t->d2h, t->after, 0));
       }
       if (ke.fetched) ACKPT_CUDA_CHECK(cudaStreamWaitEvent(t->d2h, ke.last_fetch, 0));
+      cudaEvent_t m0 = ackpt::mark(t, t->d2h);
       if (bytes > 0)
         ACKPT_CUDA_CHECK(cudaMemcpyAsync(t->stage_out, src, size_t(bytes), cudaMemcpyDeviceToHost, t->d2h));
       ke.step = step;
@@ -495,6 +531,8 @@ ACKPT_API int ackpt_tier_begin_store(ackpt_tier* t, int64_t key, int64_t step, c
       ackpt::hold(t, t->d2h, ref, bytes);
       ref.done = ackpt::new_event(t);
       ACKPT_CUDA_CHECK(cudaEventRecord(ref.done, t->d2h));
+      ref.t0 = m0;
+      ref.t1 = ackpt::mark(t, t->d2h);
       if (!ke.last_store) ACKPT_CUDA_CHECK(cudaEventCreateWithFlags(&ke.last_store, cudaEventDisableTiming));
       ACKPT_CUDA_CHECK(cudaEventRecord(ke.last_store, t->d2h));
       ke.stored = true;
@@ -517,6 +555,7 @@ ACKPT_API int ackpt_tier_begin_store(ackpt_tier* t, int64_t key, int64_t step, c
       ACKPT_CUDA_CHECK(cudaStreamWaitEvent(t->d2h, t->after, 0));
     }
     if (ke.fetched) ACKPT_CUDA_CHECK(cudaStreamWaitEvent(t->d2h, ke.last_fetch, 0));
+    cudaEvent_t m0 = ackpt::mark(t, t->d2h);
     if (bytes > 0)
       ACKPT_CUDA_CHECK(cudaMemcpyAsync(ackpt::key_ptr(t, ke), src, size_t(bytes),
                                        cudaMemcpyDeviceToHost, t->d2h));
@@ -527,6 +566,8 @@ ACKPT_API int ackpt_tier_begin_store(ackpt_tier* t, int64_t key, int64_t step, c
     ackpt::hold(t, t->d2h, ref, bytes);
     ref.done = ackpt::new_event(t);
     ACKPT_CUDA_CHECK(cudaEventRecord(ref.done, t->d2h));
+    ref.t0 = m0;
+    ref.t1 = ackpt::mark(t, t->d2h);
     if (!ke.last_store) ACKPT_CUDA_CHECK(cudaEventCreateWithFlags(&ke.last_store, cudaEventDisableTiming));
     ACKPT_CUDA_CHECK(cudaEventRecord(ke.last_store, t->d2h));
     ke.stored = true;
@@ -570,6 +611,7 @@ ACKPT_API int ackpt_tier_begin_fetch(ackpt_tier* t, int64_t key, void* dst, int6
         ACKPT_CUDA_CHECK(cudaStreamWaitEvent(t->h2d, t->after, 0));
       }
       if (ke.stored) ACKPT_CUDA_CHECK(cudaStreamWaitEvent(t->h2d, ke.last_store, 0));
+      cudaEvent_t m0 = ackpt::mark(t, t->h2d);
       ackpt_ticket id = ackpt::add_ticket(t, std::move(tk));
       ackpt::TierTicket& ref = t->tickets[size_t(id)];
       ref.tier = t;
@@ -581,6 +623,8 @@ ACKPT_API int ackpt_tier_begin_fetch(ackpt_tier* t, int64_t key, void* dst, int6
       ackpt::hold(t, t->h2d, ref, len);
       ref.done = ackpt::new_event(t);
       ACKPT_CUDA_CHECK(cudaEventRecord(ref.done, t->h2d));
+      ref.t0 = m0;
+      ref.t1 = ackpt::mark(t, t->h2d);
       if (!ke.last_fetch) ACKPT_CUDA_CHECK(cudaEventCreateWithFlags(&ke.last_fetch, cudaEventDisableTiming));
       ACKPT_CUDA_CHECK(cudaEventRecord(ke.last_fetch, t->h2d));
       ke.fetched = true;
@@ -609,6 +653,7 @@ ACKPT_API int ackpt_tier_begin_fetch(ackpt_tier* t, int64_t key, void* dst, int6
       ACKPT_CUDA_CHECK(cudaStreamWaitEvent(t->h2d, t->after, 0));
     }
     ACKPT_CUDA_CHECK(cudaStreamWaitEvent(t->h2d, ke.last_store, 0));
+    cudaEvent_t m0 = ackpt::mark(t, t->h2d);
     if (ke.len > 0)
       ACKPT_CUDA_CHECK(cudaMemcpyAsync(dst, ackpt::key_ptr(t, ke), size_t(ke.len),
                                        cudaMemcpyHostToDevice, t->h2d));
@@ -617,6 +662,8 @@ ACKPT_API int ackpt_tier_begin_fetch(ackpt_tier* t, int64_t key, void* dst, int6
     ackpt::hold(t, t->h2d, ref, ke.len);
     ref.done = ackpt::new_event(t);
     ACKPT_CUDA_CHECK(cudaEventRecord(ref.done, t->h2d));
+    ref.t0 = m0;
+    ref.t1 = ackpt::mark(t, t->h2d);
     if (!ke.last_fetch) ACKPT_CUDA_CHECK(cudaEventCreateWithFlags(&ke.last_fetch, cudaEventDisableTiming));
     ACKPT_CUDA_CHECK(cudaEventRecord(ke.last_fetch, t->h2d));
     ke.fetched = true;

@@ -356,9 +356,12 @@ def bench(
     batch: int = 1,
     dtype="f64",
     fuse: bool = False,
+    timeline_path: Optional[str] = None,
 ) -> BenchReport:
     """One forward/backward iteration timed as the minimum over ``runs``
-    (lstm.py:219-254); batch=1/f64 reproduces the reference's workload."""
+    (lstm.py:219-254); batch=1/f64 reproduces the reference's workload.
+    ``timeline_path``: also write the fastest run's measured event timeline
+    there (simulator JSON format; total = the compute stream's time)."""
     cell = random_cell(d, n, seed)
     ops = operator_pair(cell, batch, dtype)
     if batch == 1 and _torch_dtype(dtype) == torch.float64:
@@ -370,9 +373,14 @@ def bench(
         best: Optional[ExecutionStats] = None
         adjoint = b""
         for _ in range(max(1, runs)):
-            adjoint, stats = execute(strategy, ops, state0, backend, fuse=fuse)
+            adjoint, stats = execute(strategy, ops, state0, backend, fuse=fuse, timeline=timeline_path is not None)
             if best is None or stats.wall_seconds < best.wall_seconds:
                 best = stats
+        if timeline_path is not None:
+            from .simulator import timeline_to_json
+
+            with open(timeline_path, "w") as fh:
+                fh.write(timeline_to_json(strategy, best.timeline, best.device["gpu_seconds"]))
         return BenchReport(
             n=n,
             strategy=_strategy_label(strategy),

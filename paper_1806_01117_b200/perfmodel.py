@@ -92,3 +92,31 @@ def overhead_model(n: int, s: int, interval: int, t_a: float, t_b: float) -> dic
         "revolve_seconds": rv,
         "revolve_overhead": (rv / t_inf) if rv else None,
     }
+
+
+def emit_curves(s: int, intervals, n_max: int) -> list:
+    """Recompute-factor curves over n = 1, 2, 4, ... <= n_max: the single-level
+    Revolve(s) factor and, per interval I, the two-level factor R(min(I, n), s)
+    (flat once n passes I) -- the reference's emit_curves (perfmodel.py)."""
+    if n_max < 1:
+        raise ValueError(f"n_max must be >= 1, got {n_max}")
+    rows = []
+    n = 1
+    while n <= n_max:
+        row = {"n": n, "revolve": recompute_factor(n, s)}
+        for interval in intervals:
+            row[f"async_I{interval}"] = recompute_factor(min(interval, n), s)
+        rows.append(row)
+        n *= 2
+    return rows
+
+
+def curves_to_csv(rows) -> str:
+    """CSV of emit_curves rows, factors with 6 significant digits."""
+    rows = list(rows)
+    if not rows:
+        return ""
+    cols = list(rows[0])
+    body = [",".join(cols)]
+    body += [",".join([str(r["n"])] + [f"{float(r[c]):.6g}" for c in cols[1:]]) for r in rows]
+    return "\n".join(body) + "\n"

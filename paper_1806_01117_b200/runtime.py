@@ -113,6 +113,7 @@ def _stats_from(st: N.Stats) -> ExecutionStats:
         peak_l1_bytes=st.peak_l1_bytes,
         wall_seconds=st.wall_seconds,
     )
+    out.timeline = None
     out.device = {
         "gpu_seconds": st.gpu_seconds,
         "kernel_launches": st.kernel_launches,
@@ -351,6 +352,7 @@ def execute(
     *,
     fuse: bool = False,
     sample_kernels: int = 0,
+    timeline: bool = False,
 ):
     """One forward/backward pass; returns (step-0 adjoint, stats).
 
@@ -358,7 +360,10 @@ def execute(
     no atomics).  Multistage requires a backend.  ``fuse=True`` runs each
     Advance action as one fused launch (counters unchanged).  Planning,
     calibration and HBM pool allocation happen before the timed window
-    (runtime.py:355-363).
+    (runtime.py:355-363).  ``timeline=True`` also records the measured event
+    timeline (``stats.timeline``: simulator.TimelineEvent list, seconds since
+    the run's start; one compute event per launch) at two CUDA events per
+    launch -- a reporting mode, not for headline timing.
     """
     if nbytes_of(initial_state) != ops.state_size:
         raise SizeMismatch(
@@ -379,8 +384,9 @@ def execute(
         raise TypeError(f"unknown strategy {strategy!r}")
     engine, cb = _engine_for(ops)
     N.check(N.lib.ackpt_engine_set_kernel_sampling(engine.handle, int(sample_kernels)))
-    _prepare(engine, code, slots, interval, tier)
+    N.check(N.lib.ackpt_engine_set_timeline(engine.handle, 1 if timeline else 0))
     N.check(N.lib.ackpt_engine_set_fusion(engine.handle, 1 if fuse else 0))
+    _prepare(engine, code, slots, interval, tier)
     state = _device_state(initial_state)
     out = _output_like(initial_state)
     seed_ptr, seed_keep = _seed_ptr(ops, cb)
@@ -389,7 +395,21 @@ def execute(
     if cb is not None:
         cb.raise_pending()
     N.check(rc)
-    return _finish(out, initial_state), _stats_from(st)
+    stats = _stats_from(st)
+    if timeline:
+        stats.timeline = _timeline(engine)
+    return _finish(out, initial_state), stats
+
+
+def _timeline(engine: _Engine) -> list:
+    from .simulator import TimelineEvent
+
+    count = C.c_int64(0)
+    N.check(N.lib.ackpt_engine_timeline(engine.handle, None, 0, C.byref(count)))
+    buf = (N.TimelineEvent * max(1, count.value))()
+    N.check(N.lib.ackpt_engine_timeline(engine.handle, buf, count.value, C.byref(count)))
+    return [TimelineEvent(N.EV_KINDS[e.kind], int(e.from_step), int(e.to_step), float(e.start), float(e.end),
+                          N.LANES[e.lane]) for e in buf[:count.value]]
 
 
 def _sweep_engine(plan: MultistagePlan, ops: OperatorPair, backend) -> _Engine:

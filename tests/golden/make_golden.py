@@ -155,6 +155,56 @@ def storage_golden() -> dict:
     return {"crc32c": crcs, "chained_hello_world": chained, "encoded_step5": blob.hex(), "encoded_step123456789": blob2.hex()}
 
 
+SIM_CASES = [
+    # strategy, n, s, t_a, t_b, t_t, interval
+    ("full", 6, 2, 1.0, 2.0, 3.5, None),
+    ("revolve", 10, 3, 1.0, 2.0, 3.5, None),
+    ("revolve", 33, 4, 0.001, 0.0025, 0.035, None),
+    ("multistage", 24, 2, 1.0, 2.0, 7.0, None),      # calibrated I = 7, no stalls
+    ("multistage", 24, 2, 1.0, 2.0, 7.0, 4),         # forced I < t_t / t_a: stalls
+    ("multistage", 40, 6, 0.001, 0.0025, 0.035, None),
+    ("multistage", 64, 3, 1.0, 1.5, 2.5, 8),
+    ("multistage", 10, 3, 1.0, 2.0, 50.0, None),     # I >= n: fallback
+]
+
+CURVE_CASES = [(4, [8, 64], 1024), (10, [60], 10000), (1, [2, 3], 64)]
+
+
+def reporting_golden() -> dict:
+    """simulator timelines, model curves and CLI outputs of the reference
+    (simulator.py, perfmodel.emit_curves / curves_to_csv, cli.py)."""
+    from asyncckpt import cli as RC  # noqa: E402
+    from asyncckpt import simulator as RSIM  # noqa: E402
+    import contextlib
+    import io
+
+    sims = []
+    for kind, n, s, ta, tb, tt, interval in SIM_CASES:
+        strat = {"full": RR.FullStorage(), "revolve": RR.Revolve(s), "multistage": RR.Multistage(s, interval)}[kind]
+        events, total = RSIM.simulate(strat, RP.PerfParams(n=n, s=s, t_a=ta, t_b=tb, t_t=tt))
+        sims.append({"case": [kind, n, s, ta, tb, tt, interval],
+                     "json": RSIM.timeline_to_json(strat, events, total),
+                     "t_model": {"full": RP.t_infinity, "revolve": RP.t_revolve,
+                                 "multistage": RP.t_async}[kind](RP.PerfParams(n=n, s=s, t_a=ta, t_b=tb, t_t=tt))})
+    curves = []
+    for s, intervals, n_max in CURVE_CASES:
+        curves.append({"case": [s, intervals, n_max], "csv": RP.curves_to_csv(RP.emit_curves(s, intervals, n_max))})
+    cli = []
+    for argv in (["schedule", "--n", "10", "--s", "3"], ["schedule", "--n", "24", "--s", "2", "--interval", "8"],
+                 ["schedule", "--n", "10", "--s", "2", "--interval", "40"],
+                 ["model", "--s", "4", "--intervals", "8,64", "--n-max", "256"],
+                 ["model", "--s", "3", "--n-max", "64", "--ta", "0.001", "--tt", "0.035"],
+                 ["simulate", "--strategy", "multistage", "--n", "24", "--s", "2", "--ta", "1", "--tb", "2",
+                  "--tt", "7"],
+                 ["simulate", "--strategy", "revolve", "--n", "12", "--s", "3", "--ta", "1", "--tb", "2", "--tt", "1"],
+                 ["schedule", "--n", "5", "--s", "0"]):
+        out, err = io.StringIO(), io.StringIO()
+        with contextlib.redirect_stdout(out), contextlib.redirect_stderr(err):
+            rc = RC.main(argv)
+        cli.append({"argv": argv, "rc": rc, "stdout": out.getvalue(), "stderr_prefix": err.getvalue()[:60]})
+    return {"simulate": sims, "curves": curves, "cli": cli}
+
+
 def main() -> None:
     sched = schedule_golden()
     with open(os.path.join(HERE, "schedule_golden.json"), "w") as fh:
@@ -166,6 +216,8 @@ def main() -> None:
     np.savez_compressed(os.path.join(HERE, "step_golden.npz"), **step_golden())
     with open(os.path.join(HERE, "storage_golden.json"), "w") as fh:
         json.dump(storage_golden(), fh, indent=1)
+    with open(os.path.join(HERE, "reporting_golden.json"), "w") as fh:
+        json.dump(reporting_golden(), fh, indent=1)
     print("golden vectors written to", HERE)
 
 
