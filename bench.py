@@ -56,7 +56,7 @@ def parse_args(argv=None):
     p.add_argument("--no-cpu", action="store_true")
     p.add_argument("--full-n", type=int, default=1000, help="n of the measured FullStorage run")
     p.add_argument("--no-other-mode", action="store_true")
-    p.add_argument("--family", choices=["ffma2", "tcgen05", "mixed"], default="mixed",
+    p.add_argument("--family", choices=["ffma2", "tcgen05", "mixed"], default="tcgen05",
                    help="kernel family of the fused d=8 launches (lstm.set_kernel_family)")
     return p.parse_args(argv)
 
@@ -409,9 +409,14 @@ def main(argv=None) -> None:
     achieved = bytes_dom / t_dom / 1e9
     traffic = None
     tfile = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    base = dominant.split()[0]
+    kfam = "ffma2"  # which kernel family ran the dominant launch
+    if args.fuse and (args.family == "tcgen05" or (args.family == "mixed" and "rev" not in base)):
+        kfam = "tcgen05"
     if os.path.exists(tfile):
         with open(tfile) as fh:
-            traffic = json.load(fh).get(dominant.split()[0])
+            tj = json.load(fh)
+        traffic = tj.get(f"{base}@{kfam}", tj.get(base))
     link_gbs = S / t_t / 1e9
     if args.fuse:  # algorithmic HBM bytes of the fused pass
         hbm_bytes = int(args.n * S * (2 / 64 + 1 + 1) + last.backward_evals * S)
@@ -529,7 +534,7 @@ def main(argv=None) -> None:
             "host_wall_seconds_per_pass": host_elapsed / args.steps,
             "pass_roofline": {"seconds": pass_roofline, "frac": pass_roofline / (ms_per_step * 1e-3),
                               "hbm_bytes": hbm_bytes, "link_bytes": link_bytes},
-            "roofline": {"kernel": dominant, "bound": "hbm", "achieved": achieved, "peak": hbm_peak,
+            "roofline": {"kernel": f"{dominant} [{kfam}]", "bound": "hbm", "achieved": achieved, "peak": hbm_peak,
                          "unit": "GB/s", "frac": achieved / hbm_peak, "traffic": traffic,
                          "algorithmic_bytes_per_launch": bytes_dom, "avg_launch_us": t_dom * 1e6,
                          "timing": "CUDA events around back-to-back launches of the same kernel",

@@ -55,16 +55,17 @@ Variant variant() {
 }
 
 // Fused launches (advance / forward_many / backward_many) for d=8 pick a
-// kernel family: 0 packed FFMA2, 1 tcgen05 for all three, 2 "mixed" (default)
-// = tcgen05 forward launches (advance, forward_many) + FFMA2 reverse runs, the
-// fastest measured at the C2 shape.  Env ACKPT_TC=0/1/2 presets.  Families round differently (each within the
+// kernel family: 0 packed FFMA2, 1 tcgen05 for all three (default: the
+// fastest measured at the C2 shape), 2 "mixed" = tcgen05
+// forward launches (advance, forward_many) + FFMA2 reverse runs.  Env
+// ACKPT_TC=0/1/2 presets.  Families round differently (each within the
 // fp32 tolerance); within one family the strategies stay bit-identical.
 std::atomic<int> g_family{-1};  // -1: not yet read from the environment
 int family() {
   int f = g_family.load(std::memory_order_relaxed);
   if (f < 0) {
     const char* e = std::getenv("ACKPT_TC");
-    f = !e ? 2 : std::string(e) == "0" ? 0 : std::string(e) == "1" ? 1 : 2;
+    f = !e ? 1 : std::string(e) == "0" ? 0 : std::string(e) == "2" ? 2 : 1;
     g_family.store(f, std::memory_order_relaxed);
   }
   return f;

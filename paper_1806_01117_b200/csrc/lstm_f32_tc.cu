@@ -3,6 +3,7 @@
 
 #include <cstdint>
 #include <cstdlib>
+#include <string>
 
 namespace ackpt {
 
@@ -40,7 +41,23 @@ void tc_backward_many(const ackpt_lstm* c, int64_t from, int count, const float*
   for (int i = 0; i < count; ++i) sp.p[i] = states[i];
   bool pf = c->B % 4 == 0 && std::getenv("ACKPT_TC_NO_PF") == nullptr;
   for (int i = 0; i < count; ++i) pf = pf && !(reinterpret_cast<uintptr_t>(states[i]) & 15u);
-  if (pf)
+  // ACKPT_TC_REV: default / "1" gates on the tensor cores (rev_tc, fastest
+  // measured); "2" both matvecs on the tensor cores (rev_tc2: correct, but
+  // its second MMA round trip per step costs more than the FMA work it
+  // removes at 4 CTAs/SM), "2nr" the same with Newton rcp.
+  static const int rev = [] {
+    const char* e = std::getenv("ACKPT_TC_REV");
+    if (!e) return 1;
+    const std::string v(e);
+    return v == "2" ? 2 : v == "2nr" ? 3 : 1;
+  }();
+  if (pf && rev == 2)
+    tc::rev_tc2<false><<<tc_grid(c->B), tc::kThreads, 0, s>>>(
+        adj_in, adj_out, c->B, static_cast<const float*>(c->d_xbs), from, count, tc_weights(c), sp);
+  else if (pf && rev == 3)
+    tc::rev_tc2<true><<<tc_grid(c->B), tc::kThreads, 0, s>>>(
+        adj_in, adj_out, c->B, static_cast<const float*>(c->d_xbs), from, count, tc_weights(c), sp);
+  else if (pf)
     tc::rev_tc<true><<<tc_grid(c->B), tc::kThreads, 0, s>>>(
         adj_in, adj_out, c->B, static_cast<const float*>(c->d_xbs), from, count, tc_weights(c), sp);
   else
