@@ -174,7 +174,7 @@ ACKPT_API int ackpt_lstm_operator(ackpt_lstm* cell, ackpt_operator* out);
 /* Kernel family of the fused d=8 fp32 launches (advance / forward_many /
  * backward_many): 0 = packed FFMA2, 1 = tcgen05 tensor cores with the
  * 3xTF32 split (default), 2 = mixed (tcgen05 advance / forward_many, FFMA2
- * backward_many).  Families differ in rounding (all within the fp32
+ * backward_many), 3 = mma (warp-level mma.sync, register fragments, 3xTF32).  Families differ in rounding (all within the fp32
  * tolerance); switch only between executions.  Env ACKPT_TC=0/1/2 presets. */
 ACKPT_API int ackpt_set_fused_family(int32_t family);
 ACKPT_API int32_t ackpt_get_fused_family(void);

@@ -57,21 +57,23 @@ Variant variant() {
 // Fused launches (advance / forward_many / backward_many) for d=8 pick a
 // kernel family: 0 packed FFMA2, 1 tcgen05 for all three (default: the
 // fastest measured at the C2 shape), 2 "mixed" = tcgen05
-// forward launches (advance, forward_many) + FFMA2 reverse runs.  Env
-// ACKPT_TC=0/1/2 presets.  Families round differently (each within the
+// forward launches (advance, forward_many) + FFMA2 reverse runs, 3 "mma" =
+// warp-level mma.sync with register fragments for all three.  Env
+// ACKPT_TC=0/1/2/3 presets.  Families round differently (each within the
 // fp32 tolerance); within one family the strategies stay bit-identical.
 std::atomic<int> g_family{-1};  // -1: not yet read from the environment
 int family() {
   int f = g_family.load(std::memory_order_relaxed);
   if (f < 0) {
     const char* e = std::getenv("ACKPT_TC");
-    f = !e ? 1 : std::string(e) == "0" ? 0 : std::string(e) == "2" ? 2 : 1;
+    f = !e ? 1 : std::string(e) == "0" ? 0 : std::string(e) == "2" ? 2 : std::string(e) == "3" ? 3 : 1;
     g_family.store(f, std::memory_order_relaxed);
   }
   return f;
 }
-bool tc_fwd_on() { return family() != 0; }
+bool tc_fwd_on() { return family() == 1 || family() == 2; }
 bool tc_bwd_on() { return family() == 1; }
+bool hm_on() { return family() == 3; }
 
 // TMA path: d=8, B % 4 == 0 (16-byte row segments), 16-byte aligned rows.
 bool tma_ok(const ackpt_lstm* c, std::initializer_list<const void*> ptrs) {
@@ -172,6 +174,7 @@ ACKPT_API int ackpt_lstm_create(int32_t d, int64_t n_steps, int64_t batch, int32
           }
       ACKPT_CUDA_CHECK(cudaMalloc(&c->d_xbs, xbs.size() * sizeof(float)));
       ACKPT_CUDA_CHECK(cudaMemcpy(c->d_xbs, xbs.data(), xbs.size() * sizeof(float), cudaMemcpyHostToDevice));
+      if (d == 8) ackpt::hm_tables(c.get());
     }
     *out = c.release();
   });
@@ -183,6 +186,8 @@ ACKPT_API int ackpt_lstm_destroy(ackpt_lstm* cell) {
     if (cell->d_wh) cudaFree(cell->d_wh);
     if (cell->d_xb) cudaFree(cell->d_xb);
     if (cell->d_xbs) cudaFree(cell->d_xbs);
+    if (cell->d_frag_hm) cudaFree(cell->d_frag_hm);
+    if (cell->d_xbs_hm) cudaFree(cell->d_xbs_hm);
     delete cell;
   });
 }
@@ -230,7 +235,8 @@ ACKPT_API int ackpt_lstm_advance(const ackpt_lstm* cell, int64_t from_step, int6
     if (ackpt::f32_fast(cell, {state_in, state_out})) {
       auto i = static_cast<const float*>(state_in);
       auto o = static_cast<float*>(state_out);
-      if (cell->d == 8 && ackpt::tc_fwd_on()) ackpt::tc_advance(cell, from_step, int(to_step - from_step), i, o, s);
+      if (cell->d == 8 && ackpt::hm_on()) ackpt::hm_advance(cell, from_step, int(to_step - from_step), i, o, s);
+      else if (cell->d == 8 && ackpt::tc_fwd_on()) ackpt::tc_advance(cell, from_step, int(to_step - from_step), i, o, s);
       else if (cell->d == 8) ackpt::f32_advance<8>(cell, from_step, to_step, i, o, s);
       else ackpt::f32_advance<4>(cell, from_step, to_step, i, o, s);
     } else if (cell->dtype == ACKPT_F32) {
@@ -295,7 +301,8 @@ ACKPT_API int ackpt_lstm_forward_many(const ackpt_lstm* cell, int64_t from_step,
     if (fast) {
       auto in = static_cast<const float*>(state_in);
       auto outs = reinterpret_cast<float* const*>(states_out);
-      if (cell->d == 8 && ackpt::tc_fwd_on()) ackpt::tc_forward_many(cell, from_step, int(count), in, outs, s);
+      if (cell->d == 8 && ackpt::hm_on()) ackpt::hm_forward_many(cell, from_step, int(count), in, outs, s);
+      else if (cell->d == 8 && ackpt::tc_fwd_on()) ackpt::tc_forward_many(cell, from_step, int(count), in, outs, s);
       else if (cell->d == 8) ackpt::f32_forward_many<8>(cell, from_step, int(count), in, outs, s);
       else ackpt::f32_forward_many<4>(cell, from_step, int(count), in, outs, s);
       ackpt::check_launch();
@@ -323,7 +330,8 @@ ACKPT_API int ackpt_lstm_backward_many(const ackpt_lstm* cell, int64_t from_step
     auto sp = reinterpret_cast<const float* const*>(states);
     auto ai = static_cast<const float*>(adjoint_in);
     auto ao = static_cast<float*>(adjoint_out);
-    if (cell->d == 8 && ackpt::tc_bwd_on()) ackpt::tc_backward_many(cell, from_step, int(count), sp, ai, ao, s);
+    if (cell->d == 8 && ackpt::hm_on()) ackpt::hm_backward_many(cell, from_step, int(count), sp, ai, ao, s);
+    else if (cell->d == 8 && ackpt::tc_bwd_on()) ackpt::tc_backward_many(cell, from_step, int(count), sp, ai, ao, s);
     else if (cell->d == 8) ackpt::f32_backward_many<8>(cell, from_step, int(count), sp, ai, ao, s);
     else ackpt::f32_backward_many<4>(cell, from_step, int(count), sp, ai, ao, s);
     ackpt::check_launch();
@@ -360,7 +368,8 @@ ACKPT_API int ackpt_lstm_loss(const ackpt_lstm* cell, const void* final_state, v
 
 ACKPT_API int ackpt_set_fused_family(int32_t family) {
   return ackpt::guard([&] {
-    if (family < 0 || family > 2) ackpt::fail(ACKPT_VALUE_ERROR, "family must be 0 (ffma2), 1 (tcgen05) or 2 (mixed)");
+    if (family < 0 || family > 3)
+      ackpt::fail(ACKPT_VALUE_ERROR, "family must be 0 (ffma2), 1 (tcgen05), 2 (mixed) or 3 (mma)");
     ackpt::g_family.store(family);
   });
 }

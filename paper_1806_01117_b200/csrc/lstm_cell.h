@@ -19,6 +19,8 @@ struct ackpt_lstm {
   void* d_wh = nullptr;                             // 4 x d x d, dtype
   void* d_xb = nullptr;                             // n x 4 x d, dtype
   void* d_xbs = nullptr;  // n x 4 x d fp32, pre-scaled per gate (fp32 fast path, d <= 16)
+  void* d_frag_hm = nullptr;  // d = 8 fp32: per-lane mma.sync B fragments (lstm_f32_hm.cu)
+  void* d_xbs_hm = nullptr;   // d = 8 fp32: n x 4 x 8 per-thread scaled step biases
 };
 
 namespace ackpt {
@@ -58,6 +60,13 @@ void tc_advance(const ackpt_lstm* c, int64_t from, int count, const float* in, f
 void tc_forward_many(const ackpt_lstm* c, int64_t from, int count, const float* in, float* const* outs,
                      cudaStream_t s);
 void tc_backward_many(const ackpt_lstm* c, int64_t from, int count, const float* const* states, const float* adj_in,
+                      float* adj_out, cudaStream_t s);
+// Register-fragment tensor-core (mma.sync, 3xTF32) fused kernels, d = 8 (lstm_f32_hm.cu).
+void hm_tables(ackpt_lstm* c);
+void hm_advance(const ackpt_lstm* c, int64_t from, int count, const float* in, float* out, cudaStream_t s);
+void hm_forward_many(const ackpt_lstm* c, int64_t from, int count, const float* in, float* const* outs,
+                     cudaStream_t s);
+void hm_backward_many(const ackpt_lstm* c, int64_t from, int count, const float* const* states, const float* adj_in,
                       float* adj_out, cudaStream_t s);
 // Occupancy variants (MINB resident 256-thread CTAs per SM).
 template <int D, int MINB>

@@ -235,13 +235,14 @@ def _stream() -> int:
 
 def set_kernel_family(name: str) -> None:
     """Kernel family of the fused d=8 fp32 launches: "ffma2" (packed fp32
-    FMA), "tcgen05" (default: tensor cores, 3xTF32) or "mixed" (tcgen05
-    advance / forward_many, ffma2 backward_many).  All meet the fp32
+    FMA), "tcgen05" (default: tensor cores, 3xTF32), "mixed" (tcgen05
+    advance / forward_many, ffma2 backward_many) or "mma" (warp-level
+    mma.sync tensor cores with register fragments, 3xTF32).  All meet the fp32
     tolerance; they round differently, so switch only between executions."""
     N.check(N.lib.ackpt_set_fused_family(KERNEL_FAMILIES.index(name)))
 
 
-KERNEL_FAMILIES = ("ffma2", "tcgen05", "mixed")
+KERNEL_FAMILIES = ("ffma2", "tcgen05", "mixed", "mma")
 
 
 def kernel_family() -> str:

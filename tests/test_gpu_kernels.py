@@ -100,7 +100,7 @@ def test_seed_and_loss(P):
         assert L.rel_l2(losses, L.loss(ocell, x.astype(npdt).astype(np.float64))) <= tol
 
 
-@pytest.fixture(params=["ffma2", "tcgen05", "mixed"])
+@pytest.fixture(params=["ffma2", "tcgen05", "mixed", "mma"])
 def family(request, P):
     before = P.kernel_family()
     P.set_kernel_family(request.param)
@@ -110,7 +110,7 @@ def family(request, P):
 
 def _tensor_core_family(P, d, batch, dtype):
     # fused d=8 fp32 forward launches (even batch) run on tcgen05 with the 3xTF32 split
-    return P.kernel_family() in ("tcgen05", "mixed") and d == 8 and dtype == "f32" and batch % 2 == 0
+    return P.kernel_family() in ("tcgen05", "mixed", "mma") and d == 8 and dtype == "f32" and batch % 2 == 0
 
 
 @pytest.mark.parametrize("d,batch,dtype", [(8, 4096, "f32"), (4, 512, "f32"), (8, 7, "f32"), (6, 64, "f64")])
