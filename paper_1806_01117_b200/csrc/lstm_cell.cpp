@@ -161,7 +161,7 @@ ACKPT_API int ackpt_lstm_create(int32_t d, int64_t n_steps, int64_t batch, int32
     ACKPT_CUDA_CHECK(cudaMalloc(&c->d_xb, c->xb_t.size()));
     ACKPT_CUDA_CHECK(cudaMemcpy(c->d_wh, c->wh_t.data(), c->wh_t.size(), cudaMemcpyHostToDevice));
     ACKPT_CUDA_CHECK(cudaMemcpy(c->d_xb, c->xb_t.data(), c->xb_t.size(), cudaMemcpyHostToDevice));
-    if (dtype == ACKPT_F32 && d <= 16) {
+    if (dtype == ACKPT_F32 && d <= 32) {
       // per-gate pre-scaled projections for the fused fp32 advance (lstm_f32_math.cuh)
       const float scale[4] = {-1.4426950408889634f, -1.4426950408889634f, -1.4426950408889634f,
                               2.0f * 1.4426950408889634f};
@@ -175,6 +175,15 @@ ACKPT_API int ackpt_lstm_create(int32_t d, int64_t n_steps, int64_t batch, int32
       ACKPT_CUDA_CHECK(cudaMalloc(&c->d_xbs, xbs.size() * sizeof(float)));
       ACKPT_CUDA_CHECK(cudaMemcpy(c->d_xbs, xbs.data(), xbs.size() * sizeof(float), cudaMemcpyHostToDevice));
       if (d == 8) ackpt::hm_tables(c.get());
+      if (d == 16 || d == 32) {  // pre-scaled W for the tensor-core kernels
+        std::vector<float> ws(size_t(4) * D * D);
+        for (size_t g = 0; g < 4; ++g)
+          for (size_t j = 0; j < D; ++j)
+            for (size_t k = 0; k < D; ++k)
+              ws[(g * D + j) * D + k] = float(c->wh64[(g * D + j) * D + k] * double(scale[g]));
+        ACKPT_CUDA_CHECK(cudaMalloc(&c->d_ws, ws.size() * sizeof(float)));
+        ACKPT_CUDA_CHECK(cudaMemcpy(c->d_ws, ws.data(), ws.size() * sizeof(float), cudaMemcpyHostToDevice));
+      }
     }
     *out = c.release();
   });
@@ -188,6 +197,7 @@ ACKPT_API int ackpt_lstm_destroy(ackpt_lstm* cell) {
     if (cell->d_xbs) cudaFree(cell->d_xbs);
     if (cell->d_frag_hm) cudaFree(cell->d_frag_hm);
     if (cell->d_xbs_hm) cudaFree(cell->d_xbs_hm);
+    if (cell->d_ws) cudaFree(cell->d_ws);
     delete cell;
   });
 }
@@ -206,6 +216,9 @@ ACKPT_API int ackpt_lstm_forward(const ackpt_lstm* cell, int64_t step, const voi
       auto o = static_cast<float*>(state_out);
       if (ackpt::variant() == ackpt::Variant::kTma128) ackpt::tma_launch<8, 0, 128, 4>(cell, step, i, nullptr, o, s);
       else ackpt::tma_launch<8, 0, 256, 3>(cell, step, i, nullptr, o, s);
+    } else if (ackpt::tcd_ok(cell, {state_in, state_out})) {
+      ackpt::tcd_forward(cell, step, 1, static_cast<const float*>(state_in), static_cast<float*>(state_out), nullptr,
+                         s);
     } else if (ackpt::f32_fast(cell, {state_in, state_out})) {
       auto i = static_cast<const float*>(state_in);
       auto o = static_cast<float*>(state_out);
@@ -239,6 +252,9 @@ ACKPT_API int ackpt_lstm_advance(const ackpt_lstm* cell, int64_t from_step, int6
       else if (cell->d == 8 && ackpt::tc_fwd_on()) ackpt::tc_advance(cell, from_step, int(to_step - from_step), i, o, s);
       else if (cell->d == 8) ackpt::f32_advance<8>(cell, from_step, to_step, i, o, s);
       else ackpt::f32_advance<4>(cell, from_step, to_step, i, o, s);
+    } else if (ackpt::tcd_ok(cell, {state_in, state_out})) {
+      ackpt::tcd_forward(cell, from_step, int(to_step - from_step), static_cast<const float*>(state_in),
+                         static_cast<float*>(state_out), nullptr, s);
     } else if (cell->dtype == ACKPT_F32) {
       ackpt::generic_advance<float>(cell, from_step, to_step, static_cast<const float*>(state_in),
                                     static_cast<float*>(state_out), s);
@@ -265,6 +281,10 @@ ACKPT_API int ackpt_lstm_backward(const ackpt_lstm* cell, int64_t step, const vo
         case ackpt::Variant::kTmaBwd2: ackpt::tma_launch<8, 1, 256, 2>(cell, step, x, a, o, s); break;
         default: ackpt::tma_launch<8, 1, 256, 3>(cell, step, x, a, o, s);
       }
+    } else if (ackpt::tcd_ok(cell, {state, adjoint_in, adjoint_out})) {
+      const float* st = static_cast<const float*>(state);
+      ackpt::tcd_reverse(cell, step, 1, &st, static_cast<const float*>(adjoint_in), static_cast<float*>(adjoint_out),
+                         s);
     } else if (ackpt::f32_fast(cell, {state, adjoint_in, adjoint_out})) {
       auto x = static_cast<const float*>(state);
       auto a = static_cast<const float*>(adjoint_in);
@@ -308,6 +328,14 @@ ACKPT_API int ackpt_lstm_forward_many(const ackpt_lstm* cell, int64_t from_step,
       ackpt::check_launch();
       return;
     }
+    bool tcd = ackpt::tcd_ok(cell, {});
+    for (const void* q : all) tcd = tcd && !(reinterpret_cast<uintptr_t>(q) & 3u);
+    if (tcd) {
+      ackpt::tcd_forward(cell, from_step, int(count), static_cast<const float*>(state_in), nullptr,
+                         reinterpret_cast<float* const*>(states_out), s);
+      ackpt::check_launch();
+      return;
+    }
     const void* cur = state_in;  // per-step launches
     for (int64_t i = 0; i < count; ++i) {
       int rc = ackpt_lstm_forward(cell, from_step + i, cur, states_out[i], stream);
@@ -323,10 +351,18 @@ ACKPT_API int ackpt_lstm_backward_many(const ackpt_lstm* cell, int64_t from_step
   return ackpt::guard([&] {
     if (count < 1 || count > ACKPT_MAX_FUSED) ackpt::fail(ACKPT_VALUE_ERROR, "count must be in [1, 64]");
     if (from_step < 0 || from_step + count > cell->n) ackpt::fail(ACKPT_VALUE_ERROR, "steps out of range");
+    auto s = static_cast<cudaStream_t>(stream);
+    bool tcd = ackpt::tcd_ok(cell, {adjoint_in, adjoint_out});
+    for (int64_t i = 0; i < count; ++i) tcd = tcd && !(reinterpret_cast<uintptr_t>(states[i]) & 3u);
+    if (tcd) {
+      ackpt::tcd_reverse(cell, from_step, int(count), reinterpret_cast<const float* const*>(states),
+                         static_cast<const float*>(adjoint_in), static_cast<float*>(adjoint_out), s);
+      ackpt::check_launch();
+      return;
+    }
     bool fast = ackpt::f32_fast(cell, {adjoint_in, adjoint_out});
     for (int64_t i = 0; i < count; ++i) fast = fast && !(reinterpret_cast<uintptr_t>(states[i]) & 7u);
-    if (!fast) ackpt::fail(ACKPT_VALUE_ERROR, "fused backward needs the fp32 d in {4, 8} fast path");
-    auto s = static_cast<cudaStream_t>(stream);
+    if (!fast) ackpt::fail(ACKPT_VALUE_ERROR, "fused backward needs the fp32 fast path (d in {4, 8, 16, 32})");
     auto sp = reinterpret_cast<const float* const*>(states);
     auto ai = static_cast<const float*>(adjoint_in);
     auto ao = static_cast<float*>(adjoint_out);
@@ -385,7 +421,8 @@ ACKPT_API int ackpt_lstm_operator(ackpt_lstm* cell, ackpt_operator* out) {
     out->advance = ackpt::lstm_op_advance;
     out->state_bytes = ackpt_lstm_state_bytes(cell);
     out->n_steps = cell->n;
-    const bool fused = cell->dtype == ACKPT_F32 && (cell->d == 4 || cell->d == 8) && !(cell->B & 1);
+    const bool fused = (cell->dtype == ACKPT_F32 && (cell->d == 4 || cell->d == 8) && !(cell->B & 1)) ||
+                       ackpt::tcd_ok(cell, {});
     out->forward_many = fused ? ackpt::lstm_op_forward_many : nullptr;
     out->backward_many = fused ? ackpt::lstm_op_backward_many : nullptr;
   });

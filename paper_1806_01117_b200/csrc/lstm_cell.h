@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <initializer_list>
 #include <vector>
 
 #include "common.h"
@@ -21,6 +22,7 @@ struct ackpt_lstm {
   void* d_xbs = nullptr;  // n x 4 x d fp32, pre-scaled per gate (fp32 fast path, d <= 16)
   void* d_frag_hm = nullptr;  // d = 8 fp32: per-lane mma.sync B fragments (lstm_f32_hm.cu)
   void* d_xbs_hm = nullptr;   // d = 8 fp32: n x 4 x 8 per-thread scaled step biases
+  void* d_ws = nullptr;       // fp32 d in {16, 32}: 4 x d x d pre-scaled W (lstm_f32_tcd.cu)
 };
 
 namespace ackpt {
@@ -68,6 +70,12 @@ void hm_forward_many(const ackpt_lstm* c, int64_t from, int count, const float* 
                      cudaStream_t s);
 void hm_backward_many(const ackpt_lstm* c, int64_t from, int count, const float* const* states, const float* adj_in,
                       float* adj_out, cudaStream_t s);
+// Tensor-core kernels for d in {16, 32} (lstm_f32_tcd.cu); per-step = count 1.
+bool tcd_ok(const ackpt_lstm* c, std::initializer_list<const void*> ptrs);
+void tcd_forward(const ackpt_lstm* c, int64_t from, int count, const float* in, float* out, float* const* outs,
+                 cudaStream_t s);
+void tcd_reverse(const ackpt_lstm* c, int64_t from, int count, const float* const* states, const float* adj_in,
+                 float* adj_out, cudaStream_t s);
 // Occupancy variants (MINB resident 256-thread CTAs per SM).
 template <int D, int MINB>
 void f32_forward_v(const ackpt_lstm* c, int64_t step, const float* in, float* out, cudaStream_t s);

@@ -1,0 +1,75 @@
+// Launchers of the larger-d tensor-core kernels (lstm_f32_tcd.cuh).  The
+// per-step operators are the count = 1 case of the fused launches.
+#include "lstm_f32_tcd.cuh"
+
+#include <cstdlib>
+#include <string>
+
+namespace ackpt {
+
+namespace {
+
+unsigned tcd_grid(int64_t B) { return unsigned((B + tcd::kThreads - 1) / tcd::kThreads); }
+
+template <int D>
+void fwd_launch(const ackpt_lstm* c, int64_t from, int count, const float* in, float* out, float* const* outs,
+                cudaStream_t s) {
+  using L = tcd::Layout<D>;
+  static bool attr = [] {
+    cudaFuncSetAttribute(tcd::fwd_tcd<D, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(L::fwd_bytes));
+    cudaFuncSetAttribute(tcd::fwd_tcd<D, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(L::fwd_bytes));
+    return true;
+  }();
+  (void)attr;
+  tcd::OutPtrs o{};
+  const auto xb = static_cast<const float*>(c->d_xbs);
+  const auto ws = static_cast<const float*>(c->d_ws);
+  if (outs) {
+    for (int i = 0; i < count; ++i) o.p[i] = outs[i];
+    tcd::fwd_tcd<D, true><<<tcd_grid(c->B), tcd::kThreads, L::fwd_bytes, s>>>(in, nullptr, c->B, xb, ws, from, count, o);
+  } else {
+    tcd::fwd_tcd<D, false><<<tcd_grid(c->B), tcd::kThreads, L::fwd_bytes, s>>>(in, out, c->B, xb, ws, from, count, o);
+  }
+}
+
+template <int D>
+void rev_launch(const ackpt_lstm* c, int64_t from, int count, const float* const* states, const float* ai, float* ao,
+                cudaStream_t s) {
+  using L = tcd::Layout<D>;
+  static bool attr = [] {
+    cudaFuncSetAttribute(tcd::rev_tcd<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(L::rev_bytes));
+    return true;
+  }();
+  (void)attr;
+  tcd::StatePtrs sp{};
+  for (int i = 0; i < count; ++i) sp.p[i] = states[i];
+  tcd::rev_tcd<D><<<tcd_grid(c->B), tcd::kThreads, L::rev_bytes, s>>>(
+      ai, ao, c->B, static_cast<const float*>(c->d_xbs), static_cast<const float*>(c->d_ws), from, count, sp);
+}
+
+}  // namespace
+
+bool tcd_ok(const ackpt_lstm* c, std::initializer_list<const void*> ptrs) {
+  static const bool on = [] {
+    const char* e = std::getenv("ACKPT_TCD");
+    return !(e && std::string(e) == "0");
+  }();
+  if (!on || c->dtype != ACKPT_F32 || (c->d != 16 && c->d != 32) || !c->d_ws || !c->d_xbs) return false;
+  for (const void* p : ptrs)
+    if (reinterpret_cast<uintptr_t>(p) & 3u) return false;
+  return true;
+}
+
+void tcd_forward(const ackpt_lstm* c, int64_t from, int count, const float* in, float* out, float* const* outs,
+                 cudaStream_t s) {
+  if (c->d == 16) fwd_launch<16>(c, from, count, in, out, outs, s);
+  else fwd_launch<32>(c, from, count, in, out, outs, s);
+}
+
+void tcd_reverse(const ackpt_lstm* c, int64_t from, int count, const float* const* states, const float* adj_in,
+                 float* adj_out, cudaStream_t s) {
+  if (c->d == 16) rev_launch<16>(c, from, count, states, adj_in, adj_out, s);
+  else rev_launch<32>(c, from, count, states, adj_in, adj_out, s);
+}
+
+}  // namespace ackpt

@@ -1,0 +1,421 @@
+// Tensor-core (tcgen05) LSTM kernels for larger hidden sizes, D in {16, 32},
+// fp32 state: forward (one step, a fused Advance, or a TapeForward run) and
+// reverse (one step or a fused Reverse run).  Same results contract as the
+// other fp32 kernels (rel-L2 <= 1e-5 vs float64, lstm.py:114-152).
+//
+// CTA = 128 threads = one M=128 tile of sequences (thread r owns sequence
+// b0 + r, the TMEM lane r); arithmetic is packed over unit pairs (j, j+1).
+//   gates   G[128 x 4D] = h[128 x D] . W[4D x D]^T + 1 . xb^T, 3xTF32
+//           (h_hi W_hi + h_lo W_hi + h_hi W_lo, bias as two K=8 MMAs against
+//           a constant ones column), in TMEM.  Gate rows are permuted,
+//           n = 8 p + 2 gate + e for unit j = 2 p + e, so one tcgen05.ld.x8
+//           at column 8p returns (f, i, o, g) of units 2p, 2p+1 as float2s.
+//   reverse da (the scaled gate adjoints of bwd_unit) go back into TMEM as
+//           the A operand of dh[128 x D] = da[128 x 4D] . B2[D x 4D]^T with
+//           B2[m][n] = s_gate W_gate[j(n)][m], 3xTF32 as well: da_hi over G in
+//           place, da_lo in [4D, 8D), dh in [8D, 9D) (TMEM-A form validated in
+//           tools/umma_ts_probe.cu).  (A bf16 residual would save 2D columns
+//           but costs ~2^-19 per product: 1.2e-5 rel-L2 after 100 steps at d=32.)
+// Operands are K-major, no swizzle, 8-row groups of 16-byte core matrices
+// (LBO 128 B between K chunks, SBO = 32 K bytes between row groups).
+#pragma once
+
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include "lstm_f32_math.cuh"
+
+namespace ackpt {
+namespace tcd {
+
+using namespace f32m;
+
+constexpr int kThreads = 128;
+
+struct OutPtrs {
+  float* p[ACKPT_MAX_FUSED];
+};
+struct StatePtrs {
+  const float* p[ACKPT_MAX_FUSED];
+};
+
+__device__ __forceinline__ uint32_t su32(const void* p) { return uint32_t(__cvta_generic_to_shared(p)); }
+__device__ __forceinline__ uint64_t desc(uint32_t addr, uint32_t sbo) {
+  return uint64_t((addr >> 4) & 0x3FFF) | (uint64_t(128 >> 4) << 16) | (uint64_t((sbo >> 4) & 0x3FFF) << 32) |
+         (uint64_t(1) << 46);
+}
+// tf32 head of x rounded to nearest (|x - hi| <= 2^-11 |x|; the tensor core
+// truncates the residual to tf32, so each split product carries ~2^-22).
+__device__ __forceinline__ float hi_part(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return __uint_as_float(r);
+}
+
+// float index of (row, k) in a tf32 operand with K-extent K; bf16 index likewise
+template <int K>
+__device__ __forceinline__ int kofs(int r, int k) {
+  return (r >> 3) * (8 * K) + (k >> 2) * 32 + (r & 7) * 4 + (k & 3);
+}
+template <int K>
+__device__ __forceinline__ int kofs16(int r, int k) {
+  return (r >> 3) * (8 * K) + (k >> 3) * 64 + (r & 7) * 8 + (k & 7);
+}
+template <int N>
+__host__ __device__ constexpr uint32_t idesc(bool bf16) {
+  return (1u << 4) | ((bf16 ? 1u : 2u) << 7) | ((bf16 ? 1u : 2u) << 10) | (uint32_t(N >> 3) << 17) |
+         (uint32_t(128 >> 4) << 24);
+}
+__device__ __forceinline__ void mma_ss(uint32_t d, uint64_t a, uint64_t b, uint32_t id, uint32_t acc) {
+  asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+               "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
+               "l"(a), "l"(b), "r"(id), "r"(acc));
+}
+__device__ __forceinline__ void mma_ts(uint32_t d, uint32_t a, uint64_t b, uint32_t id, uint32_t acc, bool f16) {
+  if (f16)
+    asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                 "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d),
+                 "r"(a), "l"(b), "r"(id), "r"(acc));
+  else
+    asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                 "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d),
+                 "r"(a), "l"(b), "r"(id), "r"(acc));
+}
+__device__ __forceinline__ void commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void wait_bar(uint64_t* bar, uint32_t phase) {
+  uint32_t done = 0;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(su32(bar)), "r"(phase)
+        : "memory");
+  } while (!done);
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+// Barrier that publishes this step's shared-memory / TMEM writes to the
+// tensor core (issued by thread 0 afterwards).
+__device__ __forceinline__ void publish() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+}
+__device__ __forceinline__ void ld8(uint32_t addr, float (&v)[8]) {
+  uint32_t r[8];
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+               : "r"(addr));
+#pragma unroll
+  for (int i = 0; i < 8; ++i) v[i] = __uint_as_float(r[i]);
+}
+__device__ __forceinline__ void ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void st8(uint32_t addr, const uint32_t (&v)[8]) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(addr), "r"(v[0]),
+               "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7])
+               : "memory");
+}
+__device__ __forceinline__ void st4(uint32_t addr, const uint32_t (&v)[4]) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1,%2,%3,%4};" ::"r"(addr), "r"(v[0]), "r"(v[1]),
+               "r"(v[2]), "r"(v[3])
+               : "memory");
+}
+__device__ __forceinline__ uint32_t bf16x2(float even, float odd) {
+  uint32_t r;
+  asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(odd), "f"(even));
+  return r;
+}
+__host__ __device__ constexpr int tmem_cols(int c) { return c <= 32 ? 32 : c <= 64 ? 64 : c <= 128 ? 128 : c <= 256 ? 256 : 512; }
+
+// Shared-memory carve-up (dynamic).  Forward: A (h hi/lo), ones, W hi/lo,
+// bias hi/lo.  Reverse adds B2 hi/lo (tf32).
+template <int D>
+struct Layout {
+  static constexpr int kA = 128 * D, kOne = 128 * 8, kW = 4 * D * D, kBias = 4 * D * 8, kW2 = 4 * D * D;
+  static constexpr int a_hi = 0, a_lo = a_hi + kA, one = a_lo + kA, w_hi = one + kOne, w_lo = w_hi + kW,
+                       b_hi = w_lo + kW, b_lo = b_hi + kBias, fwd_end = b_lo + kBias;
+  static constexpr int w2_hi = fwd_end, w2_lo = w2_hi + kW2, rev_end = w2_lo + kW2;
+  static constexpr size_t fwd_bytes = size_t(fwd_end) * 4 + 64, rev_bytes = size_t(rev_end) * 4 + 64;
+};
+
+// TMEM base address written by tcgen05.alloc: visible to every thread only
+// after before_thread_sync / barrier / after_thread_sync.
+__device__ __forceinline__ uint32_t tmem_base(const uint32_t* slot) {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  return *reinterpret_cast<const volatile uint32_t*>(slot);
+}
+
+// gate row n -> (gate, unit)
+__device__ __forceinline__ void gate_of(int n, int& gi, int& j) {
+  gi = (n & 7) >> 1;
+  j = 2 * (n >> 3) + (n & 1);
+}
+
+// One-time setup shared by both kernels: TMEM, barriers, ones, W, zero bias rows.
+template <int D>
+__device__ __forceinline__ void setup(float* sm, uint64_t* bars, uint32_t* tmem_slot, const float* __restrict__ ws,
+                                      int cols, int nbars) {
+  using L = Layout<D>;
+  const int tid = threadIdx.x;
+  if (tid < 32) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(tmem_slot)),
+                 "r"(cols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (tid == 0) {
+    for (int i = 0; i < nbars; ++i) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(bars + i)));
+    asm volatile("fence.mbarrier_init.release.cluster;");
+  }
+  *reinterpret_cast<float4*>(sm + L::one + kofs<8>(tid, 0)) = make_float4(1.f, 0.f, 0.f, 0.f);
+  *reinterpret_cast<float4*>(sm + L::one + kofs<8>(tid, 4)) = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int idx = tid; idx < 4 * D * D; idx += kThreads) {
+    const int n = idx / D, k = idx % D;
+    int gi, j;
+    gate_of(n, gi, j);
+    const float x = __ldg(ws + (gi * D + j) * D + k);
+    sm[L::w_hi + kofs<D>(n, k)] = hi_part(x);
+    sm[L::w_lo + kofs<D>(n, k)] = x - hi_part(x);
+  }
+  for (int idx = tid; idx < 4 * D * 8; idx += kThreads) {
+    const int n = idx / 8, k = idx % 8;
+    sm[L::b_hi + kofs<8>(n, k)] = 0.f;
+    sm[L::b_lo + kofs<8>(n, k)] = 0.f;
+  }
+}
+
+// Stage A (this thread's row = its h, hi/lo) and the step's bias column.
+template <int D>
+__device__ __forceinline__ void stage(float* sm, const float2 (&h)[D / 2], const float* __restrict__ xbs_k) {
+  using L = Layout<D>;
+  const int tid = threadIdx.x;
+#pragma unroll
+  for (int c = 0; c < D / 4; ++c) {
+    const float4 x = make_float4(h[2 * c].x, h[2 * c].y, h[2 * c + 1].x, h[2 * c + 1].y);
+    const float4 hx = make_float4(hi_part(x.x), hi_part(x.y), hi_part(x.z), hi_part(x.w));
+    const float2 l01 = sub2(make_float2(x.x, x.y), make_float2(hx.x, hx.y));
+    const float2 l23 = sub2(make_float2(x.z, x.w), make_float2(hx.z, hx.w));
+    *reinterpret_cast<float4*>(sm + L::a_hi + kofs<D>(tid, 4 * c)) = hx;
+    *reinterpret_cast<float4*>(sm + L::a_lo + kofs<D>(tid, 4 * c)) = make_float4(l01.x, l01.y, l23.x, l23.y);
+  }
+  for (int n = tid; n < 4 * D; n += kThreads) {
+    int gi, j;
+    gate_of(n, gi, j);
+    const float x = __ldg(xbs_k + gi * D + j);  // table is gate-major
+    sm[L::b_hi + kofs<8>(n, 0)] = hi_part(x);
+    sm[L::b_lo + kofs<8>(n, 0)] = x - hi_part(x);
+  }
+}
+
+// Thread 0: the gate MMAs of a step into TMEM columns [0, 4D).
+template <int D>
+__device__ __forceinline__ void issue_gates(float* sm, uint32_t tmem, uint64_t* bar) {
+  using L = Layout<D>;
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  constexpr uint32_t id = idesc<4 * D>(false), sbo = 32 * D;
+#pragma unroll
+  for (int ks = 0; ks < D / 8; ++ks) {
+    const uint32_t off = uint32_t(ks) * 256u;
+    const uint64_t ah = desc(su32(sm + L::a_hi) + off, sbo), al = desc(su32(sm + L::a_lo) + off, sbo);
+    const uint64_t wh = desc(su32(sm + L::w_hi) + off, sbo), wl = desc(su32(sm + L::w_lo) + off, sbo);
+    mma_ss(tmem, al, wh, id, ks ? 1u : 0u);
+    mma_ss(tmem, ah, wl, id, 1u);
+    mma_ss(tmem, ah, wh, id, 1u);
+  }
+  const uint64_t one = desc(su32(sm + L::one), 256);
+  mma_ss(tmem, one, desc(su32(sm + L::b_lo), 256), id, 1u);
+  mma_ss(tmem, one, desc(su32(sm + L::b_hi), 256), id, 1u);
+  commit(bar);
+}
+
+__device__ __forceinline__ float ldg_nc(const float* p) {
+  float v;
+  asm volatile("ld.global.nc.L1::no_allocate.f32 %0, [%1];" : "=f"(v) : "l"(p));
+  return v;
+}
+
+// Unit pairs of this thread's sequence, block `base` (0: h, D: c) of a state.
+template <int D>
+__device__ __forceinline__ void load_rows(const float* __restrict__ x, int64_t B, int64_t b, int base,
+                                          float2 (&v)[D / 2]) {
+#pragma unroll
+  for (int p = 0; p < D / 2; ++p)
+    v[p] = make_float2(ldg_nc(x + int64_t(base + 2 * p) * B + b), ldg_nc(x + int64_t(base + 2 * p + 1) * B + b));
+}
+template <int D>
+__device__ __forceinline__ void store_rows(float* __restrict__ x, int64_t B, int64_t b, int base,
+                                           const float2 (&v)[D / 2]) {
+#pragma unroll
+  for (int p = 0; p < D / 2; ++p) {
+    x[int64_t(base + 2 * p) * B + b] = v[p].x;
+    x[int64_t(base + 2 * p + 1) * B + b] = v[p].y;
+  }
+}
+
+// Forward over `count` steps from `from` (count = 1: the per-step operator).
+// TAPE stores every step's output state to outs.p[i]; otherwise the final
+// state goes to `out`.
+template <int D, bool TAPE>
+__global__ void __launch_bounds__(kThreads)
+    fwd_tcd(const float* __restrict__ in, float* __restrict__ out, int64_t B, const float* __restrict__ xbs_all,
+            const float* __restrict__ ws, int64_t from, int count, const __grid_constant__ OutPtrs outs) {
+  using L = Layout<D>;
+  extern __shared__ __align__(128) float sm[];
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sm + L::fwd_end);
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 2);
+  const int64_t b = int64_t(blockIdx.x) * kThreads + threadIdx.x;
+  const bool live = b < B;
+  setup<D>(sm, bars, tslot, ws, tmem_cols(4 * D), 1);
+  const uint32_t tmem = tmem_base(tslot);
+  float2 h[D / 2], c[D / 2];
+  if (live) {
+    load_rows<D>(in, B, b, 0, h);
+    load_rows<D>(in, B, b, D, c);
+  } else {
+#pragma unroll
+    for (int p = 0; p < D / 2; ++p) h[p] = c[p] = make_float2(0.f, 0.f);
+  }
+  const uint32_t lane = uint32_t((threadIdx.x >> 5) * 32) << 16;
+  for (int i = 0; i < count; ++i) {
+    stage<D>(sm, h, xbs_all + (from + i) * 4 * D);
+    publish();
+    if (threadIdx.x == 0) issue_gates<D>(sm, tmem, bars);
+    wait_bar(bars, uint32_t(i & 1));
+#pragma unroll
+    for (int p0 = 0; p0 < D / 2; p0 += 4) {  // 4 unit pairs per TMEM round trip
+      float g[4][8];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) ld8(tmem + lane + uint32_t(8 * (p0 + q)), g[q]);
+      ld_wait();
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        h[p0 + q] = fwd_unit_nr(make_float2(g[q][0], g[q][1]), make_float2(g[q][2], g[q][3]),
+                                make_float2(g[q][4], g[q][5]), make_float2(g[q][6], g[q][7]), c[p0 + q]);
+    }
+    if (TAPE && live) {
+      store_rows<D>(outs.p[i], B, b, 0, h);
+      store_rows<D>(outs.p[i], B, b, D, c);
+    }
+  }
+  if (!TAPE && live) {
+    store_rows<D>(out, B, b, 0, h);
+    store_rows<D>(out, B, b, D, c);
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (threadIdx.x < 32)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(tmem_cols(4 * D)));
+}
+
+// Reverse over steps from+count-1 .. from (count = 1: the per-step adjoint).
+template <int D>
+__global__ void __launch_bounds__(kThreads)
+    rev_tcd(const float* __restrict__ adj_in, float* __restrict__ adj_out, int64_t B, const float* __restrict__ xbs_all,
+            const float* __restrict__ ws, int64_t from, int count, const __grid_constant__ StatePtrs states) {
+  using L = Layout<D>;
+  extern __shared__ __align__(128) float sm[];
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sm + L::rev_end);
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 2);
+  constexpr int kCols = tmem_cols(9 * D);
+  constexpr uint32_t kLo = 4 * D, kDh = 8 * D;
+  const int64_t b = int64_t(blockIdx.x) * kThreads + threadIdx.x;
+  const bool live = b < B;
+  setup<D>(sm, bars, tslot, ws, kCols, 2);
+  const uint32_t tmem = tmem_base(tslot);
+  // B2[m][n] = s_gate W_gate[j(n)][m], K = 4D (gate-row order), tf32 hi/lo
+  for (int idx = threadIdx.x; idx < 4 * D * D; idx += kThreads) {
+    const int m = idx / (4 * D), n = idx % (4 * D);
+    int gi, j;
+    gate_of(n, gi, j);
+    const float x = __ldg(ws + (gi * D + j) * D + m);
+    sm[L::w2_hi + kofs<4 * D>(m, n)] = hi_part(x);
+    sm[L::w2_lo + kofs<4 * D>(m, n)] = x - hi_part(x);
+  }
+  float2 dh[D / 2], dc[D / 2];
+  if (live) {
+    load_rows<D>(adj_in, B, b, 0, dh);
+    load_rows<D>(adj_in, B, b, D, dc);
+  } else {
+#pragma unroll
+    for (int p = 0; p < D / 2; ++p) dh[p] = dc[p] = make_float2(0.f, 0.f);
+  }
+  const uint32_t lane = uint32_t((threadIdx.x >> 5) * 32) << 16;
+  int phase = 0;
+  for (int i = count - 1; i >= 0; --i, ++phase) {
+    float2 h[D / 2], c[D / 2];
+    if (live) {
+      load_rows<D>(states.p[i], B, b, 0, h);
+      load_rows<D>(states.p[i], B, b, D, c);
+    } else {
+#pragma unroll
+      for (int p = 0; p < D / 2; ++p) h[p] = c[p] = make_float2(0.f, 0.f);
+    }
+    stage<D>(sm, h, xbs_all + (from + i) * 4 * D);
+    publish();
+    if (threadIdx.x == 0) issue_gates<D>(sm, tmem, bars);
+    wait_bar(bars, uint32_t(phase & 1));
+#pragma unroll
+    for (int p0 = 0; p0 < D / 2; p0 += 4) {
+      float g[4][8];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) ld8(tmem + lane + uint32_t(8 * (p0 + q)), g[q]);
+      ld_wait();
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int p = p0 + q;
+        float2 da[4];
+        bwd_unit(make_float2(g[q][0], g[q][1]), make_float2(g[q][2], g[q][3]), make_float2(g[q][4], g[q][5]),
+                 make_float2(g[q][6], g[q][7]), c[p], dh[p], dc[p], da[0], da[1], da[2], da[3], dc[p]);
+        uint32_t hv[8], lv[8];
+#pragma unroll
+        for (int gi = 0; gi < 4; ++gi) {
+          const float2 hi = make_float2(hi_part(da[gi].x), hi_part(da[gi].y));
+          const float2 lo = sub2(da[gi], hi);
+          hv[2 * gi] = __float_as_uint(hi.x);
+          hv[2 * gi + 1] = __float_as_uint(hi.y);
+          lv[2 * gi] = __float_as_uint(lo.x);
+          lv[2 * gi + 1] = __float_as_uint(lo.y);
+        }
+        st8(tmem + lane + uint32_t(8 * p), hv);
+        st8(tmem + lane + kLo + uint32_t(8 * p), lv);
+      }
+    }
+    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+    publish();
+    if (threadIdx.x == 0) {
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      constexpr uint32_t it = idesc<D>(false), sbo32 = 32 * 4 * D;
+#pragma unroll
+      for (int ks = 0; ks < D / 2; ++ks) {  // K = 8 per MMA over K = 4D, small terms first
+        const uint32_t off = uint32_t(ks) * 256u;
+        const uint64_t bh = desc(su32(sm + L::w2_hi) + off, sbo32), bl = desc(su32(sm + L::w2_lo) + off, sbo32);
+        mma_ts(tmem + kDh, tmem + kLo + uint32_t(8 * ks), bh, it, ks ? 1u : 0u, false);
+        mma_ts(tmem + kDh, tmem + uint32_t(8 * ks), bl, it, 1u, false);
+        mma_ts(tmem + kDh, tmem + uint32_t(8 * ks), bh, it, 1u, false);
+      }
+      commit(bars + 1);
+    }
+    wait_bar(bars + 1, uint32_t(phase & 1));
+#pragma unroll
+    for (int m0 = 0; m0 < D; m0 += 8) {
+      float v[8];
+      ld8(tmem + lane + kDh + uint32_t(m0), v);
+      ld_wait();
+#pragma unroll
+      for (int q = 0; q < 4; ++q) dh[m0 / 2 + q] = make_float2(v[2 * q], v[2 * q + 1]);
+    }
+  }
+  if (live) {
+    store_rows<D>(adj_out, B, b, 0, dh);
+    store_rows<D>(adj_out, B, b, D, dc);
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (threadIdx.x < 32) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kCols));
+}
+
+}  // namespace tcd
+}  // namespace ackpt

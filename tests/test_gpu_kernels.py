@@ -37,7 +37,8 @@ def _states(d, seed, batch, scale=1.0):
     "d,batch",
     # 4096/4100/516: TMA tiles (full, partial last tile, tiny); 2/1002: float2
     # kernels; odd B and other d: generic kernels
-    [(8, 4096), (8, 4100), (8, 516), (8, 2), (8, 1002), (4, 1024), (8, 1001), (5, 64), (16, 300), (32, 17)],
+    [(8, 4096), (8, 4100), (8, 516), (8, 2), (8, 1002), (4, 1024), (8, 1001), (5, 64), (16, 300), (32, 17),
+     (16, 4096), (32, 1000), (32, 256), (64, 40)],
 )
 def test_forward_backward_f32_vs_oracle(P, d, batch):
     cell, ocell = _cells(P, d, 6, 11 + d)
@@ -180,3 +181,35 @@ def test_c2_shape_kernels_on_sampled_rows(P):
     ys = y[:, :, idx].double().cpu().numpy()
     a_ref = L.seed(ocell, ys)
     assert L.rel_l2(g[:, :, idx].cpu().numpy(), L.backward_step(ocell, 2, xs, a_ref)) <= F32_TOL
+
+
+@pytest.mark.parametrize("d,batch", [(16, 4096), (16, 130), (32, 1000), (32, 128)])
+def test_large_d_tensor_core_fused(P, d, batch):
+    # d in {16, 32}: tcgen05 kernels (lstm_f32_tcd.cuh) for the per-step
+    # operators and the fused advance / tape / reverse launches
+    cell, ocell = _cells(P, d, 40, 30 + d)
+    x = torch.from_numpy(_states(d, 31, batch).astype(np.float32)).cuda()
+    a = torch.from_numpy(_states(d, 32, batch).astype(np.float32)).cuda()
+    dc = P.device_cell(cell, batch, "f32")
+    ref = x.double().cpu().numpy()
+    refs = []
+    for k in range(2, 34):
+        ref = L.forward_step(ocell, k, ref)
+        refs.append(ref)
+    adv = dc.advance(2, 34, x).cpu().numpy()
+    assert L.rel_l2(adv, refs[-1]) <= F32_TOL, L.rel_l2(adv, refs[-1])
+    outs = dc.forward_many(2, 32, x)
+    for i in (0, 7, 31):
+        assert L.rel_l2(outs[i].cpu().numpy(), refs[i]) <= F32_TOL
+    assert torch.equal(outs[-1], dc.advance(2, 34, x))  # same kernel, same bits
+    states = [x] + outs[:-1]
+    fused = dc.backward_many(2, states, a).cpu().numpy()
+    adj = a.double().cpu().numpy()
+    for i, k in reversed(list(enumerate(range(2, 34)))):
+        adj = L.backward_step(ocell, k, states[i].double().cpu().numpy(), adj)
+    assert L.rel_l2(fused, adj) <= F32_TOL, L.rel_l2(fused, adj)
+    # the per-step operator chain equals the fused launches bit for bit
+    chain = a
+    for i, k in reversed(list(enumerate(range(2, 34)))):
+        chain = dc.backward(k, states[i], chain)
+    assert torch.equal(chain.cpu(), torch.from_numpy(fused))

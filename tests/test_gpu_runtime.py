@@ -193,10 +193,14 @@ def test_disable_prefetch_hook(P, monkeypatch):
         finally:
             backend.close()
 
+    # stall is wall-clock based (host sleeps on the copy streams): compare the
+    # best of two runs per mode so one scheduling hiccup cannot flip the order
     monkeypatch.delenv("CKPT_DISABLE_PREFETCH", raising=False)
-    g_async, st_async = run()
+    runs_async = [run() for _ in range(2)]
     monkeypatch.setenv("CKPT_DISABLE_PREFETCH", "1")
-    g_sync, st_sync = run()
+    runs_sync = [run() for _ in range(2)]
+    g_async, st_async = min(runs_async, key=lambda r: r[1].stall_seconds)
+    g_sync, st_sync = min(runs_sync, key=lambda r: r[1].stall_seconds)
     assert g_sync == g_async
     assert st_sync.stall_seconds > st_async.stall_seconds
     assert st_sync.prefetches_issued == st_async.prefetches_issued == 4
@@ -416,3 +420,23 @@ def test_callback_engine_not_leaked(P):
     eng = weakref.ref(ops.__dict__["_ackpt_engine"][0])
     del ops
     assert eng() is None
+
+
+@pytest.mark.parametrize("d", [16, 32])
+def test_large_d_executions_match_oracle(P, d):
+    # tensor-core kernels for d in {16, 32}: every strategy, per-step and
+    # fused, equal to the float64 oracle executor; strategies bit-identical
+    pkg, lstm, _ = P
+    n, batch = 30, 512
+    cell = lstm.random_cell(d, n, 4)
+    ops = lstm.operator_pair(cell, batch, "f32")
+    s0 = lstm.random_states(d, 5, batch, "f32")
+    ref, ost = RO.execute("full", L.random_cell(d, n, 4), s0.double().cpu().numpy())
+    with pkg.PinnedHostBackend() as b:
+        for fuse in (False, True):
+            full, _ = pkg.execute(pkg.FullStorage(), ops, s0, fuse=fuse)
+            rev, st = pkg.execute(pkg.Revolve(5), ops, s0, fuse=fuse)
+            ms, stm = pkg.execute(pkg.Multistage(6, interval=6), ops, s0, b, fuse=fuse)
+            assert torch.equal(full, rev) and torch.equal(full, ms), fuse
+            assert L.rel_l2(full.double().cpu().numpy(), ref) <= 1e-5, (fuse, L.rel_l2(full.double().cpu().numpy(), ref))
+            assert st.forward_evals == pkg.forward_cost(n, 5) and stm.forward_evals == 2 * n
