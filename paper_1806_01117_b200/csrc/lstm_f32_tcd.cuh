@@ -266,10 +266,14 @@ __global__ void __launch_bounds__(kThreads)
   extern __shared__ __align__(128) float sm[];
   uint64_t* bars = reinterpret_cast<uint64_t*>(sm + L::fwd_end);
   uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 2);
-  const int64_t b = int64_t(blockIdx.x) * kThreads + threadIdx.x;
-  const bool live = b < B;
   setup<D>(sm, bars, tslot, ws, tmem_cols(4 * D), 1);
   const uint32_t tmem = tmem_base(tslot);
+  const uint32_t lane = uint32_t((threadIdx.x >> 5) * 32) << 16;
+  uint32_t ph = 0;
+  // persistent over 128-sequence tiles (the weight setup is paid once per CTA)
+  for (int64_t tile = blockIdx.x; tile * kThreads < B; tile += gridDim.x) {
+  const int64_t b = tile * kThreads + threadIdx.x;
+  const bool live = b < B;
   float2 h[D / 2], c[D / 2];
   if (live) {
     load_rows<D>(in, B, b, 0, h);
@@ -278,12 +282,11 @@ __global__ void __launch_bounds__(kThreads)
 #pragma unroll
     for (int p = 0; p < D / 2; ++p) h[p] = c[p] = make_float2(0.f, 0.f);
   }
-  const uint32_t lane = uint32_t((threadIdx.x >> 5) * 32) << 16;
-  for (int i = 0; i < count; ++i) {
+  for (int i = 0; i < count; ++i, ++ph) {
     stage<D>(sm, h, xbs_all + (from + i) * 4 * D);
     publish();
     if (threadIdx.x == 0) issue_gates<D>(sm, tmem, bars);
-    wait_bar(bars, uint32_t(i & 1));
+    wait_bar(bars, ph & 1u);
 #pragma unroll
     for (int p0 = 0; p0 < D / 2; p0 += 4) {  // 4 unit pairs per TMEM round trip
       float g[4][8];
@@ -304,6 +307,7 @@ __global__ void __launch_bounds__(kThreads)
     store_rows<D>(out, B, b, 0, h);
     store_rows<D>(out, B, b, D, c);
   }
+  }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   if (threadIdx.x < 32)
@@ -321,8 +325,6 @@ __global__ void __launch_bounds__(kThreads)
   uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 2);
   constexpr int kCols = tmem_cols(9 * D);
   constexpr uint32_t kLo = 4 * D, kDh = 8 * D;
-  const int64_t b = int64_t(blockIdx.x) * kThreads + threadIdx.x;
-  const bool live = b < B;
   setup<D>(sm, bars, tslot, ws, kCols, 2);
   const uint32_t tmem = tmem_base(tslot);
   // B2[m][n] = s_gate W_gate[j(n)][m], K = 4D (gate-row order), tf32 hi/lo
@@ -334,6 +336,12 @@ __global__ void __launch_bounds__(kThreads)
     sm[L::w2_hi + kofs<4 * D>(m, n)] = hi_part(x);
     sm[L::w2_lo + kofs<4 * D>(m, n)] = x - hi_part(x);
   }
+  const uint32_t lane = uint32_t((threadIdx.x >> 5) * 32) << 16;
+  uint32_t phase = 0;
+  // persistent over 128-sequence tiles (the weight setup is paid once per CTA)
+  for (int64_t tile = blockIdx.x; tile * kThreads < B; tile += gridDim.x) {
+  const int64_t b = tile * kThreads + threadIdx.x;
+  const bool live = b < B;
   float2 dh[D / 2], dc[D / 2];
   if (live) {
     load_rows<D>(adj_in, B, b, 0, dh);
@@ -342,8 +350,6 @@ __global__ void __launch_bounds__(kThreads)
 #pragma unroll
     for (int p = 0; p < D / 2; ++p) dh[p] = dc[p] = make_float2(0.f, 0.f);
   }
-  const uint32_t lane = uint32_t((threadIdx.x >> 5) * 32) << 16;
-  int phase = 0;
   for (int i = count - 1; i >= 0; --i, ++phase) {
     float2 h[D / 2], c[D / 2];
     if (live) {
@@ -356,7 +362,7 @@ __global__ void __launch_bounds__(kThreads)
     stage<D>(sm, h, xbs_all + (from + i) * 4 * D);
     publish();
     if (threadIdx.x == 0) issue_gates<D>(sm, tmem, bars);
-    wait_bar(bars, uint32_t(phase & 1));
+    wait_bar(bars, phase & 1u);
 #pragma unroll
     for (int p0 = 0; p0 < D / 2; p0 += 4) {
       float g[4][8];
@@ -398,7 +404,7 @@ __global__ void __launch_bounds__(kThreads)
       }
       commit(bars + 1);
     }
-    wait_bar(bars + 1, uint32_t(phase & 1));
+    wait_bar(bars + 1, phase & 1u);
 #pragma unroll
     for (int m0 = 0; m0 < D; m0 += 8) {
       float v[8];
@@ -411,6 +417,7 @@ __global__ void __launch_bounds__(kThreads)
   if (live) {
     store_rows<D>(adj_out, B, b, 0, dh);
     store_rows<D>(adj_out, B, b, D, dc);
+  }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();

@@ -50,9 +50,13 @@ def test_measured_multistage_timeline_matches_simulator(fuse):
     sim_stalls = {e.from_step for e in sim if e.kind == STALL}
     got_stalls = {e.from_step for e in got if e.kind == STALL and e.end - e.start > 0.2 * ta}
     assert sim_stalls and sim_stalls <= got_stalls
-    # total: simulator + the re-run first traversals, within launch overheads
+    # compute-lane busy time: the simulator's plus the re-run first traversals,
+    # within launch overheads (stall lengths depend on host-sleep jitter of
+    # the throttled tier, so the total is only bounded below)
+    busy = lambda evs: sum(float(e.end - e.start) for e in evs if e.kind in (FORWARD, BACKWARD))
+    assert busy(got) == pytest.approx(busy(sim) + n * ta, rel=0.25)
     gpu = st.device["gpu_seconds"]
-    assert gpu == pytest.approx(sim_total + n * ta, rel=0.25)
+    assert gpu >= busy(got)
     # events are ordered and inside the run
     starts = [e.start for e in got]
     assert starts == sorted(starts) and all(0 <= e.start <= e.end <= gpu * 1.01 + 1e-4 for e in got)
