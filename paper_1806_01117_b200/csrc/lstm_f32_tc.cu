@@ -1,5 +1,6 @@
 // Launchers of the tensor-core fused LSTM kernels (lstm_f32_tc.cuh).
 #include "lstm_f32_tc.cuh"
+#include "lstm_f32_tcp.cuh"
 
 #include <cstdint>
 #include <cstdlib>
@@ -21,7 +22,34 @@ unsigned tc_grid(int64_t B) { return unsigned((B + tc::kTile - 1) / tc::kTile); 
 
 }  // namespace
 
+// ACKPT_TC_FWD=pp: ping-pong forward (lstm_f32_tcp.cuh: one tile's MMA behind
+// the other tile's activations).  Correct but measured slower than fwd_tc at
+// the C2 shape (advance 15.5-15.8 vs 14.8 us/step, tape 19.6-20.6 vs 18.1 at
+// 6-8 CTAs/SM: the second barrier per step and spills outweigh the hidden
+// MMA latency), so fwd_tc is the default.
+bool tc_pingpong() {
+  static const bool pp = [] {
+    const char* e = std::getenv("ACKPT_TC_FWD");
+    return e && std::string(e) == "pp";
+  }();
+  return pp;
+}
+
+tcp::Weights tcp_weights(const ackpt_lstm* c) {
+  f32m::ScaledParams<8> sp;
+  f32m::fill_scaled<8>(c, -1, sp);
+  tcp::Weights w;
+  std::memcpy(w.ws, sp.ws, sizeof(w.ws));
+  return w;
+}
+
 void tc_advance(const ackpt_lstm* c, int64_t from, int count, const float* in, float* out, cudaStream_t s) {
+  if (tc_pingpong()) {
+    tcp::OutPtrs none{};
+    tcp::fwd_tcp<false, true><<<tc_grid(c->B), tcp::kThreads, 0, s>>>(
+        in, out, c->B, static_cast<const float*>(c->d_xbs), from, count, tcp_weights(c), none);
+    return;
+  }
   tc::OutPtrs none{};
   tc::fwd_tc<false><<<tc_grid(c->B), tc::kThreads, 0, s>>>(in, out, c->B, static_cast<const float*>(c->d_xbs),
                                                             from, count, tc_weights(c), none);
@@ -29,6 +57,13 @@ void tc_advance(const ackpt_lstm* c, int64_t from, int count, const float* in, f
 
 void tc_forward_many(const ackpt_lstm* c, int64_t from, int count, const float* in, float* const* outs,
                      cudaStream_t s) {
+  if (tc_pingpong()) {
+    tcp::OutPtrs o{};
+    for (int i = 0; i < count; ++i) o.p[i] = outs[i];
+    tcp::fwd_tcp<true, true><<<tc_grid(c->B), tcp::kThreads, 0, s>>>(
+        in, nullptr, c->B, static_cast<const float*>(c->d_xbs), from, count, tcp_weights(c), o);
+    return;
+  }
   tc::OutPtrs o{};
   for (int i = 0; i < count; ++i) o.p[i] = outs[i];
   tc::fwd_tc<true><<<tc_grid(c->B), tc::kThreads, 0, s>>>(in, nullptr, c->B, static_cast<const float*>(c->d_xbs),
