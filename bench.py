@@ -409,6 +409,7 @@ def main(argv=None) -> None:
     achieved = bytes_dom / t_dom / 1e9
     traffic = None
     tfile = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    pipes = None
     base = dominant.split()[0]
     kfam = "ffma2"  # which kernel family ran the dominant launch
     if args.fuse and (args.family == "tcgen05" or (args.family == "mixed" and "rev" not in base)):
@@ -419,6 +420,7 @@ def main(argv=None) -> None:
         with open(tfile) as fh:
             tj = json.load(fh)
         traffic = tj.get(f"{base}@{kfam}", tj.get(base))
+        pipes = tj.get("pipes", {}).get(f"{base}@{kfam}", tj.get("pipes", {}).get(base))
     link_gbs = S / t_t / 1e9
     if args.fuse:  # algorithmic HBM bytes of the fused pass
         hbm_bytes = int(args.n * S * (2 / 64 + 1 + 1) + last.backward_evals * S)
@@ -540,7 +542,11 @@ def main(argv=None) -> None:
                          "unit": "GB/s", "frac": achieved / hbm_peak, "traffic": traffic,
                          "algorithmic_bytes_per_launch": bytes_dom, "avg_launch_us": t_dom * 1e6,
                          "timing": "CUDA events around back-to-back launches of the same kernel",
-                         "peak_source": peak_src},
+                         "peak_source": peak_src,
+                         "binding_pipes": pipes,
+                         "note": ("the fused launches are compute bound (FMA / MUFU issue, see binding_pipes "
+                                  "from ncu); frac is their HBM fraction, not a pipe fraction")
+                         if args.fuse else "per-step kernels: HBM bound"},
             "other_mode": other,
             "fused_kernels_us_per_step": {k: fk[k] * 1e6 for k in ("adv", "tape", "rev")},
             "store_all_us_per_step": {k: v * 1e6 for k, v in t_store_all.items()},
