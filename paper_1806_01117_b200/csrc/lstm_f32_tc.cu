@@ -1,6 +1,7 @@
 // Launchers of the tensor-core fused LSTM kernels (lstm_f32_tc.cuh).
 #include "lstm_f32_tc.cuh"
 #include "lstm_f32_tcp.cuh"
+#include "lstm_f32_tcr.cuh"
 
 #include <cstdint>
 #include <cstdlib>
@@ -77,15 +78,28 @@ void tc_backward_many(const ackpt_lstm* c, int64_t from, int count, const float*
   bool pf = c->B % 4 == 0 && std::getenv("ACKPT_TC_NO_PF") == nullptr;
   for (int i = 0; i < count; ++i) pf = pf && !(reinterpret_cast<uintptr_t>(states[i]) & 15u);
   // ACKPT_TC_REV: default / "1" gates on the tensor cores (rev_tc, fastest
-  // measured); "2" both matvecs on the tensor cores (rev_tc2: correct, but
-  // its second MMA round trip per step costs more than the FMA work it
-  // removes at 4 CTAs/SM), "2nr" the same with Newton rcp.
+  // measured, 28.4 us/step); "2" both matvecs on the tensor cores (rev_tc2,
+  // 34.2: its second MMA round trip per step costs more than the FMA work it
+  // removes at 4 CTAs/SM), "2nr" the same with Newton rcp,
+  // "3" the same with the two tiles in ping-pong (rev_tcr, 34.9: a third
+  // barrier per step).  All pass the parity suite.
   static const int rev = [] {
     const char* e = std::getenv("ACKPT_TC_REV");
     if (!e) return 1;
     const std::string v(e);
-    return v == "2" ? 2 : v == "2nr" ? 3 : 1;
+    return v == "2" ? 2 : v == "2nr" ? 3 : v == "3" ? 4 : 1;
   }();
+  if (pf && rev == 4) {  // both products on tensor cores, tiles in ping-pong (lstm_f32_tcr.cuh)
+    tcr::StatePtrs rp{};
+    for (int i = 0; i < count; ++i) rp.p[i] = states[i];
+    tcr::Weights w;
+    f32m::ScaledParams<8> sp8;
+    f32m::fill_scaled<8>(c, -1, sp8);
+    std::memcpy(w.ws, sp8.ws, sizeof(w.ws));
+    tcr::rev_tcr<<<tc_grid(c->B), tcr::kThreads, 0, s>>>(adj_in, adj_out, c->B, static_cast<const float*>(c->d_xbs),
+                                                         from, count, w, rp);
+    return;
+  }
   if (pf && rev == 2)
     tc::rev_tc2<false><<<tc_grid(c->B), tc::kThreads, 0, s>>>(
         adj_in, adj_out, c->B, static_cast<const float*>(c->d_xbs), from, count, tc_weights(c), sp);
