@@ -219,5 +219,23 @@ __device__ __forceinline__ void bwd_unit(float2 af, float2 ai, float2 ao, float2
   dck = mul2(dco, f);                                                          // :151
 }
 
+// As bwd_unit, but the gate adjoints are the true ones (dL/da, not divided
+// by the exponent scales): the transposed matvec then uses the unscaled
+// weights and three constant multiplies per unit disappear.
+__device__ __forceinline__ void bwd_unit_u(float2 af, float2 ai, float2 ao, float2 ag, float2 c, float2 dhn,
+                                           float2 dcn, float2& daf, float2& dai, float2& dao, float2& dag,
+                                           float2& dck) {
+  float2 f, ig, o, g;
+  activate(af, ai, ao, ag, f, ig, o, g);
+  const float2 cn = fma2(f, c, mul2(ig, g));
+  const float2 t = tanh2(cn);
+  const float2 dco = fma2(mul2(dhn, o), fma2(neg(t), t, bc(1.0f)), dcn);  // lstm.py:143
+  daf = mul2(mul2(dco, c), fma2(neg(f), f, f));                           // :144
+  dai = mul2(mul2(dco, g), fma2(neg(ig), ig, ig));                        // :145
+  dao = mul2(mul2(dhn, t), fma2(neg(o), o, o));                           // :142, :146
+  dag = mul2(mul2(dco, ig), fma2(neg(g), g, bc(1.0f)));                   // :147
+  dck = mul2(dco, f);                                                     // :151
+}
+
 }  // namespace f32m
 }  // namespace ackpt

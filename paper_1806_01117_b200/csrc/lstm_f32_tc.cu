@@ -16,6 +16,9 @@ tc::Weights tc_weights(const ackpt_lstm* c) {
   f32m::fill_scaled<8>(c, -1, sp);
   tc::Weights w;
   std::memcpy(w.ws, sp.ws, sizeof(w.ws));
+  for (int g = 0; g < 4; ++g)
+    for (int j = 0; j < 8; ++j)
+      for (int k = 0; k < 8; ++k) w.wu[g][j][k] = float(c->wh64[(size_t(g) * 8 + j) * 8 + k]);
   return w;
 }
 

@@ -77,8 +77,9 @@ __device__ __forceinline__ void ld8(uint32_t addr, float (&v)[8]) {
   for (int i = 0; i < 8; ++i) v[i] = __uint_as_float(r[i]);
 }
 
-struct Weights {  // pre-scaled (lstm_f32_math.cuh ScaledParams layout)
-  float ws[4][kD][kD];
+struct Weights {
+  float ws[4][kD][kD];  // pre-scaled (lstm_f32_math.cuh ScaledParams layout): gate products
+  float wu[4][kD][kD];  // unscaled W_h: rev_tc's transposed matvec of true adjoints
 };
 
 // One-time CTA setup: TMEM, mbarrier, constant operand parts.
@@ -367,13 +368,13 @@ __global__ void __launch_bounds__(kThreads, 5)  // 96 registers, 5 CTAs/SM: 28.3
       for (int q = 0; q < 2; ++q) {
         const int j = u + q;
         float2 daf, dai, dao, dag;
-        bwd_unit(pre[q][0], pre[q][1], pre[q][2], pre[q][3], c[j], dh[j], dc[j], daf, dai, dao, dag, dc[j]);
+        bwd_unit_u(pre[q][0], pre[q][1], pre[q][2], pre[q][3], c[j], dh[j], dc[j], daf, dai, dao, dag, dc[j]);
 #pragma unroll
         for (int m = 0; m < kD; ++m) {
-          acc[m] = fma2(bc(w.ws[0][j][m]), daf, acc[m]);
-          acc[m] = fma2(bc(w.ws[1][j][m]), dai, acc[m]);
-          acc[m] = fma2(bc(w.ws[2][j][m]), dao, acc[m]);
-          acc[m] = fma2(bc(w.ws[3][j][m]), dag, acc[m]);
+          acc[m] = fma2(bc(w.wu[0][j][m]), daf, acc[m]);
+          acc[m] = fma2(bc(w.wu[1][j][m]), dai, acc[m]);
+          acc[m] = fma2(bc(w.wu[2][j][m]), dao, acc[m]);
+          acc[m] = fma2(bc(w.wu[3][j][m]), dag, acc[m]);
         }
       }
     }
