@@ -1,0 +1,40 @@
+"""Every opt-in kernel variant (selected by environment variables that are
+read once per process) stays within the fp32 parity tolerance: each runs
+tests/variant_check.py in its own subprocess."""
+import json
+import os
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+
+VARIANTS = [
+    ({"ACKPT_TC": "0"}, 8, 4096),                       # FFMA2 fused family
+    ({"ACKPT_TC": "2"}, 8, 4096),                       # mixed
+    ({"ACKPT_TC": "3"}, 8, 4096),                       # mma.sync register fragments
+    ({"ACKPT_TC": "3", "ACKPT_HM_NR": "1"}, 8, 4096),
+    ({"ACKPT_TC": "3", "ACKPT_HM_NR": "0"}, 8, 4096),
+    ({"ACKPT_TC_REV": "2"}, 8, 4096),                   # both matvecs on tcgen05
+    ({"ACKPT_TC_REV": "2nr"}, 8, 4096),
+    ({"ACKPT_TC_REV": "3"}, 8, 4096),                   # ping-pong TMEM-A reverse
+    ({"ACKPT_TC_FWD": "pp"}, 8, 4096),                  # ping-pong forward
+    ({"ACKPT_TC_NO_PF": "1"}, 8, 4096),                 # reverse without the bulk prefetch
+    ({"ACKPT_KERNEL_VARIANT": "tma"}, 8, 4096),         # TMA per-step kernels
+    ({"ACKPT_KERNEL_VARIANT": "ldg3"}, 8, 4096),
+    ({"ACKPT_TCD": "0"}, 16, 1024),                     # generic kernels for d = 16
+    ({}, 32, 1000),                                     # tensor-core d = 32, ragged tile
+]
+
+
+@pytest.mark.parametrize("env,d,batch", VARIANTS, ids=lambda v: json.dumps(v) if isinstance(v, dict) else str(v))
+def test_variant_parity(env, d, batch):
+    full_env = dict(os.environ, **env)
+    out = subprocess.run([sys.executable, os.path.join(HERE, "variant_check.py"), str(d), str(batch)],
+                         env=full_env, capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0, out.stderr[-2000:]
+    errs = json.loads(out.stdout.strip().splitlines()[-1])
+    assert max(errs.values()) <= 1e-5, errs
