@@ -2,6 +2,7 @@
 #include "lstm_f32_tc.cuh"
 #include "lstm_f32_tcp.cuh"
 #include "lstm_f32_tcr.cuh"
+#include "lstm_f32_tcq.cuh"
 
 #include <cstdint>
 #include <cstdlib>
@@ -47,7 +48,22 @@ tcp::Weights tcp_weights(const ackpt_lstm* c) {
   return w;
 }
 
+// ACKPT_TC_P=2: two float2 pairs per thread in the forward (lstm_f32_tcq.cuh).
+int tc_pairs() {
+  static const int p = [] {
+    const char* e = std::getenv("ACKPT_TC_P");
+    return (e && std::string(e) == "2") ? 2 : 1;
+  }();
+  return p;
+}
+
 void tc_advance(const ackpt_lstm* c, int64_t from, int count, const float* in, float* out, cudaStream_t s) {
+  if (tc_pairs() == 2) {
+    tc::OutPtrs none{};
+    tcq::fwd_tcq<2><<<unsigned((c->B + 511) / 512), tcq::kThreads, 0, s>>>(
+        in, out, c->B, static_cast<const float*>(c->d_xbs), from, count, false, tc_weights(c), none);
+    return;
+  }
   if (tc_pingpong()) {
     tcp::OutPtrs none{};
     tcp::fwd_tcp<false, true><<<tc_grid(c->B), tcp::kThreads, 0, s>>>(
@@ -61,6 +77,13 @@ void tc_advance(const ackpt_lstm* c, int64_t from, int count, const float* in, f
 
 void tc_forward_many(const ackpt_lstm* c, int64_t from, int count, const float* in, float* const* outs,
                      cudaStream_t s) {
+  if (tc_pairs() == 2) {
+    tc::OutPtrs o{};
+    for (int i = 0; i < count; ++i) o.p[i] = outs[i];
+    tcq::fwd_tcq<2><<<unsigned((c->B + 511) / 512), tcq::kThreads, 0, s>>>(
+        in, nullptr, c->B, static_cast<const float*>(c->d_xbs), from, count, true, tc_weights(c), o);
+    return;
+  }
   if (tc_pingpong()) {
     tcp::OutPtrs o{};
     for (int i = 0; i < count; ++i) o.p[i] = outs[i];

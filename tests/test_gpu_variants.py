@@ -22,6 +22,7 @@ VARIANTS = [
     ({"ACKPT_TC_REV": "2nr"}, 8, 4096),
     ({"ACKPT_TC_REV": "3"}, 8, 4096),                   # ping-pong TMEM-A reverse
     ({"ACKPT_TC_FWD": "pp"}, 8, 4096),                  # ping-pong forward
+    ({"ACKPT_TC_P": "2"}, 8, 1002),                     # two pairs per thread, ragged tail
     ({"ACKPT_TC_NO_PF": "1"}, 8, 4096),                 # reverse without the bulk prefetch
     ({"ACKPT_KERNEL_VARIANT": "tma"}, 8, 4096),         # TMA per-step kernels
     ({"ACKPT_KERNEL_VARIANT": "ldg3"}, 8, 4096),
