@@ -108,13 +108,20 @@ void tc_backward_many(const ackpt_lstm* c, int64_t from, int count, const float*
   // 34.2: its second MMA round trip per step costs more than the FMA work it
   // removes at 4 CTAs/SM), "2nr" the same with Newton rcp,
   // "3" the same with the two tiles in ping-pong (rev_tcr, 34.9: a third
-  // barrier per step).  All pass the parity suite.
+  // barrier per step), "sp" rev_tc software-pipelined across steps (rev_tcs,
+  // 29.7: its double-buffered accumulator allows 4 CTAs/SM instead of 5).
+  // All pass the parity suite (tests/test_gpu_variants.py).
   static const int rev = [] {
     const char* e = std::getenv("ACKPT_TC_REV");
     if (!e) return 1;
     const std::string v(e);
-    return v == "2" ? 2 : v == "2nr" ? 3 : v == "3" ? 4 : 1;
+    return v == "2" ? 2 : v == "2nr" ? 3 : v == "3" ? 4 : v == "sp" ? 5 : 1;
   }();
+  if (pf && rev == 5) {
+    tc::rev_tcs<<<tc_grid(c->B), tc::kThreads, 0, s>>>(adj_in, adj_out, c->B, static_cast<const float*>(c->d_xbs),
+                                                       from, count, tc_weights(c), sp);
+    return;
+  }
   if (pf && rev == 4) {  // both products on tensor cores, tiles in ping-pong (lstm_f32_tcr.cuh)
     tcr::StatePtrs rp{};
     for (int i = 0; i < count; ++i) rp.p[i] = states[i];

@@ -391,6 +391,144 @@ __global__ void __launch_bounds__(kThreads, 5)  // 96 registers, 5 CTAs/SM: 28.3
   teardown(sm);
 }
 
+// ---- software-pipelined reverse (ACKPT_TC_REV=sp) ----------------------------
+// The gates of step i-1 depend only on the taped state, not on the adjoint,
+// so their MMAs are issued before the epilogue of step i and run underneath
+// it: the accumulator is double-buffered in TMEM (columns [0, 64) and
+// [64, 128)), one barrier per step, the MMA round trip off the critical path.
+__device__ __forceinline__ void read_units_at(const Smem& sm, uint32_t col0, int u, float2 (&pre)[2][4]) {
+  const uint32_t lane = uint32_t((threadIdx.x >> 5) * 32) << 16;
+  float a[8], b[8];
+  ld8(sm.tmem + lane + col0 + uint32_t(4 * u), a);
+  ld8(sm.tmem + lane + col0 + uint32_t(kN + 4 * u), b);
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int q = 0; q < 2; ++q)
+#pragma unroll
+    for (int g = 0; g < 4; ++g) pre[q][g] = make_float2(a[4 * q + g], b[4 * q + g]);
+}
+
+// Barrier (A and bias staged by every thread), then thread 0 issues the gate
+// MMAs into columns col0 and commits them to sm.mbar.
+__device__ __forceinline__ void gates_issue_at(Smem& sm, uint32_t col0) {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint64_t wh = desc(su32(sm.bw[0])), wl = desc(su32(sm.bw[1]));
+    const uint64_t xh = desc(su32(sm.bb[0])), xl = desc(su32(sm.bb[1])), one = desc(su32(sm.a1));
+#pragma unroll
+    for (int t = 0; t < 2; ++t) {
+      const uint32_t d = sm.tmem + col0 + uint32_t(t * kN);
+      const uint64_t ah = desc(su32(sm.a[t][0])), al = desc(su32(sm.a[t][1]));
+      mma(d, ah, wh, 0u);
+      mma(d, al, wh, 1u);
+      mma(d, ah, wl, 1u);
+      mma(d, one, xh, 1u);
+      mma(d, one, xl, 1u);
+    }
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(&sm.mbar))
+                 : "memory");
+  }
+}
+
+__global__ void __launch_bounds__(kThreads, 4)
+    rev_tcs(const float* __restrict__ adj_in, float* __restrict__ adj_out, int64_t B, const float* __restrict__ xbs_all,
+            int64_t from, int count, const __grid_constant__ Weights w, const __grid_constant__ StatePtrs states) {
+  __shared__ __align__(128) RevSmem rs;
+  Smem& sm = rs.g;
+  const int64_t b0 = int64_t(blockIdx.x) * kTile + 2 * threadIdx.x;
+  const bool live = b0 < B;
+  const int64_t rem = B - int64_t(blockIdx.x) * kTile;
+  const uint32_t seg = uint32_t(rem < kTile ? rem : kTile) * 4u;
+  setup(sm, w, 128);
+  if (threadIdx.x == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(&rs.mbar_st)));
+    asm volatile("fence.mbarrier_init.release.cluster;");
+    stage_state(rs, states.p[count - 1], B, seg);
+  }
+  __syncthreads();
+  float2 dh[kD], dc[kD], c[kD];
+#pragma unroll
+  for (int j = 0; j < kD; ++j) {
+    dh[j] = live ? ldg2(adj_in + b0 + int64_t(j) * B) : make_float2(0.f, 0.f);
+    dc[j] = live ? ldg2(adj_in + b0 + int64_t(kD + j) * B) : make_float2(0.f, 0.f);
+  }
+  // prologue: gates of the last step
+  uint32_t st_phase = 0;
+  {
+    mbar_wait(&rs.mbar_st, st_phase);
+    st_phase ^= 1u;
+    float2 h[kD];
+#pragma unroll
+    for (int j = 0; j < kD; ++j) {
+      h[j] = *reinterpret_cast<const float2*>(&rs.st[j][2 * threadIdx.x]);
+      c[j] = *reinterpret_cast<const float2*>(&rs.st[kD + j][2 * threadIdx.x]);
+    }
+    stage_operands(sm, h, load_bias(xbs_all, from + count - 1));
+    gates_issue_at(sm, 0);  // every thread has read rs.st
+    if (count > 1 && threadIdx.x == 0) stage_state(rs, states.p[count - 2], B, seg);
+  }
+  uint32_t g_phase = 0;
+  float xb = count > 1 ? load_bias(xbs_all, from + count - 2) : 0.f;
+  for (int i = count - 1; i >= 0; --i) {
+    const uint32_t cur = uint32_t((count - 1 - i) & 1) * 64u;
+    mbar_wait(&sm.mbar, g_phase);  // gates of step i are in TMEM
+    g_phase ^= 1u;
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    float2 cn[kD];
+    if (i > 0) {  // stage step i-1 and start its gate MMAs under this step's epilogue
+      mbar_wait(&rs.mbar_st, st_phase);
+      st_phase ^= 1u;
+      float2 h[kD];
+#pragma unroll
+      for (int j = 0; j < kD; ++j) {
+        h[j] = *reinterpret_cast<const float2*>(&rs.st[j][2 * threadIdx.x]);
+        cn[j] = *reinterpret_cast<const float2*>(&rs.st[kD + j][2 * threadIdx.x]);
+      }
+      stage_operands(sm, h, xb);
+      if (i > 1) xb = load_bias(xbs_all, from + i - 2);
+      gates_issue_at(sm, 64u - cur);
+      if (i > 1 && threadIdx.x == 0) stage_state(rs, states.p[i - 2], B, seg);
+    }
+    float2 acc[kD];
+#pragma unroll
+    for (int m = 0; m < kD; ++m) acc[m] = bc(0.0f);
+#pragma unroll
+    for (int u = 0; u < kD; u += 2) {
+      float2 pre[2][4];
+      read_units_at(sm, cur, u, pre);
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        const int j = u + q;
+        float2 daf, dai, dao, dag;
+        bwd_unit_u(pre[q][0], pre[q][1], pre[q][2], pre[q][3], c[j], dh[j], dc[j], daf, dai, dao, dag, dc[j]);
+#pragma unroll
+        for (int m = 0; m < kD; ++m) {
+          acc[m] = fma2(bc(w.wu[0][j][m]), daf, acc[m]);
+          acc[m] = fma2(bc(w.wu[1][j][m]), dai, acc[m]);
+          acc[m] = fma2(bc(w.wu[2][j][m]), dao, acc[m]);
+          acc[m] = fma2(bc(w.wu[3][j][m]), dag, acc[m]);
+        }
+      }
+    }
+#pragma unroll
+    for (int m = 0; m < kD; ++m) {
+      dh[m] = acc[m];
+      c[m] = cn[m];
+    }
+  }
+  if (live) {
+#pragma unroll
+    for (int j = 0; j < kD; ++j) {
+      stg2(adj_out + b0 + int64_t(j) * B, dh[j]);
+      stg2(adj_out + b0 + int64_t(kD + j) * B, dc[j]);
+    }
+  }
+  teardown(sm, 128);
+}
+
 // ---- reverse run with both matvecs on the tensor cores ---------------------
 // Step i: gates G = [h 1] . [W xb]^T as in rev_tc (MMA1, 3xTF32, TMEM cols
 // [0, 64)); each thread turns its rows' pre-activations into the scaled gate

@@ -21,6 +21,7 @@ VARIANTS = [
     ({"ACKPT_TC_REV": "2"}, 8, 4096),                   # both matvecs on tcgen05
     ({"ACKPT_TC_REV": "2nr"}, 8, 4096),
     ({"ACKPT_TC_REV": "3"}, 8, 4096),                   # ping-pong TMEM-A reverse
+    ({"ACKPT_TC_REV": "sp"}, 8, 1000),                  # software-pipelined reverse, ragged tail
     ({"ACKPT_TC_FWD": "pp"}, 8, 4096),                  # ping-pong forward
     ({"ACKPT_TC_P": "2"}, 8, 1002),                     # two pairs per thread, ragged tail
     ({"ACKPT_TC_NO_PF": "1"}, 8, 4096),                 # reverse without the bulk prefetch
