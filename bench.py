@@ -56,6 +56,7 @@ def parse_args(argv=None):
     p.add_argument("--no-cpu", action="store_true")
     p.add_argument("--full-n", type=int, default=1000, help="n of the measured FullStorage run")
     p.add_argument("--no-other-mode", action="store_true")
+    p.add_argument("--no-c1", action="store_true", help="skip the BASELINE config-1 block (reference workload)")
     p.add_argument("--family", choices=["ffma2", "tcgen05", "mixed", "mma"], default="tcgen05",
                    help="kernel family of the fused d=8 launches (lstm.set_kernel_family)")
     return p.parse_args(argv)
@@ -275,6 +276,41 @@ def fused_kernel_times(dc, state0, steps=64, reps=5):
     return out
 
 
+# reference CPU numbers for config 1 (unmodified
+# reference, min of 5 runs, this build container's Xeon): d=32 row
+C1_REFERENCE_MS = {"full": 116.2, "revolve": 244.2, "multistage": 282.4}
+
+
+def run_c1(pkg, lstm) -> dict:
+    """BASELINE config 1 exactly as the reference runs it (`asyncckpt bench
+    --strategy X --n 1000 --d 32 --s 10 --backend file --runs 5`): B=1
+    float64 byte-image states, CKPT file tier, min of 5 runs, through the
+    same lstm.bench API (per-step contract).  A GPU launch per step: this
+    workload is launch-latency bound, not bandwidth bound."""
+    import shutil
+    import tempfile
+
+    out = {"workload": "n=1000, d=32, s=10, B=1 float64, file tier, min of 5 (asyncckpt bench)",
+           "reference_cpu_ms": C1_REFERENCE_MS, "reference_cpu_source": "BASELINE.md section 2 (build container)"}
+    scratch = tempfile.mkdtemp(prefix="ackpt_c1_")
+    try:
+        for name, strat in (("full", pkg.FullStorage()), ("revolve", pkg.Revolve(10)),
+                            ("multistage", pkg.Multistage(10))):
+            rep = lstm.bench(strat, n=1000, d=32, s=10, backend_config={"kind": "file", "dir": scratch}, seed=0,
+                             runs=5)
+            fused = lstm.bench(strat, n=1000, d=32, s=10, backend_config={"kind": "file", "dir": scratch}, seed=0,
+                               runs=5, fuse=True)
+            assert fused.gradient_checksum == rep.gradient_checksum  # same kernels, same bits
+            out[name] = {"wall_ms": rep.wall_seconds * 1e3, "forward_evals": rep.forward_evals,
+                         "recompute_factor": rep.recompute_factor_measured, "stall_ms": rep.stall_seconds * 1e3,
+                         "speedup_vs_reference_cpu": C1_REFERENCE_MS[name] / (rep.wall_seconds * 1e3),
+                         "fused_wall_ms": fused.wall_seconds * 1e3,
+                         "fused_speedup_vs_reference_cpu": C1_REFERENCE_MS[name] / (fused.wall_seconds * 1e3)}
+    finally:
+        shutil.rmtree(scratch, ignore_errors=True)
+    return out
+
+
 def workload_config(args, interval, slots) -> dict:
     return {
         "workload": "BASELINE config 2: 1 GPU, 64 MiB fp32 state, n=10^4, memory ratio 0.1, "
@@ -456,6 +492,11 @@ def main(argv=None) -> None:
                  "adjoint_rel_l2_vs_headline": float((o_adj.double() - adj.double()).norm()
                                                      / max(adj.double().norm().item(), 1e-300))}
 
+    # --- BASELINE config 1: the reference's own workload, same API, on the GPU ---
+    c1 = None
+    if not args.no_c1 and rank == 0 and world == 1:
+        c1 = run_c1(pkg, lstm)
+
     # --- Revolve(s) at the same memory ratio, for comparison ---
     revolve = None
     if not args.no_revolve:
@@ -548,6 +589,7 @@ def main(argv=None) -> None:
                                   "from ncu); frac is their HBM fraction, not a pipe fraction")
                          if args.fuse else "per-step kernels: HBM bound"},
             "other_mode": other,
+            "c1_reference_workload": c1,
             "fused_kernels_us_per_step": {k: fk[k] * 1e6 for k in ("adv", "tape", "rev")},
             "store_all_us_per_step": {k: v * 1e6 for k, v in t_store_all.items()},
             "overhead_vs_per_step_store_all": (ms_per_step * 1e-3) / t_inf_per_step,

@@ -228,6 +228,9 @@ ACKPT_API int ackpt_lstm_forward(const ackpt_lstm* cell, int64_t step, const voi
       } else {
         ackpt::f32_forward<4>(cell, step, i, o, s);
       }
+    } else if (ackpt::sb_ok(cell)) {
+      if (cell->dtype == ACKPT_F32) ackpt::sb_forward<float>(cell, step, 1, state_in, state_out, nullptr, s);
+      else ackpt::sb_forward<double>(cell, step, 1, state_in, state_out, nullptr, s);
     } else if (cell->dtype == ACKPT_F32) {
       ackpt::generic_forward<float>(cell, step, static_cast<const float*>(state_in),
                                     static_cast<float*>(state_out), s);
@@ -255,6 +258,10 @@ ACKPT_API int ackpt_lstm_advance(const ackpt_lstm* cell, int64_t from_step, int6
     } else if (ackpt::tcd_ok(cell, {state_in, state_out})) {
       ackpt::tcd_forward(cell, from_step, int(to_step - from_step), static_cast<const float*>(state_in),
                          static_cast<float*>(state_out), nullptr, s);
+    } else if (ackpt::sb_ok(cell)) {
+      const int cnt = int(to_step - from_step);
+      if (cell->dtype == ACKPT_F32) ackpt::sb_forward<float>(cell, from_step, cnt, state_in, state_out, nullptr, s);
+      else ackpt::sb_forward<double>(cell, from_step, cnt, state_in, state_out, nullptr, s);
     } else if (cell->dtype == ACKPT_F32) {
       ackpt::generic_advance<float>(cell, from_step, to_step, static_cast<const float*>(state_in),
                                     static_cast<float*>(state_out), s);
@@ -295,6 +302,9 @@ ACKPT_API int ackpt_lstm_backward(const ackpt_lstm* cell, int64_t step, const vo
       } else {
         ackpt::f32_backward<4>(cell, step, x, a, o, s);
       }
+    } else if (ackpt::sb_ok(cell)) {
+      if (cell->dtype == ACKPT_F32) ackpt::sb_reverse<float>(cell, step, 1, &state, adjoint_in, adjoint_out, s);
+      else ackpt::sb_reverse<double>(cell, step, 1, &state, adjoint_in, adjoint_out, s);
     } else if (cell->dtype == ACKPT_F32) {
       ackpt::generic_backward<float>(cell, step, static_cast<const float*>(state),
                                      static_cast<const float*>(adjoint_in),
@@ -336,6 +346,12 @@ ACKPT_API int ackpt_lstm_forward_many(const ackpt_lstm* cell, int64_t from_step,
       ackpt::check_launch();
       return;
     }
+    if (ackpt::sb_ok(cell)) {
+      if (cell->dtype == ACKPT_F32) ackpt::sb_forward<float>(cell, from_step, int(count), state_in, nullptr, states_out, s);
+      else ackpt::sb_forward<double>(cell, from_step, int(count), state_in, nullptr, states_out, s);
+      ackpt::check_launch();
+      return;
+    }
     const void* cur = state_in;  // per-step launches
     for (int64_t i = 0; i < count; ++i) {
       int rc = ackpt_lstm_forward(cell, from_step + i, cur, states_out[i], stream);
@@ -362,7 +378,14 @@ ACKPT_API int ackpt_lstm_backward_many(const ackpt_lstm* cell, int64_t from_step
     }
     bool fast = ackpt::f32_fast(cell, {adjoint_in, adjoint_out});
     for (int64_t i = 0; i < count; ++i) fast = fast && !(reinterpret_cast<uintptr_t>(states[i]) & 7u);
-    if (!fast) ackpt::fail(ACKPT_VALUE_ERROR, "fused backward needs the fp32 fast path (d in {4, 8, 16, 32})");
+    if (!fast && ackpt::sb_ok(cell)) {
+      if (cell->dtype == ACKPT_F32) ackpt::sb_reverse<float>(cell, from_step, int(count), states, adjoint_in, adjoint_out, s);
+      else ackpt::sb_reverse<double>(cell, from_step, int(count), states, adjoint_in, adjoint_out, s);
+      ackpt::check_launch();
+      return;
+    }
+    if (!fast)
+      ackpt::fail(ACKPT_VALUE_ERROR, "fused backward needs a fused kernel (fp32 d in {4, 8, 16, 32} or B <= 1024)");
     auto sp = reinterpret_cast<const float* const*>(states);
     auto ai = static_cast<const float*>(adjoint_in);
     auto ao = static_cast<float*>(adjoint_out);
@@ -422,7 +445,7 @@ ACKPT_API int ackpt_lstm_operator(ackpt_lstm* cell, ackpt_operator* out) {
     out->state_bytes = ackpt_lstm_state_bytes(cell);
     out->n_steps = cell->n;
     const bool fused = (cell->dtype == ACKPT_F32 && (cell->d == 4 || cell->d == 8) && !(cell->B & 1)) ||
-                       ackpt::tcd_ok(cell, {});
+                       ackpt::tcd_ok(cell, {}) || ackpt::sb_ok(cell);
     out->forward_many = fused ? ackpt::lstm_op_forward_many : nullptr;
     out->backward_many = fused ? ackpt::lstm_op_backward_many : nullptr;
   });

@@ -40,6 +40,7 @@ struct TargetParams {
 };
 
 constexpr int kMaxD = 128;
+constexpr int64_t kSmallBatch = 1024;  // CTA-per-sequence kernels at or below this batch (lstm_small.cu)
 
 // fp32 fast path, d in {4, 8}: float2-paired kernels (lstm_f32_d*.cu).
 template <int D>
@@ -70,6 +71,15 @@ void hm_forward_many(const ackpt_lstm* c, int64_t from, int count, const float* 
                      cudaStream_t s);
 void hm_backward_many(const ackpt_lstm* c, int64_t from, int count, const float* const* states, const float* adj_in,
                       float* adj_out, cudaStream_t s);
+// Small-batch kernels (B <= kSmallBatch, any d, f32 / f64): one CTA per
+// sequence, one thread per gate row (lstm_small.cu); per-step = count 1.
+bool sb_ok(const ackpt_lstm* c);
+template <typename T>
+void sb_forward(const ackpt_lstm* c, int64_t from, int count, const void* in, void* out, void* const* outs,
+                cudaStream_t s);
+template <typename T>
+void sb_reverse(const ackpt_lstm* c, int64_t from, int count, const void* const* states, const void* adj_in,
+                void* adj_out, cudaStream_t s);
 // Tensor-core kernels for d in {16, 32} (lstm_f32_tcd.cu); per-step = count 1.
 bool tcd_ok(const ackpt_lstm* c, std::initializer_list<const void*> ptrs);
 void tcd_forward(const ackpt_lstm* c, int64_t from, int count, const float* in, float* out, float* const* outs,

@@ -1,0 +1,171 @@
+// Small-batch LSTM kernels (B <= kSmallBatch, any d <= 128, f32 or f64):
+// the reference's own workload is a single sequence (B = 1, float64 byte
+// image, lstm.py:99-107), where one thread per sequence would run all 4 d^2
+// products serially.  Here a CTA owns one sequence and its 4d threads own
+// the gate rows:
+//   phase 1  thread n = gate row (g, j): a[n] = xb_k[n] + sum_k W[n][k] h[k]
+//   phase 2  thread j < d: the activations, c' and h' (forward), or the
+//            gate adjoints da[g][j] and dc (reverse, lstm.py:141-151)
+//   phase 3  (reverse) thread m < d: dh[m] = sum_{g,j} W[g][j][m] da[g][j]
+// with __syncthreads between phases and the state in shared memory across
+// steps, so a fused Advance / TapeForward / Reverse run is one launch.  Same
+// formulas and math-library calls as the generic kernels (lstm_generic.cu),
+// so float64 results stay within 1e-12 of the reference.
+#include <cuda_runtime.h>
+
+#include <cmath>
+
+#include "lstm_cell.h"
+
+namespace ackpt {
+namespace sb {
+
+__device__ __forceinline__ float sigmoid(float z) { return 1.0f / (1.0f + expf(-z)); }
+__device__ __forceinline__ double sigmoid(double z) { return 1.0 / (1.0 + exp(-z)); }
+__device__ __forceinline__ float tanh_(float z) { return tanhf(z); }
+__device__ __forceinline__ double tanh_(double z) { return tanh(z); }
+
+struct Ptrs {
+  const void* p[ACKPT_MAX_FUSED];
+};
+
+// a[n] = xb[n] + W[n] . h for this thread's gate row n (n < 4d)
+template <typename T>
+__device__ __forceinline__ T gate_row(const T* __restrict__ wh, const T* __restrict__ xb, const T* h, int d, int n) {
+  const T* w = wh + int64_t(n) * d;
+  T acc = __ldg(xb + n);
+#pragma unroll 4
+  for (int k = 0; k < d; ++k) acc = fma(__ldg(w + k), h[k], acc);
+  return acc;
+}
+
+// Forward over `count` steps from `from`.  tape != null: store every step's
+// state to tape[i]; otherwise the final state to `out`.
+template <typename T>
+__global__ void fwd(const T* __restrict__ in, T* __restrict__ out, int64_t B, int d, const T* __restrict__ wh,
+                    const T* __restrict__ xb_all, int64_t from, int count, bool tape, const __grid_constant__ Ptrs outs) {
+  extern __shared__ __align__(16) unsigned char raw[];
+  T* h = reinterpret_cast<T*>(raw);
+  T* c = h + d;
+  T* a = c + d;  // 4d
+  const int64_t b = blockIdx.x;
+  const int n = threadIdx.x;
+  if (n < d) {
+    h[n] = in[int64_t(n) * B + b];
+    c[n] = in[int64_t(d + n) * B + b];
+  }
+  __syncthreads();
+  for (int i = 0; i < count; ++i) {
+    a[n] = gate_row(wh, xb_all + (from + i) * 4 * d, h, d, n);
+    __syncthreads();
+    if (n < d) {
+      const T f = sigmoid(a[n]), ig = sigmoid(a[d + n]), o = sigmoid(a[2 * d + n]), g = tanh_(a[3 * d + n]);
+      const T cn = f * c[n] + ig * g;  // lstm.py:127
+      c[n] = cn;
+      h[n] = o * tanh_(cn);            // lstm.py:128
+      if (tape) {
+        T* dst = static_cast<T*>(const_cast<void*>(outs.p[i]));
+        dst[int64_t(n) * B + b] = h[n];
+        dst[int64_t(d + n) * B + b] = cn;
+      }
+    }
+    __syncthreads();
+  }
+  if (!tape && n < d) {
+    out[int64_t(n) * B + b] = h[n];
+    out[int64_t(d + n) * B + b] = c[n];
+  }
+}
+
+// Reverse over steps from+count-1 .. from; states.p[i] is the state of step from+i.
+template <typename T>
+__global__ void rev(const T* __restrict__ adj_in, T* __restrict__ adj_out, int64_t B, int d, const T* __restrict__ wh,
+                    const T* __restrict__ xb_all, int64_t from, int count, const __grid_constant__ Ptrs states) {
+  extern __shared__ __align__(16) unsigned char raw[];
+  T* h = reinterpret_cast<T*>(raw);
+  T* c = h + d;
+  T* dh = c + d;
+  T* dc = dh + d;
+  T* a = dc + d;   // 4d gate pre-activations
+  T* da = a + 4 * d;  // 4d gate adjoints
+  const int64_t b = blockIdx.x;
+  const int n = threadIdx.x;
+  if (n < d) {
+    dh[n] = adj_in[int64_t(n) * B + b];
+    dc[n] = adj_in[int64_t(d + n) * B + b];
+  }
+  for (int i = count - 1; i >= 0; --i) {
+    const T* st = static_cast<const T*>(states.p[i]);
+    if (n < d) {
+      h[n] = st[int64_t(n) * B + b];
+      c[n] = st[int64_t(d + n) * B + b];
+    }
+    __syncthreads();
+    a[n] = gate_row(wh, xb_all + (from + i) * 4 * d, h, d, n);
+    __syncthreads();
+    if (n < d) {
+      const T f = sigmoid(a[n]), ig = sigmoid(a[d + n]), o = sigmoid(a[2 * d + n]), g = tanh_(a[3 * d + n]);
+      const T cn = f * c[n] + ig * g;
+      const T t = tanh_(cn);
+      const T dhn = dh[n];
+      const T dco = dc[n] + dhn * o * (T(1) - t * t);  // lstm.py:143
+      da[n] = dco * c[n] * f * (T(1) - f);            // lstm.py:144
+      da[d + n] = dco * g * ig * (T(1) - ig);         // lstm.py:145
+      da[2 * d + n] = dhn * t * o * (T(1) - o);       // lstm.py:142,146
+      da[3 * d + n] = dco * ig * (T(1) - g * g);      // lstm.py:147
+      dc[n] = dco * f;                                // lstm.py:151
+    }
+    __syncthreads();
+    if (n < d) {  // lstm.py:149-150: dh = sum_g W_g^T da_g
+      T acc = T(0);
+      for (int g = 0; g < 4; ++g) {
+        const T* w = wh + int64_t(g) * d * d + n;
+        const T* dg = da + g * d;
+#pragma unroll 4
+        for (int j = 0; j < d; ++j) acc = fma(__ldg(w + int64_t(j) * d), dg[j], acc);
+      }
+      dh[n] = acc;
+    }
+    __syncthreads();
+  }
+  if (n < d) {
+    adj_out[int64_t(n) * B + b] = dh[n];
+    adj_out[int64_t(d + n) * B + b] = dc[n];
+  }
+}
+
+}  // namespace sb
+
+bool sb_ok(const ackpt_lstm* c) { return c->B <= kSmallBatch && c->d <= kMaxD; }
+
+template <typename T>
+void sb_forward(const ackpt_lstm* c, int64_t from, int count, const void* in, void* out, void* const* outs,
+                cudaStream_t s) {
+  sb::Ptrs o{};
+  if (outs)
+    for (int i = 0; i < count; ++i) o.p[i] = outs[i];
+  const size_t smem = size_t(6) * c->d * sizeof(T);
+  sb::fwd<T><<<unsigned(c->B), unsigned(4 * c->d), smem, s>>>(
+      static_cast<const T*>(in), static_cast<T*>(out), c->B, c->d, static_cast<const T*>(c->d_wh),
+      static_cast<const T*>(c->d_xb), from, count, outs != nullptr, o);
+}
+
+template <typename T>
+void sb_reverse(const ackpt_lstm* c, int64_t from, int count, const void* const* states, const void* adj_in,
+                void* adj_out, cudaStream_t s) {
+  sb::Ptrs p{};
+  for (int i = 0; i < count; ++i) p.p[i] = states[i];
+  const size_t smem = size_t(12) * c->d * sizeof(T);
+  sb::rev<T><<<unsigned(c->B), unsigned(4 * c->d), smem, s>>>(
+      static_cast<const T*>(adj_in), static_cast<T*>(adj_out), c->B, c->d, static_cast<const T*>(c->d_wh),
+      static_cast<const T*>(c->d_xb), from, count, p);
+}
+
+template void sb_forward<float>(const ackpt_lstm*, int64_t, int, const void*, void*, void* const*, cudaStream_t);
+template void sb_forward<double>(const ackpt_lstm*, int64_t, int, const void*, void*, void* const*, cudaStream_t);
+template void sb_reverse<float>(const ackpt_lstm*, int64_t, int, const void* const*, const void*, void*,
+                                cudaStream_t);
+template void sb_reverse<double>(const ackpt_lstm*, int64_t, int, const void* const*, const void*, void*,
+                                 cudaStream_t);
+
+}  // namespace ackpt

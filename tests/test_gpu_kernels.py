@@ -213,3 +213,37 @@ def test_large_d_tensor_core_fused(P, d, batch):
     for i, k in reversed(list(enumerate(range(2, 34)))):
         chain = dc.backward(k, states[i], chain)
     assert torch.equal(chain.cpu(), torch.from_numpy(fused))
+
+
+@pytest.mark.parametrize("d,batch,dtype", [(32, 1, "f64"), (16, 3, "f64"), (5, 37, "f32"), (8, 1, "f32"), (128, 2, "f64")])
+def test_small_batch_kernels(P, d, batch, dtype):
+    # B <= 1024 outside the fp32 fast paths: one CTA per sequence
+    # (lstm_small.cu), per-step and fused launches, float64 within 1e-12
+    cell, ocell = _cells(P, d, 30, 40 + d)
+    npdt = np.float64 if dtype == "f64" else np.float32
+    tol = 1e-12 if dtype == "f64" else F32_TOL
+    x = torch.from_numpy(_states(d, 41, batch).astype(npdt)).cuda()
+    a = torch.from_numpy(_states(d, 42, batch).astype(npdt)).cuda()
+    dc = P.device_cell(cell, batch, dtype)
+    ref = x.double().cpu().numpy()
+    refs = []
+    for k in range(3, 23):
+        ref = L.forward_step(ocell, k, ref)
+        refs.append(ref)
+    assert L.rel_l2(dc.advance(3, 23, x).cpu().numpy(), refs[-1]) <= tol
+    outs = dc.forward_many(3, 20, x)
+    assert max(L.rel_l2(o.cpu().numpy(), r) for o, r in zip(outs, refs)) <= tol
+    chain = x
+    for k in range(3, 23):
+        chain = dc.forward(k, chain)
+    assert torch.equal(chain, outs[-1])
+    states = [x] + outs[:-1]
+    adj = a.double().cpu().numpy()
+    for i, k in reversed(list(enumerate(range(3, 23)))):
+        adj = L.backward_step(ocell, k, states[i].double().cpu().numpy(), adj)
+    fused = dc.backward_many(3, states, a)
+    assert L.rel_l2(fused.cpu().numpy(), adj) <= tol
+    per_step = a
+    for i, k in reversed(list(enumerate(range(3, 23)))):
+        per_step = dc.backward(k, states[i], per_step)
+    assert torch.equal(per_step, fused)
