@@ -29,25 +29,38 @@ struct Ptrs {
   const void* p[ACKPT_MAX_FUSED];
 };
 
-// a[n] = xb[n] + W[n] . h for this thread's gate row n (n < 4d)
+// a[n] = xb[n] + W[n] . h for this thread's gate row n (n < 4d); W is the
+// CTA's shared-memory copy when it fits (else global).
 template <typename T>
-__device__ __forceinline__ T gate_row(const T* __restrict__ wh, const T* __restrict__ xb, const T* h, int d, int n) {
-  const T* w = wh + int64_t(n) * d;
+__device__ __forceinline__ T gate_row(const T* w_all, const T* __restrict__ xb, const T* h, int d, int n) {
+  const T* w = w_all + int64_t(n) * d;
   T acc = __ldg(xb + n);
 #pragma unroll 4
-  for (int k = 0; k < d; ++k) acc = fma(__ldg(w + k), h[k], acc);
+  for (int k = 0; k < d; ++k) acc = fma(w[k], h[k], acc);
   return acc;
+}
+
+// W (4 d x d) into shared memory when it fits next to the state: returns the
+// pointer the gate / transposed products read.
+template <typename T>
+__device__ __forceinline__ const T* stage_w(T* ws, bool in_smem, const T* __restrict__ wh, int d) {
+  if (!in_smem) return wh;
+  for (int i = threadIdx.x; i < 4 * d * d; i += blockDim.x) ws[i] = __ldg(wh + i);
+  __syncthreads();
+  return ws;
 }
 
 // Forward over `count` steps from `from`.  tape != null: store every step's
 // state to tape[i]; otherwise the final state to `out`.
 template <typename T>
 __global__ void fwd(const T* __restrict__ in, T* __restrict__ out, int64_t B, int d, const T* __restrict__ wh,
-                    const T* __restrict__ xb_all, int64_t from, int count, bool tape, const __grid_constant__ Ptrs outs) {
+                    const T* __restrict__ xb_all, int64_t from, int count, bool tape, bool w_smem,
+                    const __grid_constant__ Ptrs outs) {
   extern __shared__ __align__(16) unsigned char raw[];
   T* h = reinterpret_cast<T*>(raw);
   T* c = h + d;
   T* a = c + d;  // 4d
+  const T* w = stage_w(a + 4 * d, w_smem, wh, d);
   const int64_t b = blockIdx.x;
   const int n = threadIdx.x;
   if (n < d) {
@@ -56,7 +69,7 @@ __global__ void fwd(const T* __restrict__ in, T* __restrict__ out, int64_t B, in
   }
   __syncthreads();
   for (int i = 0; i < count; ++i) {
-    a[n] = gate_row(wh, xb_all + (from + i) * 4 * d, h, d, n);
+    a[n] = gate_row(w, xb_all + (from + i) * 4 * d, h, d, n);
     __syncthreads();
     if (n < d) {
       const T f = sigmoid(a[n]), ig = sigmoid(a[d + n]), o = sigmoid(a[2 * d + n]), g = tanh_(a[3 * d + n]);
@@ -80,14 +93,16 @@ __global__ void fwd(const T* __restrict__ in, T* __restrict__ out, int64_t B, in
 // Reverse over steps from+count-1 .. from; states.p[i] is the state of step from+i.
 template <typename T>
 __global__ void rev(const T* __restrict__ adj_in, T* __restrict__ adj_out, int64_t B, int d, const T* __restrict__ wh,
-                    const T* __restrict__ xb_all, int64_t from, int count, const __grid_constant__ Ptrs states) {
+                    const T* __restrict__ xb_all, int64_t from, int count, bool w_smem,
+                    const __grid_constant__ Ptrs states) {
   extern __shared__ __align__(16) unsigned char raw[];
   T* h = reinterpret_cast<T*>(raw);
   T* c = h + d;
   T* dh = c + d;
   T* dc = dh + d;
-  T* a = dc + d;   // 4d gate pre-activations
+  T* a = dc + d;      // 4d gate pre-activations, then the 4 per-gate partial dh
   T* da = a + 4 * d;  // 4d gate adjoints
+  const T* w = stage_w(da + 4 * d, w_smem, wh, d);
   const int64_t b = blockIdx.x;
   const int n = threadIdx.x;
   if (n < d) {
@@ -101,7 +116,7 @@ __global__ void rev(const T* __restrict__ adj_in, T* __restrict__ adj_out, int64
       c[n] = st[int64_t(d + n) * B + b];
     }
     __syncthreads();
-    a[n] = gate_row(wh, xb_all + (from + i) * 4 * d, h, d, n);
+    a[n] = gate_row(w, xb_all + (from + i) * 4 * d, h, d, n);
     __syncthreads();
     if (n < d) {
       const T f = sigmoid(a[n]), ig = sigmoid(a[d + n]), o = sigmoid(a[2 * d + n]), g = tanh_(a[3 * d + n]);
@@ -116,16 +131,17 @@ __global__ void rev(const T* __restrict__ adj_in, T* __restrict__ adj_out, int64
       dc[n] = dco * f;                                // lstm.py:151
     }
     __syncthreads();
-    if (n < d) {  // lstm.py:149-150: dh = sum_g W_g^T da_g
+    {  // lstm.py:149-150: dh = sum_g W_g^T da_g; thread (g, m) sums gate g, then a fixed-order reduction
+      const int g = n / d, m = n - g * d;
+      const T* wg = w + int64_t(g) * d * d + m;
+      const T* dg = da + g * d;
       T acc = T(0);
-      for (int g = 0; g < 4; ++g) {
-        const T* w = wh + int64_t(g) * d * d + n;
-        const T* dg = da + g * d;
 #pragma unroll 4
-        for (int j = 0; j < d; ++j) acc = fma(__ldg(w + int64_t(j) * d), dg[j], acc);
-      }
-      dh[n] = acc;
+      for (int j = 0; j < d; ++j) acc = fma(wg[int64_t(j) * d], dg[j], acc);
+      a[n] = acc;  // gate pre-activations are dead by now
     }
+    __syncthreads();
+    if (n < d) dh[n] = (a[n] + a[d + n]) + (a[2 * d + n] + a[3 * d + n]);
     __syncthreads();
   }
   if (n < d) {
@@ -138,16 +154,22 @@ __global__ void rev(const T* __restrict__ adj_in, T* __restrict__ adj_out, int64
 
 bool sb_ok(const ackpt_lstm* c) { return c->B <= kSmallBatch && c->d <= kMaxD; }
 
+// shared-memory budget of the small-batch kernels (W copied in when it fits)
+constexpr size_t kSmallWBytes = 160 * 1024;
+
 template <typename T>
 void sb_forward(const ackpt_lstm* c, int64_t from, int count, const void* in, void* out, void* const* outs,
                 cudaStream_t s) {
   sb::Ptrs o{};
   if (outs)
     for (int i = 0; i < count; ++i) o.p[i] = outs[i];
-  const size_t smem = size_t(6) * c->d * sizeof(T);
+  const size_t base = size_t(6) * c->d * sizeof(T), wbytes = size_t(4) * c->d * c->d * sizeof(T);
+  const bool w_smem = count >= 8 && base + wbytes <= kSmallWBytes;  // amortised over >= 8 steps
+  const size_t smem = base + (w_smem ? wbytes : 0);
+  if (smem > 48 * 1024) cudaFuncSetAttribute(sb::fwd<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
   sb::fwd<T><<<unsigned(c->B), unsigned(4 * c->d), smem, s>>>(
       static_cast<const T*>(in), static_cast<T*>(out), c->B, c->d, static_cast<const T*>(c->d_wh),
-      static_cast<const T*>(c->d_xb), from, count, outs != nullptr, o);
+      static_cast<const T*>(c->d_xb), from, count, outs != nullptr, w_smem, o);
 }
 
 template <typename T>
@@ -155,10 +177,13 @@ void sb_reverse(const ackpt_lstm* c, int64_t from, int count, const void* const*
                 void* adj_out, cudaStream_t s) {
   sb::Ptrs p{};
   for (int i = 0; i < count; ++i) p.p[i] = states[i];
-  const size_t smem = size_t(12) * c->d * sizeof(T);
+  const size_t base = size_t(12) * c->d * sizeof(T), wbytes = size_t(4) * c->d * c->d * sizeof(T);
+  const bool w_smem = count >= 8 && base + wbytes <= kSmallWBytes;  // amortised over >= 8 steps
+  const size_t smem = base + (w_smem ? wbytes : 0);
+  if (smem > 48 * 1024) cudaFuncSetAttribute(sb::rev<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
   sb::rev<T><<<unsigned(c->B), unsigned(4 * c->d), smem, s>>>(
       static_cast<const T*>(adj_in), static_cast<T*>(adj_out), c->B, c->d, static_cast<const T*>(c->d_wh),
-      static_cast<const T*>(c->d_xb), from, count, p);
+      static_cast<const T*>(c->d_xb), from, count, w_smem, p);
 }
 
 template void sb_forward<float>(const ackpt_lstm*, int64_t, int, const void*, void*, void* const*, cudaStream_t);
