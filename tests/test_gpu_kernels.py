@@ -135,7 +135,7 @@ def test_fused_advance(P, family, d, batch, dtype):
         assert torch.equal(fused, chain)  # identical arithmetic per step
 
 
-@pytest.mark.parametrize("d,batch", [(8, 4096), (4, 512), (8, 1002), (8, 300)])
+@pytest.mark.parametrize("d,batch", [(8, 4096), (4, 512), (8, 1002), (8, 300), (8, 2), (8, 258)])
 def test_fused_tape_and_reverse(P, family, d, batch):
     cell, ocell = _cells(P, d, 70, 22)
     x = torch.from_numpy(_states(d, 9, batch).astype(np.float32)).cuda()
