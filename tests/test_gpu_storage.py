@@ -52,9 +52,13 @@ def test_simulated_latency_and_bandwidth(pkg):
         b.close()
     b = pkg.SimulatedBackend(bandwidth=16 * 2**20, latency=0.0)
     try:
-        t0 = time.perf_counter()
-        b.wait(b.begin_store(0, pkg.CheckpointPayload(0, b"\x01" * 2**20)))
-        assert time.perf_counter() - t0 == pytest.approx(0.0625, rel=0.10)
+        b.wait(b.begin_store(0, pkg.CheckpointPayload(0, b"\x01" * 2**20)))  # first use: pinned allocation
+        el = []
+        for i in range(3):
+            t0 = time.perf_counter()
+            b.wait(b.begin_store(i, pkg.CheckpointPayload(i, b"\x01" * 2**20)))
+            el.append(time.perf_counter() - t0)
+        assert sorted(el)[1] == pytest.approx(0.0625, rel=0.10)
     finally:
         b.close()
 
