@@ -3,6 +3,7 @@
 #include "lstm_f32_tcd.cuh"
 
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <string>
 
@@ -18,7 +19,7 @@ unsigned tcd_tiles(int64_t B) { return unsigned((B + tcd::kThreads - 1) / tcd::k
 // (measured at 32 MiB: d=32 reverse step 102 -> 65 us; d=16 forward step
 // 23 -> 35 us, hence not there).
 template <class K>
-unsigned tcd_grid(int64_t B, int count, K kernel, size_t smem, bool persistent) {
+unsigned tcd_grid(int64_t B, int count, K kernel, size_t smem, bool persistent, int tmem_cols) {
   const unsigned tiles = tcd_tiles(B);
   if (count > 1 || !persistent) return tiles;
   static int sms = [] {
@@ -27,8 +28,20 @@ unsigned tcd_grid(int64_t B, int count, K kernel, size_t smem, bool persistent) 
     cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
     return n;
   }();
-  int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, tcd::kThreads, smem);
+  // resident CTAs per SM from the three real limits (the occupancy API does
+  // not know TMEM and reported 1 here): 512 TMEM columns, shared memory
+  // (1 KB reserved per CTA), registers
+  cudaFuncAttributes fa{};
+  cudaFuncGetAttributes(&fa, kernel);
+  int smem_sm = 0, dev = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
+  const int by_tmem = 512 / std::max(32, tmem_cols);
+  const int by_smem = int(size_t(smem_sm) / (smem + fa.sharedSizeBytes + 1024));
+  const int by_regs = 65536 / std::max(1, fa.numRegs * tcd::kThreads);
+  const int per_sm = std::min({by_tmem, by_smem, by_regs});
+  if (std::getenv("ACKPT_TCD_TRACE"))
+    std::fprintf(stderr, "tcd grid: %d CTAs/SM (tmem %d smem %d regs %d)\n", per_sm, by_tmem, by_smem, by_regs);
   const unsigned cap = unsigned(std::max(1, per_sm) * sms);
   return std::min(tiles, cap);
 }
@@ -38,8 +51,10 @@ void fwd_launch(const ackpt_lstm* c, int64_t from, int count, const float* in, f
                 cudaStream_t s) {
   using L = tcd::Layout<D>;
   static bool attr = [] {
-    cudaFuncSetAttribute(tcd::fwd_tcd<D, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(L::fwd_bytes));
-    cudaFuncSetAttribute(tcd::fwd_tcd<D, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(L::fwd_bytes));
+    for (auto k : {tcd::fwd_tcd<D, false>, tcd::fwd_tcd<D, true>}) {
+      cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(L::fwd_bytes));
+      cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100);  // max shared memory
+    }
     return true;
   }();
   (void)attr;
@@ -48,10 +63,10 @@ void fwd_launch(const ackpt_lstm* c, int64_t from, int count, const float* in, f
   const auto ws = static_cast<const float*>(c->d_ws);
   if (outs) {
     for (int i = 0; i < count; ++i) o.p[i] = outs[i];
-    tcd::fwd_tcd<D, true><<<tcd_grid(c->B, count, tcd::fwd_tcd<D, true>, L::fwd_bytes, D > 16), tcd::kThreads, L::fwd_bytes,
+    tcd::fwd_tcd<D, true><<<tcd_grid(c->B, count, tcd::fwd_tcd<D, true>, L::fwd_bytes, D > 16, tcd::tmem_cols(4 * D)), tcd::kThreads, L::fwd_bytes,
                             s>>>(in, nullptr, c->B, xb, ws, from, count, o);
   } else {
-    tcd::fwd_tcd<D, false><<<tcd_grid(c->B, count, tcd::fwd_tcd<D, false>, L::fwd_bytes, D > 16), tcd::kThreads,
+    tcd::fwd_tcd<D, false><<<tcd_grid(c->B, count, tcd::fwd_tcd<D, false>, L::fwd_bytes, D > 16, tcd::tmem_cols(4 * D)), tcd::kThreads,
                              L::fwd_bytes, s>>>(in, out, c->B, xb, ws, from, count, o);
   }
 }
@@ -62,12 +77,13 @@ void rev_launch(const ackpt_lstm* c, int64_t from, int count, const float* const
   using L = tcd::Layout<D>;
   static bool attr = [] {
     cudaFuncSetAttribute(tcd::rev_tcd<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(L::rev_bytes));
+    cudaFuncSetAttribute(tcd::rev_tcd<D>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     return true;
   }();
   (void)attr;
   tcd::StatePtrs sp{};
   for (int i = 0; i < count; ++i) sp.p[i] = states[i];
-  tcd::rev_tcd<D><<<tcd_grid(c->B, count, tcd::rev_tcd<D>, L::rev_bytes, true), tcd::kThreads, L::rev_bytes, s>>>(
+  tcd::rev_tcd<D><<<tcd_grid(c->B, count, tcd::rev_tcd<D>, L::rev_bytes, true, tcd::tmem_cols(9 * D)), tcd::kThreads, L::rev_bytes, s>>>(
       ai, ao, c->B, static_cast<const float*>(c->d_xbs), static_cast<const float*>(c->d_ws), from, count, sp);
 }
 
