@@ -83,7 +83,7 @@ void rev_launch(const ackpt_lstm* c, int64_t from, int count, const float* const
   (void)attr;
   tcd::StatePtrs sp{};
   for (int i = 0; i < count; ++i) sp.p[i] = states[i];
-  tcd::rev_tcd<D><<<tcd_grid(c->B, count, tcd::rev_tcd<D>, L::rev_bytes, true, tcd::tmem_cols(9 * D)), tcd::kThreads, L::rev_bytes, s>>>(
+  tcd::rev_tcd<D><<<tcd_grid(c->B, count, tcd::rev_tcd<D>, L::rev_bytes, true, tcd::tmem_cols(7 * D)), tcd::kThreads, L::rev_bytes, s>>>(
       ai, ao, c->B, static_cast<const float*>(c->d_xbs), static_cast<const float*>(c->d_ws), from, count, sp);
 }
 

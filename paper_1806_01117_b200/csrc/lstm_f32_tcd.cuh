@@ -13,8 +13,8 @@
 //   reverse da (the scaled gate adjoints of bwd_unit) go back into TMEM as
 //           the A operand of dh[128 x D] = da[128 x 4D] . B2[D x 4D]^T with
 //           B2[m][n] = s_gate W_gate[j(n)][m], 3xTF32 as well: da_hi over G in
-//           place, da_lo in [4D, 8D), dh in [8D, 9D) (TMEM-A form validated in
-//           tools/umma_ts_probe.cu).  (A bf16 residual would save 2D columns
+//           place, da_lo of one K half at a time in [4D, 6D), dh in [6D, 7D)
+//           (TMEM-A form validated in tools/umma_ts_probe.cu).  (A bf16 residual would save 2D columns
 //           but costs ~2^-19 per product: 1.2e-5 rel-L2 after 100 steps at d=32.)
 // Operands are K-major, no swizzle, 8-row groups of 16-byte core matrices
 // (LBO 128 B between K chunks, SBO = 32 K bytes between row groups).
@@ -315,6 +315,10 @@ __global__ void __launch_bounds__(kThreads)
 }
 
 // Reverse over steps from+count-1 .. from (count = 1: the per-step adjoint).
+// The transposed product runs in two K halves (unit pairs p < D/4, then the
+// rest) that share one 2D-column residual region: the first half's MMAs run
+// while the threads compute the second half's gate adjoints, and TMEM drops
+// from 9D to 7D columns (d=32: 512 -> 256, so 2 CTAs/SM instead of 1).
 template <int D>
 __global__ void __launch_bounds__(kThreads)
     rev_tcd(const float* __restrict__ adj_in, float* __restrict__ adj_out, int64_t B, const float* __restrict__ xbs_all,
@@ -323,8 +327,9 @@ __global__ void __launch_bounds__(kThreads)
   extern __shared__ __align__(128) float sm[];
   uint64_t* bars = reinterpret_cast<uint64_t*>(sm + L::rev_end);
   uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 2);
-  constexpr int kCols = tmem_cols(9 * D);
-  constexpr uint32_t kLo = 4 * D, kDh = 8 * D;
+  constexpr int kCols = tmem_cols(7 * D);
+  constexpr uint32_t kLo = 4 * D, kDh = 6 * D;
+  constexpr int kHalf = D / 4;  // unit pairs per K half
   setup<D>(sm, bars, tslot, ws, kCols, 2);
   const uint32_t tmem = tmem_base(tslot);
   // B2[m][n] = s_gate W_gate[j(n)][m], K = 4D (gate-row order), tf32 hi/lo
@@ -337,7 +342,22 @@ __global__ void __launch_bounds__(kThreads)
     sm[L::w2_lo + kofs<4 * D>(m, n)] = x - hi_part(x);
   }
   const uint32_t lane = uint32_t((threadIdx.x >> 5) * 32) << 16;
-  uint32_t phase = 0;
+  // Thread 0: dh (+)= da . B2^T over unit pairs [p0, p0 + kHalf) (residual at kLo).
+  auto issue_half = [&](int p0, bool first) {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    constexpr uint32_t it = idesc<D>(false), sbo32 = 32 * 4 * D;
+#pragma unroll
+    for (int q = 0; q < kHalf; ++q) {  // K = 8 per MMA = one unit pair, small terms first
+      const int ks = p0 + q;
+      const uint32_t off = uint32_t(ks) * 256u;
+      const uint64_t bh = desc(su32(sm + L::w2_hi) + off, sbo32), bl = desc(su32(sm + L::w2_lo) + off, sbo32);
+      mma_ts(tmem + kDh, tmem + kLo + uint32_t(8 * q), bh, it, (first && q == 0) ? 0u : 1u, false);
+      mma_ts(tmem + kDh, tmem + uint32_t(8 * ks), bl, it, 1u, false);
+      mma_ts(tmem + kDh, tmem + uint32_t(8 * ks), bh, it, 1u, false);
+    }
+    commit(bars + 1);
+  };
+  uint32_t phase = 0, phase2 = 0;
   // persistent over 128-sequence tiles (the weight setup is paid once per CTA)
   for (int64_t tile = blockIdx.x; tile * kThreads < B; tile += gridDim.x) {
   const int64_t b = tile * kThreads + threadIdx.x;
@@ -364,47 +384,43 @@ __global__ void __launch_bounds__(kThreads)
     if (threadIdx.x == 0) issue_gates<D>(sm, tmem, bars);
     wait_bar(bars, phase & 1u);
 #pragma unroll
-    for (int p0 = 0; p0 < D / 2; p0 += 4) {
-      float g[4][8];
+    for (int half = 0; half < 2; ++half) {
 #pragma unroll
-      for (int q = 0; q < 4; ++q) ld8(tmem + lane + uint32_t(8 * (p0 + q)), g[q]);
-      ld_wait();
+      for (int p0 = half * kHalf; p0 < (half + 1) * kHalf; p0 += 4) {
+        float g[4][8];
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const int p = p0 + q;
-        float2 da[4];
-        bwd_unit(make_float2(g[q][0], g[q][1]), make_float2(g[q][2], g[q][3]), make_float2(g[q][4], g[q][5]),
-                 make_float2(g[q][6], g[q][7]), c[p], dh[p], dc[p], da[0], da[1], da[2], da[3], dc[p]);
-        uint32_t hv[8], lv[8];
-#pragma unroll
-        for (int gi = 0; gi < 4; ++gi) {
-          const float2 hi = make_float2(hi_part(da[gi].x), hi_part(da[gi].y));
-          const float2 lo = sub2(da[gi], hi);
-          hv[2 * gi] = __float_as_uint(hi.x);
-          hv[2 * gi + 1] = __float_as_uint(hi.y);
-          lv[2 * gi] = __float_as_uint(lo.x);
-          lv[2 * gi + 1] = __float_as_uint(lo.y);
+        for (int q = 0; q < 4; ++q) ld8(tmem + lane + uint32_t(8 * (p0 + q)), g[q]);
+        ld_wait();
+        if (half == 1 && p0 == kHalf) {  // the residual region is free once the first half's MMAs are done
+          wait_bar(bars + 1, phase2 & 1u);
+          ++phase2;
         }
-        st8(tmem + lane + uint32_t(8 * p), hv);
-        st8(tmem + lane + kLo + uint32_t(8 * p), lv);
-      }
-    }
-    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-    publish();
-    if (threadIdx.x == 0) {
-      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      constexpr uint32_t it = idesc<D>(false), sbo32 = 32 * 4 * D;
 #pragma unroll
-      for (int ks = 0; ks < D / 2; ++ks) {  // K = 8 per MMA over K = 4D, small terms first
-        const uint32_t off = uint32_t(ks) * 256u;
-        const uint64_t bh = desc(su32(sm + L::w2_hi) + off, sbo32), bl = desc(su32(sm + L::w2_lo) + off, sbo32);
-        mma_ts(tmem + kDh, tmem + kLo + uint32_t(8 * ks), bh, it, ks ? 1u : 0u, false);
-        mma_ts(tmem + kDh, tmem + uint32_t(8 * ks), bl, it, 1u, false);
-        mma_ts(tmem + kDh, tmem + uint32_t(8 * ks), bh, it, 1u, false);
+        for (int q = 0; q < 4; ++q) {
+          const int p = p0 + q;
+          float2 da[4];
+          bwd_unit(make_float2(g[q][0], g[q][1]), make_float2(g[q][2], g[q][3]), make_float2(g[q][4], g[q][5]),
+                   make_float2(g[q][6], g[q][7]), c[p], dh[p], dc[p], da[0], da[1], da[2], da[3], dc[p]);
+          uint32_t hv[8], lv[8];
+#pragma unroll
+          for (int gi = 0; gi < 4; ++gi) {
+            const float2 hi = make_float2(hi_part(da[gi].x), hi_part(da[gi].y));
+            const float2 lo = sub2(da[gi], hi);
+            hv[2 * gi] = __float_as_uint(hi.x);
+            hv[2 * gi + 1] = __float_as_uint(hi.y);
+            lv[2 * gi] = __float_as_uint(lo.x);
+            lv[2 * gi + 1] = __float_as_uint(lo.y);
+          }
+          st8(tmem + lane + uint32_t(8 * p), hv);
+          st8(tmem + lane + kLo + uint32_t(8 * (p - half * kHalf)), lv);
+        }
       }
-      commit(bars + 1);
+      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+      publish();
+      if (threadIdx.x == 0) issue_half(half * kHalf, half == 0);
     }
-    wait_bar(bars + 1, phase & 1u);
+    wait_bar(bars + 1, phase2 & 1u);
+    ++phase2;
 #pragma unroll
     for (int m0 = 0; m0 < D; m0 += 8) {
       float v[8];
