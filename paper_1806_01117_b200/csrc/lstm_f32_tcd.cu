@@ -13,11 +13,9 @@ namespace {
 
 unsigned tcd_tiles(int64_t B) { return unsigned((B + tcd::kThreads - 1) / tcd::kThreads); }
 
-// Grid: one CTA per tile for fused launches (long-running) and for the light
-// d=16 forward step; otherwise persistent CTAs up to the resident capacity,
-// each looping over tiles so the weight setup is paid once per CTA
-// (measured at 32 MiB: d=32 reverse step 102 -> 65 us; d=16 forward step
-// 23 -> 35 us, hence not there).
+// Grid: one CTA per tile for fused launches (long-running); per-step
+// launches run persistent CTAs, as many per SM as fit, each looping over
+// tiles so the weight setup is paid once per CTA.
 template <class K>
 unsigned tcd_grid(int64_t B, int count, K kernel, size_t smem, bool persistent, int tmem_cols) {
   const unsigned tiles = tcd_tiles(B);
@@ -63,10 +61,10 @@ void fwd_launch(const ackpt_lstm* c, int64_t from, int count, const float* in, f
   const auto ws = static_cast<const float*>(c->d_ws);
   if (outs) {
     for (int i = 0; i < count; ++i) o.p[i] = outs[i];
-    tcd::fwd_tcd<D, true><<<tcd_grid(c->B, count, tcd::fwd_tcd<D, true>, L::fwd_bytes, D > 16, tcd::tmem_cols(4 * D)), tcd::kThreads, L::fwd_bytes,
+    tcd::fwd_tcd<D, true><<<tcd_grid(c->B, count, tcd::fwd_tcd<D, true>, L::fwd_bytes, true, tcd::tmem_cols(4 * D)), tcd::kThreads, L::fwd_bytes,
                             s>>>(in, nullptr, c->B, xb, ws, from, count, o);
   } else {
-    tcd::fwd_tcd<D, false><<<tcd_grid(c->B, count, tcd::fwd_tcd<D, false>, L::fwd_bytes, D > 16, tcd::tmem_cols(4 * D)), tcd::kThreads,
+    tcd::fwd_tcd<D, false><<<tcd_grid(c->B, count, tcd::fwd_tcd<D, false>, L::fwd_bytes, true, tcd::tmem_cols(4 * D)), tcd::kThreads,
                              L::fwd_bytes, s>>>(in, out, c->B, xb, ws, from, count, o);
   }
 }
