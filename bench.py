@@ -301,11 +301,16 @@ def run_c1(pkg, lstm) -> dict:
             fused = lstm.bench(strat, n=1000, d=32, s=10, backend_config={"kind": "file", "dir": scratch}, seed=0,
                                runs=5, fuse=True)
             assert fused.gradient_checksum == rep.gradient_checksum  # same kernels, same bits
+            graphed = lstm.bench(strat, n=1000, d=32, s=10, backend_config={"kind": "file", "dir": scratch}, seed=0,
+                                 runs=5, graph=True)
+            assert graphed.gradient_checksum == rep.gradient_checksum
             out[name] = {"wall_ms": rep.wall_seconds * 1e3, "forward_evals": rep.forward_evals,
                          "recompute_factor": rep.recompute_factor_measured, "stall_ms": rep.stall_seconds * 1e3,
                          "speedup_vs_reference_cpu": C1_REFERENCE_MS[name] / (rep.wall_seconds * 1e3),
                          "fused_wall_ms": fused.wall_seconds * 1e3,
-                         "fused_speedup_vs_reference_cpu": C1_REFERENCE_MS[name] / (fused.wall_seconds * 1e3)}
+                         "fused_speedup_vs_reference_cpu": C1_REFERENCE_MS[name] / (fused.wall_seconds * 1e3),
+                         "graph_wall_ms": graphed.wall_seconds * 1e3,
+                         "graph_speedup_vs_reference_cpu": C1_REFERENCE_MS[name] / (graphed.wall_seconds * 1e3)}
     finally:
         shutil.rmtree(scratch, ignore_errors=True)
     return out

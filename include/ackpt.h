@@ -275,6 +275,14 @@ ACKPT_API int ackpt_engine_set_fusion(ackpt_engine* engine, int32_t fuse_advance
 /* Time every k-th forward and backward launch with a CUDA event pair on the
  * compute stream (0 = off).  Takes effect at the next prepare. */
 ACKPT_API int ackpt_engine_set_kernel_sampling(ackpt_engine* engine, int64_t every);
+/* CUDA-graph mode (default off): ackpt_engine_run captures a pass into a CUDA
+ * graph on the second run with the same buffers (the first runs eagerly and
+ * performs every first-use allocation) and replays it with one launch while
+ * the plan, fusion, prefetch order and buffers stay the same.  Counters come
+ * from the captured pass; times from its event nodes.  Not with the timeline
+ * or kernel sampling on.  For launch-bound passes (per-step contract, small
+ * states). */
+ACKPT_API int ackpt_engine_set_graph(ackpt_engine* engine, int32_t on);
 /* Mirrors CKPT_DISABLE_PREFETCH=1 (runtime.py:302): -1 read the env var at run. */
 ACKPT_API int ackpt_engine_set_prefetch(ackpt_engine* engine, int32_t prefetch);
 /* One forward/backward pass (runtime.py:339-381).  seed may be NULL when the

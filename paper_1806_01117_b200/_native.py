@@ -181,6 +181,7 @@ _SIGS = {
     "ackpt_engine_calibrate": ([_vp, _vp, C.c_int64, _vp, _dp, _dp, _dp], C.c_int),
     "ackpt_engine_interval": ([_vp], C.c_int64),
     "ackpt_engine_set_timeline": ([_vp, C.c_int32], C.c_int),
+    "ackpt_engine_set_graph": ([_vp, C.c_int32], C.c_int),
     "ackpt_engine_timeline": ([_vp, C.POINTER(TimelineEvent), C.c_int64, _i64p], C.c_int),
     "ackpt_crc32c": ([_vp, C.c_int64, C.c_uint32], C.c_uint32),
 }

@@ -47,6 +47,8 @@ int tier_ticket_status(ackpt_tier* t, ackpt_ticket id, std::string* msg);
 int tier_async_status(ackpt_tier* t, ackpt_ticket id, std::string* msg);
 void tier_retire(ackpt_tier* t, ackpt_ticket id);
 void tier_set_timing(ackpt_tier* t, bool on);
+void tier_reset_async(ackpt_tier* t, ackpt_ticket id);
+void tier_quiesce(ackpt_tier* t);
 bool tier_ticket_times(ackpt_tier* t, ackpt_ticket id, cudaEvent_t* t0, cudaEvent_t* t1);
 int64_t tier_slot_bytes(const ackpt_tier* t);
 cudaStream_t tier_d2h(const ackpt_tier* t);
@@ -85,6 +87,24 @@ struct ackpt_engine {
   int64_t sample_every = 0;
   int timeline = 0;                               // record a measured event timeline
   std::vector<ackpt_timeline_event> timeline_out;  // of the last run
+  // CUDA-graph mode (ackpt_engine_set_graph): a pass captured once and replayed
+  struct Graph {
+    bool pending = false;  // an eager run with these buffers happened: capture next time
+    bool prefetch = true;  // the prefetch order the pass was enqueued with
+    const void* init = nullptr;
+    const void* seed = nullptr;
+    void* out = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    ackpt_stats st{};  // host-side counters of the captured pass
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> stall_pairs;
+    std::vector<ackpt_ticket> issued;
+  };
+  int graph = 0;
+  Graph g;
+  void drop_graph() {
+    if (g.exec) cudaGraphExecDestroy(g.exec);
+    g = Graph{};
+  }
 };
 
 namespace ackpt {
@@ -311,14 +331,17 @@ struct Run {
     if (rc != ACKPT_OK) fail(rc, msg);
     cudaEvent_t done = tier_ticket_event(E->tier, t);
     cudaEvent_t before = timing_event(), after = timing_event();
-    ACKPT_CUDA_CHECK(cudaEventRecord(before, s));
+    // under graph capture these are event-record nodes (re-recorded on replay)
+    const unsigned rf = capturing ? cudaEventRecordExternal : cudaEventRecordDefault;
+    ACKPT_CUDA_CHECK(cudaEventRecordWithFlags(before, s, rf));
     if (done) ACKPT_CUDA_CHECK(cudaStreamWaitEvent(s, done, 0));
-    ACKPT_CUDA_CHECK(cudaEventRecord(after, s));
+    ACKPT_CUDA_CHECK(cudaEventRecordWithFlags(after, s, rf));
     stall_pairs.emplace_back(before, after);
     if (E->timeline) spans.push_back({ACKPT_EV_STALL, at_step, at_step, before, after});
   }
 
   std::vector<ackpt_ticket> issued;  // checked for file-stage errors after the run
+  bool capturing = false;            // enqueued under CUDA-graph stream capture
 
   ackpt_ticket begin_store(int64_t key, int state) {
     ackpt_ticket t = -1;
@@ -580,31 +603,11 @@ SegPlan make_plan(std::vector<Action>&& acts) {
 
 enum class Mode { kFull, kForwardSweep, kBackwardSweep };
 
-void run_impl(ackpt_engine* E, Mode mode, const void* initial_state, const void* seed,
-              void* adjoint_out, void* final_state, ackpt_stats* stats, cudaStream_t caller) {
-  if (!E->prepared) fail(ACKPT_VALUE_ERROR, "engine not prepared");
+// The stream work of one pass on E->compute (between ev_start and ev_end).
+void enqueue_pass(ackpt_engine* E, Run& r, Mode mode, void* final_state) {
   const bool ms = E->strategy == ACKPT_MULTISTAGE && !E->fallback;
-  if (mode != Mode::kFull && !ms)
-    fail(ACKPT_VALUE_ERROR, "fallback plans have no Level-2 phase; use execute()");  // runtime.py:395-396
-  if (mode == Mode::kFull && !adjoint_out) fail(ACKPT_VALUE_ERROR, "adjoint_out is required");
-  if (mode == Mode::kBackwardSweep && !seed) fail(ACKPT_VALUE_ERROR, "seed is required");
-
-  Run r(E, false, E->compute);
-  r.ext = initial_state;
-  r.seed_bytes = seed;
-  r.adj[0] = adjoint_out;
-  r.adj[1] = E->adj_internal;
-  if (mode == Mode::kForwardSweep) {
-    r.adj[0] = E->adj_internal;  // seed computed at step n is discarded
-    r.adj[1] = E->adj_internal;
-  }
-
-  // Order after the caller's stream, then time on the engine's stream.
-  ACKPT_CUDA_CHECK(cudaEventRecord(E->ev_sync, caller));
-  ACKPT_CUDA_CHECK(cudaStreamWaitEvent(E->compute, E->ev_sync, 0));
-  const auto t0 = std::chrono::steady_clock::now();
-  ACKPT_CUDA_CHECK(cudaEventRecord(E->ev_start, E->compute));
-
+  // a captured pass is bracketed outside the graph, around its launch
+  if (!r.capturing) ACKPT_CUDA_CHECK(cudaEventRecord(E->ev_start, E->compute));
   if (mode == Mode::kFull) {
     if (ms) {
       int last = r.multistage_forward(kExt);
@@ -623,50 +626,127 @@ void run_impl(ackpt_engine* E, Mode mode, const void* initial_state, const void*
     r.release(last);
   } else {
     r.a = (E->n % 2 == 0) ? 0 : 1;
-    ACKPT_CUDA_CHECK(cudaMemcpyAsync(r.adj[r.a], seed, size_t(E->S), cudaMemcpyDeviceToDevice,
+    ACKPT_CUDA_CHECK(cudaMemcpyAsync(r.adj[r.a], r.seed_bytes, size_t(E->S), cudaMemcpyDeviceToDevice,
                                      E->compute));
     r.seeded = true;
     r.multistage_backward();
   }
-
   // Per-step runs end with the adjoint in adj[0] (seed parity); fused reverse
   // runs swap once per launch, so the result may sit in the internal buffer.
   if (mode != Mode::kForwardSweep && r.a != 0)
     ACKPT_CUDA_CHECK(cudaMemcpyAsync(r.adj[0], r.adj[r.a], size_t(E->S), cudaMemcpyDeviceToDevice,
                                      E->compute));
-  ACKPT_CUDA_CHECK(cudaEventRecord(E->ev_end, E->compute));
+  if (!r.capturing) ACKPT_CUDA_CHECK(cudaEventRecord(E->ev_end, E->compute));
+}
+
+double elapsed_s(cudaEvent_t a, cudaEvent_t b) {
+  float msv = 0.f;
+  ACKPT_CUDA_CHECK(cudaEventElapsedTime(&msv, a, b));
+  return double(msv) * 1e-3;
+}
+
+void run_impl(ackpt_engine* E, Mode mode, const void* initial_state, const void* seed,
+              void* adjoint_out, void* final_state, ackpt_stats* stats, cudaStream_t caller) {
+  if (!E->prepared) fail(ACKPT_VALUE_ERROR, "engine not prepared");
+  const bool ms = E->strategy == ACKPT_MULTISTAGE && !E->fallback;
+  if (mode != Mode::kFull && !ms)
+    fail(ACKPT_VALUE_ERROR, "fallback plans have no Level-2 phase; use execute()");  // runtime.py:395-396
+  if (mode == Mode::kFull && !adjoint_out) fail(ACKPT_VALUE_ERROR, "adjoint_out is required");
+  if (mode == Mode::kBackwardSweep && !seed) fail(ACKPT_VALUE_ERROR, "seed is required");
+
+  // CUDA-graph mode: replay a captured pass when the buffers match; capture
+  // on the second run with the same buffers (the first, eager one performs
+  // every first-use allocation, which a capture must not contain).
+  const bool graphable = E->graph && mode == Mode::kFull && !E->timeline && E->sample_every == 0;
+  auto& G = E->g;
+  const bool pf_now = E->prefetch < 0 ? env_prefetch() : E->prefetch != 0;
+  const bool same = G.init == initial_state && G.seed == seed && G.out == adjoint_out && G.prefetch == pf_now;
+  if (!graphable || !same) E->drop_graph();
+  const bool replay = graphable && G.exec;
+  const bool capture = graphable && !G.exec && G.pending;
+
+  // Order after the caller's stream, then time on the engine's stream.
+  ACKPT_CUDA_CHECK(cudaEventRecord(E->ev_sync, caller));
+  ACKPT_CUDA_CHECK(cudaStreamWaitEvent(E->compute, E->ev_sync, 0));
+
+  Run r(E, false, E->compute);
+  r.ext = initial_state;
+  r.seed_bytes = seed;
+  r.adj[0] = adjoint_out;
+  r.adj[1] = E->adj_internal;
+  if (mode == Mode::kForwardSweep) {
+    r.adj[0] = E->adj_internal;  // seed computed at step n is discarded
+    r.adj[1] = E->adj_internal;
+  }
+  auto t0 = std::chrono::steady_clock::now();
+  if (replay) {
+    for (ackpt_ticket tk : G.issued) tier_reset_async(E->tier, tk);
+    ACKPT_CUDA_CHECK(cudaEventRecord(E->ev_start, E->compute));
+    ACKPT_CUDA_CHECK(cudaGraphLaunch(G.exec, E->compute));
+    ACKPT_CUDA_CHECK(cudaEventRecord(E->ev_end, E->compute));
+  } else if (capture) {
+    r.capturing = true;
+    if (E->tier) tier_quiesce(E->tier);
+    cudaGraph_t graph = nullptr;
+    ACKPT_CUDA_CHECK(cudaStreamBeginCapture(E->compute, cudaStreamCaptureModeRelaxed));
+    try {
+      enqueue_pass(E, r, mode, final_state);
+    } catch (...) {
+      cudaStreamEndCapture(E->compute, &graph);
+      if (graph) cudaGraphDestroy(graph);
+      E->drop_graph();
+      throw;
+    }
+    ACKPT_CUDA_CHECK(cudaStreamEndCapture(E->compute, &graph));
+    const cudaError_t ie = cudaGraphInstantiate(&G.exec, graph, 0);
+    cudaGraphDestroy(graph);
+    if (ie != cudaSuccess) fail(ACKPT_CUDA_ERROR, std::string("graph instantiate: ") + cudaGetErrorString(ie));
+    r.finish_stats();
+    G.st = r.st;
+    G.stall_pairs = r.stall_pairs;
+    G.issued = r.issued;
+    t0 = std::chrono::steady_clock::now();
+    ACKPT_CUDA_CHECK(cudaEventRecord(E->ev_start, E->compute));
+    ACKPT_CUDA_CHECK(cudaGraphLaunch(G.exec, E->compute));
+    ACKPT_CUDA_CHECK(cudaEventRecord(E->ev_end, E->compute));
+  } else {
+    enqueue_pass(E, r, mode, final_state);
+    if (graphable) {  // remember the buffers: the next identical run is captured
+      G.pending = true;
+      G.prefetch = pf_now;
+      G.init = initial_state;
+      G.seed = seed;
+      G.out = adjoint_out;
+    }
+  }
+  const bool graphed = replay || capture;
   const auto t_enq = std::chrono::steady_clock::now();
   ACKPT_CUDA_CHECK(cudaEventSynchronize(E->ev_end));
   const auto t1 = std::chrono::steady_clock::now();
   ACKPT_CUDA_CHECK(cudaStreamWaitEvent(caller, E->ev_end, 0));
-  for (ackpt_ticket tk : r.issued) {  // file-stage I/O errors surface once the run drained
+  for (ackpt_ticket tk : graphed ? G.issued : r.issued) {  // file-stage I/O errors surface once the run drained
     std::string msg;
     const int rc = tier_async_status(E->tier, tk, &msg);
     if (rc != ACKPT_OK) fail(rc, msg);
   }
-  if (mode == Mode::kFull && !r.seeded)
-    fail(ACKPT_EXECUTION_ERROR, "execution finished without producing an adjoint");  // runtime.py:379-380
-
-  r.finish_stats();
+  if (graphed) {
+    if (E->tier) tier_quiesce(E->tier);
+    r.st = G.st;
+    r.stall_pairs = G.stall_pairs;
+  } else {
+    if (mode == Mode::kFull && !r.seeded)
+      fail(ACKPT_EXECUTION_ERROR, "execution finished without producing an adjoint");  // runtime.py:379-380
+    r.finish_stats();
+  }
   r.st.wall_seconds = std::chrono::duration<double>(t1 - t0).count();
   r.st.host_enqueue_seconds = std::chrono::duration<double>(t_enq - t0).count();
-  float ms_gpu = 0.f;
-  ACKPT_CUDA_CHECK(cudaEventElapsedTime(&ms_gpu, E->ev_start, E->ev_end));
-  r.st.gpu_seconds = double(ms_gpu) * 1e-3;
+  r.st.gpu_seconds = elapsed_s(E->ev_start, E->ev_end);
   double stall = 0.0;
-  for (auto& pr : r.stall_pairs) {
-    float msv = 0.f;
-    ACKPT_CUDA_CHECK(cudaEventElapsedTime(&msv, pr.first, pr.second));
-    stall += std::max(0.0, double(msv) * 1e-3);
-  }
+  for (auto& pr : r.stall_pairs) stall += std::max(0.0, elapsed_s(pr.first, pr.second));
   r.st.stall_seconds = stall;
   auto sum_pairs = [](const std::vector<std::pair<cudaEvent_t, cudaEvent_t>>& v) {
     double acc = 0.0;
-    for (auto& pr : v) {
-      float msv = 0.f;
-      ACKPT_CUDA_CHECK(cudaEventElapsedTime(&msv, pr.first, pr.second));
-      acc += double(msv) * 1e-3;
-    }
+    for (auto& pr : v) acc += elapsed_s(pr.first, pr.second);
     return acc;
   };
   r.st.fwd_sample_seconds = sum_pairs(r.fwd_pairs);
@@ -675,17 +755,13 @@ void run_impl(ackpt_engine* E, Mode mode, const void* initial_state, const void*
   r.st.bwd_samples = int64_t(r.bwd_pairs.size());
   E->timeline_out.clear();
   if (E->timeline) {
-    auto since = [&](cudaEvent_t ev) {
-      float msv = 0.f;
-      ACKPT_CUDA_CHECK(cudaEventElapsedTime(&msv, E->ev_start, ev));
-      return double(msv) * 1e-3;
-    };
+    auto since = [&](cudaEvent_t ev) { return elapsed_s(E->ev_start, ev); };
     for (const auto& sp : r.spans)
       E->timeline_out.push_back({sp.kind, ACKPT_LANE_COMPUTE, sp.from, sp.to, since(sp.e0), since(sp.e1)});
     for (const auto& x : r.xfers) {
-      cudaEvent_t t0 = nullptr, t1 = nullptr;
-      if (tier_ticket_times(E->tier, x.id, &t0, &t1))
-        E->timeline_out.push_back({x.kind, ACKPT_LANE_TRANSFER, x.key, x.key, since(t0), since(t1)});
+      cudaEvent_t t0e = nullptr, t1e = nullptr;
+      if (tier_ticket_times(E->tier, x.id, &t0e, &t1e))
+        E->timeline_out.push_back({x.kind, ACKPT_LANE_TRANSFER, x.key, x.key, since(t0e), since(t1e)});
     }
     std::stable_sort(E->timeline_out.begin(), E->timeline_out.end(),
                      [](const ackpt_timeline_event& a, const ackpt_timeline_event& b) { return a.start < b.start; });
@@ -731,6 +807,7 @@ ACKPT_API int ackpt_engine_destroy(ackpt_engine* e) {
   return ackpt::guard([&] {
     if (!e) return;
     if (e->compute) cudaStreamSynchronize(e->compute);
+    e->drop_graph();
     for (auto s : e->slabs) cudaFree(s);
     if (e->adj_internal) cudaFree(e->adj_internal);
     for (auto ev : e->timing) cudaEventDestroy(ev);
@@ -747,6 +824,7 @@ ACKPT_API int ackpt_engine_prepare(ackpt_engine* E, int32_t strategy, int64_t sl
   return ackpt::guard([&] {
     using namespace ackpt;
     E->prepared = false;
+    E->drop_graph();
     E->strategy = strategy;
     E->slots = slots;
     E->interval = 0;
@@ -807,6 +885,7 @@ ACKPT_API int ackpt_engine_prepare(ackpt_engine* E, int32_t strategy, int64_t sl
 }
 
 ACKPT_API int ackpt_engine_set_fusion(ackpt_engine* e, int32_t fuse_advance) {
+  if (e->fuse != fuse_advance) e->drop_graph();
   e->fuse = fuse_advance;
   return ACKPT_OK;
 }
@@ -814,6 +893,12 @@ ACKPT_API int ackpt_engine_set_fusion(ackpt_engine* e, int32_t fuse_advance) {
 ACKPT_API int ackpt_engine_set_kernel_sampling(ackpt_engine* e, int64_t every) {
   e->sample_every = every < 0 ? 0 : every;
   e->prepared = false;  // the timing-event pool is sized by the next prepare
+  return ACKPT_OK;
+}
+
+ACKPT_API int ackpt_engine_set_graph(ackpt_engine* e, int32_t on) {
+  if (!on) e->drop_graph();
+  e->graph = on ? 1 : 0;
   return ACKPT_OK;
 }
 
@@ -832,6 +917,7 @@ ACKPT_API int ackpt_engine_timeline(const ackpt_engine* e, ackpt_timeline_event*
 }
 
 ACKPT_API int ackpt_engine_set_prefetch(ackpt_engine* e, int32_t prefetch) {
+  if (e->prefetch != prefetch) e->drop_graph();
   e->prefetch = prefetch;
   return ACKPT_OK;
 }

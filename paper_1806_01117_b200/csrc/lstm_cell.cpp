@@ -161,6 +161,14 @@ ACKPT_API int ackpt_lstm_create(int32_t d, int64_t n_steps, int64_t batch, int32
     ACKPT_CUDA_CHECK(cudaMalloc(&c->d_xb, c->xb_t.size()));
     ACKPT_CUDA_CHECK(cudaMemcpy(c->d_wh, c->wh_t.data(), c->wh_t.size(), cudaMemcpyHostToDevice));
     ACKPT_CUDA_CHECK(cudaMemcpy(c->d_xb, c->xb_t.data(), c->xb_t.size(), cudaMemcpyHostToDevice));
+    {  // W_h transposed ([k][n] = W_h[n][k]): coalesced gate rows when W is read from global memory
+      const size_t es = size_t(c->esize), R = 4 * D;
+      std::vector<unsigned char> wt(c->wh_t.size());
+      for (size_t r = 0; r < R; ++r)
+        for (size_t k = 0; k < D; ++k) std::memcpy(&wt[(k * R + r) * es], &c->wh_t[(r * D + k) * es], es);
+      ACKPT_CUDA_CHECK(cudaMalloc(&c->d_wht, wt.size()));
+      ACKPT_CUDA_CHECK(cudaMemcpy(c->d_wht, wt.data(), wt.size(), cudaMemcpyHostToDevice));
+    }
     if (dtype == ACKPT_F32 && d <= 32) {
       // per-gate pre-scaled projections for the fused fp32 advance (lstm_f32_math.cuh)
       const float scale[4] = {-1.4426950408889634f, -1.4426950408889634f, -1.4426950408889634f,
@@ -193,6 +201,7 @@ ACKPT_API int ackpt_lstm_destroy(ackpt_lstm* cell) {
   return ackpt::guard([&] {
     if (!cell) return;
     if (cell->d_wh) cudaFree(cell->d_wh);
+    if (cell->d_wht) cudaFree(cell->d_wht);
     if (cell->d_xb) cudaFree(cell->d_xb);
     if (cell->d_xbs) cudaFree(cell->d_xbs);
     if (cell->d_frag_hm) cudaFree(cell->d_frag_hm);
@@ -211,7 +220,10 @@ ACKPT_API int ackpt_lstm_forward(const ackpt_lstm* cell, int64_t step, const voi
   return ackpt::guard([&] {
     ackpt::check_step(cell, step);
     auto s = static_cast<cudaStream_t>(stream);
-    if (ackpt::tma_ok(cell, {state_in, state_out})) {
+    if (ackpt::sb_first(cell)) {
+      if (cell->dtype == ACKPT_F32) ackpt::sb_forward<float>(cell, step, 1, state_in, state_out, nullptr, s);
+      else ackpt::sb_forward<double>(cell, step, 1, state_in, state_out, nullptr, s);
+    } else if (ackpt::tma_ok(cell, {state_in, state_out})) {
       auto i = static_cast<const float*>(state_in);
       auto o = static_cast<float*>(state_out);
       if (ackpt::variant() == ackpt::Variant::kTma128) ackpt::tma_launch<8, 0, 128, 4>(cell, step, i, nullptr, o, s);
@@ -248,7 +260,11 @@ ACKPT_API int ackpt_lstm_advance(const ackpt_lstm* cell, int64_t from_step, int6
     if (from_step < 0 || to_step > cell->n || from_step >= to_step)
       ackpt::fail(ACKPT_VALUE_ERROR, "advance range out of bounds");
     auto s = static_cast<cudaStream_t>(stream);
-    if (ackpt::f32_fast(cell, {state_in, state_out})) {
+    if (ackpt::sb_first(cell)) {
+      const int cnt = int(to_step - from_step);
+      if (cell->dtype == ACKPT_F32) ackpt::sb_forward<float>(cell, from_step, cnt, state_in, state_out, nullptr, s);
+      else ackpt::sb_forward<double>(cell, from_step, cnt, state_in, state_out, nullptr, s);
+    } else if (ackpt::f32_fast(cell, {state_in, state_out})) {
       auto i = static_cast<const float*>(state_in);
       auto o = static_cast<float*>(state_out);
       if (cell->d == 8 && ackpt::hm_on()) ackpt::hm_advance(cell, from_step, int(to_step - from_step), i, o, s);
@@ -279,7 +295,10 @@ ACKPT_API int ackpt_lstm_backward(const ackpt_lstm* cell, int64_t step, const vo
   return ackpt::guard([&] {
     ackpt::check_step(cell, step);
     auto s = static_cast<cudaStream_t>(stream);
-    if (ackpt::tma_ok(cell, {state, adjoint_in, adjoint_out})) {
+    if (ackpt::sb_first(cell)) {
+      if (cell->dtype == ACKPT_F32) ackpt::sb_reverse<float>(cell, step, 1, &state, adjoint_in, adjoint_out, s);
+      else ackpt::sb_reverse<double>(cell, step, 1, &state, adjoint_in, adjoint_out, s);
+    } else if (ackpt::tma_ok(cell, {state, adjoint_in, adjoint_out})) {
       auto x = static_cast<const float*>(state);
       auto a = static_cast<const float*>(adjoint_in);
       auto o = static_cast<float*>(adjoint_out);
@@ -326,7 +345,7 @@ ACKPT_API int ackpt_lstm_forward_many(const ackpt_lstm* cell, int64_t from_step,
     auto s = static_cast<cudaStream_t>(stream);
     std::vector<const void*> all{state_in};
     for (int64_t i = 0; i < count; ++i) all.push_back(states_out[i]);
-    bool fast = ackpt::f32_fast(cell, {});
+    bool fast = !ackpt::sb_first(cell) && ackpt::f32_fast(cell, {});
     for (const void* p : all) fast = fast && !(reinterpret_cast<uintptr_t>(p) & 7u);
     if (fast) {
       auto in = static_cast<const float*>(state_in);
@@ -338,7 +357,7 @@ ACKPT_API int ackpt_lstm_forward_many(const ackpt_lstm* cell, int64_t from_step,
       ackpt::check_launch();
       return;
     }
-    bool tcd = ackpt::tcd_ok(cell, {});
+    bool tcd = !ackpt::sb_first(cell) && ackpt::tcd_ok(cell, {});
     for (const void* q : all) tcd = tcd && !(reinterpret_cast<uintptr_t>(q) & 3u);
     if (tcd) {
       ackpt::tcd_forward(cell, from_step, int(count), static_cast<const float*>(state_in), nullptr,
@@ -368,7 +387,8 @@ ACKPT_API int ackpt_lstm_backward_many(const ackpt_lstm* cell, int64_t from_step
     if (count < 1 || count > ACKPT_MAX_FUSED) ackpt::fail(ACKPT_VALUE_ERROR, "count must be in [1, 64]");
     if (from_step < 0 || from_step + count > cell->n) ackpt::fail(ACKPT_VALUE_ERROR, "steps out of range");
     auto s = static_cast<cudaStream_t>(stream);
-    bool tcd = ackpt::tcd_ok(cell, {adjoint_in, adjoint_out});
+    const bool sbf = ackpt::sb_first(cell);
+    bool tcd = !sbf && ackpt::tcd_ok(cell, {adjoint_in, adjoint_out});
     for (int64_t i = 0; i < count; ++i) tcd = tcd && !(reinterpret_cast<uintptr_t>(states[i]) & 3u);
     if (tcd) {
       ackpt::tcd_reverse(cell, from_step, int(count), reinterpret_cast<const float* const*>(states),
@@ -376,7 +396,7 @@ ACKPT_API int ackpt_lstm_backward_many(const ackpt_lstm* cell, int64_t from_step
       ackpt::check_launch();
       return;
     }
-    bool fast = ackpt::f32_fast(cell, {adjoint_in, adjoint_out});
+    bool fast = !sbf && ackpt::f32_fast(cell, {adjoint_in, adjoint_out});
     for (int64_t i = 0; i < count; ++i) fast = fast && !(reinterpret_cast<uintptr_t>(states[i]) & 7u);
     if (!fast && ackpt::sb_ok(cell)) {
       if (cell->dtype == ACKPT_F32) ackpt::sb_reverse<float>(cell, from_step, int(count), states, adjoint_in, adjoint_out, s);
@@ -385,7 +405,7 @@ ACKPT_API int ackpt_lstm_backward_many(const ackpt_lstm* cell, int64_t from_step
       return;
     }
     if (!fast)
-      ackpt::fail(ACKPT_VALUE_ERROR, "fused backward needs a fused kernel (fp32 d in {4, 8, 16, 32} or B <= 1024)");
+      ackpt::fail(ACKPT_VALUE_ERROR, "fused backward needs a fused kernel (fp32 d in {4, 8, 16, 32} or the CTA-per-sequence kernels)");
     auto sp = reinterpret_cast<const float* const*>(states);
     auto ai = static_cast<const float*>(adjoint_in);
     auto ao = static_cast<float*>(adjoint_out);

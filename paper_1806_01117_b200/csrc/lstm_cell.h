@@ -18,6 +18,7 @@ struct ackpt_lstm {
   std::vector<double> wh64, xb64, target64;         // float64 master copies
   std::vector<unsigned char> wh_t, xb_t, target_t;  // rounded to the cell dtype
   void* d_wh = nullptr;                             // 4 x d x d, dtype
+  void* d_wht = nullptr;                            // d x 4d (W_h transposed), dtype
   void* d_xb = nullptr;                             // n x 4 x d, dtype
   void* d_xbs = nullptr;  // n x 4 x d fp32, pre-scaled per gate (fp32 fast path, d <= 16)
   void* d_frag_hm = nullptr;  // d = 8 fp32: per-lane mma.sync B fragments (lstm_f32_hm.cu)
@@ -40,7 +41,8 @@ struct TargetParams {
 };
 
 constexpr int kMaxD = 128;
-constexpr int64_t kSmallBatch = 1024;  // CTA-per-sequence kernels at or below this batch (lstm_small.cu)
+constexpr int64_t kSmallBatch = (int64_t(1) << 31) - 1;// CTA-per-sequence kernels (lstm_small.cu): grid-x limit
+constexpr int64_t kSbFirstBatch = 2048;   // ... preferred over the batch-tiled fp32 kernels up to this one
 
 // fp32 fast path, d in {4, 8}: float2-paired kernels (lstm_f32_d*.cu).
 template <int D>
@@ -74,6 +76,7 @@ void hm_backward_many(const ackpt_lstm* c, int64_t from, int count, const float*
 // Small-batch kernels (B <= kSmallBatch, any d, f32 / f64): one CTA per
 // sequence, one thread per gate row (lstm_small.cu); per-step = count 1.
 bool sb_ok(const ackpt_lstm* c);
+bool sb_first(const ackpt_lstm* c);
 template <typename T>
 void sb_forward(const ackpt_lstm* c, int64_t from, int count, const void* in, void* out, void* const* outs,
                 cudaStream_t s);

@@ -3,17 +3,23 @@
 // image, lstm.py:99-107), where one thread per sequence would run all 4 d^2
 // products serially.  Here a CTA owns one sequence and its 4d threads own
 // the gate rows:
-//   phase 1  thread n = gate row (g, j): a[n] = xb_k[n] + sum_k W[n][k] h[k]
+//   phase 1  thread n = gate row (g, j): a[n] = act_g(xb_k[n] + sum_k W[n][k] h[k])
+//            (the gate activation is applied by the row's own thread)
 //   phase 2  thread j < d: the activations, c' and h' (forward), or the
 //            gate adjoints da[g][j] and dc (reverse, lstm.py:141-151)
 //   phase 3  (reverse) thread m < d: dh[m] = sum_{g,j} W[g][j][m] da[g][j]
 // with __syncthreads between phases and the state in shared memory across
-// steps, so a fused Advance / TapeForward / Reverse run is one launch.  Same
+// steps, so a fused Advance / TapeForward / Reverse run is one launch.  The
+// shared copy of W has row stride d+1 so both the row-per-thread gate product
+// and the column-per-thread transposed product are bank-conflict free, and the
+// next step's bias (and, in reverse, state) is loaded during the current step
+// so no global-load latency sits on the step's dependency chain.  Same
 // formulas and math-library calls as the generic kernels (lstm_generic.cu),
 // so float64 results stay within 1e-12 of the reference.
 #include <cuda_runtime.h>
 
 #include <cmath>
+#include <cstdlib>
 
 #include "lstm_cell.h"
 
@@ -25,54 +31,75 @@ __device__ __forceinline__ double sigmoid(double z) { return 1.0 / (1.0 + exp(-z
 __device__ __forceinline__ float tanh_(float z) { return tanhf(z); }
 __device__ __forceinline__ double tanh_(double z) { return tanh(z); }
 
+// gates f, i, o: sigmoid; candidate g: tanh (lstm.py:120-126)
+template <typename T>
+__device__ __forceinline__ T act(T z, bool cand) { return cand ? tanh_(z) : sigmoid(z); }
+
 struct Ptrs {
   const void* p[ACKPT_MAX_FUSED];
 };
 
-// a[n] = xb[n] + W[n] . h for this thread's gate row n (n < 4d); W is the
-// CTA's shared-memory copy when it fits (else global).
+// Where a CTA reads W from: W[n][k] = g[n * grs + k * gcs] for the gate rows
+// and W[r][m] = p[r * prs + m] for the transposed product.  Shared copy with
+// row stride d+1 when it fits (both products conflict-free); else global
+// memory, the gate rows from the transposed copy (coalesced across n) and the
+// product from the row-major one (coalesced across m).
 template <typename T>
-__device__ __forceinline__ T gate_row(const T* w_all, const T* __restrict__ xb, const T* h, int d, int n) {
-  const T* w = w_all + int64_t(n) * d;
-  T acc = __ldg(xb + n);
+struct WView {
+  const T* g;
+  int grs, gcs;
+  const T* p;
+  int prs;
+};
+
+// a[n] = xb + W[n] . h for this thread's gate row n (n < 4d)
+template <typename T>
+__device__ __forceinline__ T gate_row(const WView<T>& w, T xb, const T* h, int d, int n) {
+  const T* row = w.g + int64_t(n) * w.grs;
+  T acc = xb;
 #pragma unroll 4
-  for (int k = 0; k < d; ++k) acc = fma(w[k], h[k], acc);
+  for (int k = 0; k < d; ++k) acc = fma(row[int64_t(k) * w.gcs], h[k], acc);
   return acc;
 }
 
-// W (4 d x d) into shared memory when it fits next to the state: returns the
-// pointer the gate / transposed products read.
 template <typename T>
-__device__ __forceinline__ const T* stage_w(T* ws, bool in_smem, const T* __restrict__ wh, int d) {
-  if (!in_smem) return wh;
-  for (int i = threadIdx.x; i < 4 * d * d; i += blockDim.x) ws[i] = __ldg(wh + i);
+__device__ __forceinline__ WView<T> stage_w(T* ws, bool in_smem, const T* __restrict__ wh,
+                                            const T* __restrict__ wht, int d) {
+  if (!in_smem) return {wht, 1, 4 * d, wh, d};
+  // blockDim = 4d: thread n copies column n % d of rows n / d + 4 t (coalesced reads)
+  const int r0 = int(threadIdx.x) / d, k = int(threadIdx.x) - r0 * d;
+#pragma unroll 8
+  for (int t = 0; t < d; ++t) ws[(r0 + 4 * t) * (d + 1) + k] = __ldg(wh + threadIdx.x + size_t(4 * d) * t);
   __syncthreads();
-  return ws;
+  return {ws, d + 1, 1, ws, d + 1};
 }
 
 // Forward over `count` steps from `from`.  tape != null: store every step's
 // state to tape[i]; otherwise the final state to `out`.
 template <typename T>
 __global__ void fwd(const T* __restrict__ in, T* __restrict__ out, int64_t B, int d, const T* __restrict__ wh,
-                    const T* __restrict__ xb_all, int64_t from, int count, bool tape, bool w_smem,
+                    const T* __restrict__ wht, const T* __restrict__ xb_all, int64_t from, int count, bool tape, bool w_smem,
                     const __grid_constant__ Ptrs outs) {
   extern __shared__ __align__(16) unsigned char raw[];
   T* h = reinterpret_cast<T*>(raw);
   T* c = h + d;
   T* a = c + d;  // 4d
-  const T* w = stage_w(a + 4 * d, w_smem, wh, d);
+  const WView<T> w = stage_w(a + 4 * d, w_smem, wh, wht, d);
   const int64_t b = blockIdx.x;
   const int n = threadIdx.x;
   if (n < d) {
     h[n] = in[int64_t(n) * B + b];
     c[n] = in[int64_t(d + n) * B + b];
   }
+  T xb = __ldg(xb_all + from * 4 * d + n);
   __syncthreads();
   for (int i = 0; i < count; ++i) {
-    a[n] = gate_row(w, xb_all + (from + i) * 4 * d, h, d, n);
+    const T xb_next = i + 1 < count ? __ldg(xb_all + (from + i + 1) * 4 * d + n) : T(0);
+    a[n] = act(gate_row(w, xb, h, d, n), n >= 3 * d);
+    xb = xb_next;
     __syncthreads();
     if (n < d) {
-      const T f = sigmoid(a[n]), ig = sigmoid(a[d + n]), o = sigmoid(a[2 * d + n]), g = tanh_(a[3 * d + n]);
+      const T f = a[n], ig = a[d + n], o = a[2 * d + n], g = a[3 * d + n];
       const T cn = f * c[n] + ig * g;  // lstm.py:127
       c[n] = cn;
       h[n] = o * tanh_(cn);            // lstm.py:128
@@ -93,7 +120,7 @@ __global__ void fwd(const T* __restrict__ in, T* __restrict__ out, int64_t B, in
 // Reverse over steps from+count-1 .. from; states.p[i] is the state of step from+i.
 template <typename T>
 __global__ void rev(const T* __restrict__ adj_in, T* __restrict__ adj_out, int64_t B, int d, const T* __restrict__ wh,
-                    const T* __restrict__ xb_all, int64_t from, int count, bool w_smem,
+                    const T* __restrict__ wht, const T* __restrict__ xb_all, int64_t from, int count, bool w_smem,
                     const __grid_constant__ Ptrs states) {
   extern __shared__ __align__(16) unsigned char raw[];
   T* h = reinterpret_cast<T*>(raw);
@@ -102,24 +129,39 @@ __global__ void rev(const T* __restrict__ adj_in, T* __restrict__ adj_out, int64
   T* dc = dh + d;
   T* a = dc + d;      // 4d gate pre-activations, then the 4 per-gate partial dh
   T* da = a + 4 * d;  // 4d gate adjoints
-  const T* w = stage_w(da + 4 * d, w_smem, wh, d);
+  const WView<T> w = stage_w(da + 4 * d, w_smem, wh, wht, d);
   const int64_t b = blockIdx.x;
   const int n = threadIdx.x;
   if (n < d) {
     dh[n] = adj_in[int64_t(n) * B + b];
     dc[n] = adj_in[int64_t(d + n) * B + b];
   }
+  // step i's state and bias in registers, step i-1's loaded during step i
+  T hs = T(0), cs = T(0), xb = __ldg(xb_all + (from + count - 1) * 4 * d + n);
+  if (n < d) {
+    const T* st = static_cast<const T*>(states.p[count - 1]);
+    hs = st[int64_t(n) * B + b];
+    cs = st[int64_t(d + n) * B + b];
+  }
   for (int i = count - 1; i >= 0; --i) {
-    const T* st = static_cast<const T*>(states.p[i]);
     if (n < d) {
-      h[n] = st[int64_t(n) * B + b];
-      c[n] = st[int64_t(d + n) * B + b];
+      h[n] = hs;
+      c[n] = cs;
+    }
+    const T xb_i = xb;
+    if (i > 0) {
+      xb = __ldg(xb_all + (from + i - 1) * 4 * d + n);
+      if (n < d) {
+        const T* st = static_cast<const T*>(states.p[i - 1]);
+        hs = st[int64_t(n) * B + b];
+        cs = st[int64_t(d + n) * B + b];
+      }
     }
     __syncthreads();
-    a[n] = gate_row(w, xb_all + (from + i) * 4 * d, h, d, n);
+    a[n] = act(gate_row(w, xb_i, h, d, n), n >= 3 * d);
     __syncthreads();
     if (n < d) {
-      const T f = sigmoid(a[n]), ig = sigmoid(a[d + n]), o = sigmoid(a[2 * d + n]), g = tanh_(a[3 * d + n]);
+      const T f = a[n], ig = a[d + n], o = a[2 * d + n], g = a[3 * d + n];
       const T cn = f * c[n] + ig * g;
       const T t = tanh_(cn);
       const T dhn = dh[n];
@@ -133,11 +175,11 @@ __global__ void rev(const T* __restrict__ adj_in, T* __restrict__ adj_out, int64
     __syncthreads();
     {  // lstm.py:149-150: dh = sum_g W_g^T da_g; thread (g, m) sums gate g, then a fixed-order reduction
       const int g = n / d, m = n - g * d;
-      const T* wg = w + int64_t(g) * d * d + m;
+      const T* wg = w.p + int64_t(g) * d * w.prs + m;
       const T* dg = da + g * d;
       T acc = T(0);
 #pragma unroll 4
-      for (int j = 0; j < d; ++j) acc = fma(wg[int64_t(j) * d], dg[j], acc);
+      for (int j = 0; j < d; ++j) acc = fma(wg[int64_t(j) * w.prs], dg[j], acc);
       a[n] = acc;  // gate pre-activations are dead by now
     }
     __syncthreads();
@@ -152,7 +194,24 @@ __global__ void rev(const T* __restrict__ adj_in, T* __restrict__ adj_out, int64
 
 }  // namespace sb
 
-bool sb_ok(const ackpt_lstm* c) { return c->B <= kSmallBatch && c->d <= kMaxD; }
+bool sb_ok(const ackpt_lstm* c) {
+  static const int64_t max_b = [] {  // ACKPT_SB_MAX: probe override of the batch cap
+    const char* e = std::getenv("ACKPT_SB_MAX");
+    return e ? std::atoll(e) : int64_t(kSmallBatch);
+  }();
+  return c->B <= max_b && c->d <= kMaxD;
+}
+
+// Batches small enough that a CTA per sequence beats the batch-tiled fp32
+// kernels (whose 128/256-sequence tiles would run mostly empty): measured
+// crossover, overridable with ACKPT_SB_FIRST=<max batch>.
+bool sb_first(const ackpt_lstm* c) {
+  static const int64_t max_b = [] {
+    const char* e = std::getenv("ACKPT_SB_FIRST");
+    return e ? std::atoll(e) : int64_t(kSbFirstBatch);
+  }();
+  return c->B <= max_b && sb_ok(c);
+}
 
 // shared-memory budget of the small-batch kernels (W copied in when it fits)
 constexpr size_t kSmallWBytes = 160 * 1024;
@@ -163,13 +222,15 @@ void sb_forward(const ackpt_lstm* c, int64_t from, int count, const void* in, vo
   sb::Ptrs o{};
   if (outs)
     for (int i = 0; i < count; ++i) o.p[i] = outs[i];
-  const size_t base = size_t(6) * c->d * sizeof(T), wbytes = size_t(4) * c->d * c->d * sizeof(T);
-  const bool w_smem = count >= 8 && base + wbytes <= kSmallWBytes;  // amortised over >= 8 steps
+  const size_t base = size_t(6) * c->d * sizeof(T), wbytes = size_t(4) * c->d * (c->d + 1) * sizeof(T);
+  // staged even for one step: the row-per-thread product straight from global
+  // memory touches one cache line per thread per load (uncoalesced)
+  const bool w_smem = base + wbytes <= kSmallWBytes;
   const size_t smem = base + (w_smem ? wbytes : 0);
   if (smem > 48 * 1024) cudaFuncSetAttribute(sb::fwd<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
   sb::fwd<T><<<unsigned(c->B), unsigned(4 * c->d), smem, s>>>(
       static_cast<const T*>(in), static_cast<T*>(out), c->B, c->d, static_cast<const T*>(c->d_wh),
-      static_cast<const T*>(c->d_xb), from, count, outs != nullptr, w_smem, o);
+      static_cast<const T*>(c->d_wht), static_cast<const T*>(c->d_xb), from, count, outs != nullptr, w_smem, o);
 }
 
 template <typename T>
@@ -177,13 +238,15 @@ void sb_reverse(const ackpt_lstm* c, int64_t from, int count, const void* const*
                 void* adj_out, cudaStream_t s) {
   sb::Ptrs p{};
   for (int i = 0; i < count; ++i) p.p[i] = states[i];
-  const size_t base = size_t(12) * c->d * sizeof(T), wbytes = size_t(4) * c->d * c->d * sizeof(T);
-  const bool w_smem = count >= 8 && base + wbytes <= kSmallWBytes;  // amortised over >= 8 steps
+  const size_t base = size_t(12) * c->d * sizeof(T), wbytes = size_t(4) * c->d * (c->d + 1) * sizeof(T);
+  // staged even for one step: the row-per-thread product straight from global
+  // memory touches one cache line per thread per load (uncoalesced)
+  const bool w_smem = base + wbytes <= kSmallWBytes;
   const size_t smem = base + (w_smem ? wbytes : 0);
   if (smem > 48 * 1024) cudaFuncSetAttribute(sb::rev<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
   sb::rev<T><<<unsigned(c->B), unsigned(4 * c->d), smem, s>>>(
       static_cast<const T*>(adj_in), static_cast<T*>(adj_out), c->B, c->d, static_cast<const T*>(c->d_wh),
-      static_cast<const T*>(c->d_xb), from, count, w_smem, p);
+      static_cast<const T*>(c->d_wht), static_cast<const T*>(c->d_xb), from, count, w_smem, p);
 }
 
 template void sb_forward<float>(const ackpt_lstm*, int64_t, int, const void*, void*, void* const*, cudaStream_t);

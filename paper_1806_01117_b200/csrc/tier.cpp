@@ -437,6 +437,22 @@ int tier_ticket_status(ackpt_tier* t, ackpt_ticket id, std::string* msg) {
   if (msg) *msg = tk.msg;
   return tk.err;
 }
+// Clear a file-stage ticket's asynchronous status before a CUDA-graph replay
+// re-runs its host functions.
+void tier_reset_async(ackpt_tier* t, ackpt_ticket id) {
+  std::lock_guard<std::mutex> lk(t->mu);
+  TierTicket& tk = get_ticket(t, id);
+  if (tk.async) tk.async->err.store(ACKPT_OK, std::memory_order_release);
+}
+// Drain the copy streams and forget the per-key copy-ordering events, so no
+// stream wait crosses a CUDA-graph capture boundary (before a capture, after
+// a graphed run): the events last recorded inside a capture are graph nodes.
+void tier_quiesce(ackpt_tier* t) {
+  std::lock_guard<std::mutex> lk(t->mu);
+  ACKPT_CUDA_CHECK(cudaStreamSynchronize(t->d2h));
+  ACKPT_CUDA_CHECK(cudaStreamSynchronize(t->h2d));
+  for (auto& kv : t->keys) kv.second.fetched = false;
+}
 void tier_set_timing(ackpt_tier* t, bool on) {
   std::lock_guard<std::mutex> lk(t->mu);
   t->timing = on;

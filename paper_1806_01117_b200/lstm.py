@@ -358,11 +358,13 @@ def bench(
     dtype="f64",
     fuse: bool = False,
     timeline_path: Optional[str] = None,
+    graph: bool = False,
 ) -> BenchReport:
     """One forward/backward iteration timed as the minimum over ``runs``
     (lstm.py:219-254); batch=1/f64 reproduces the reference's workload.
     ``timeline_path``: also write the fastest run's measured event timeline
-    there (simulator JSON format; total = the compute stream's time)."""
+    there (simulator JSON format; total = the compute stream's time).
+    ``graph``: replay the pass as a captured CUDA graph (runtime.execute)."""
     cell = random_cell(d, n, seed)
     ops = operator_pair(cell, batch, dtype)
     if batch == 1 and _torch_dtype(dtype) == torch.float64:
@@ -374,7 +376,8 @@ def bench(
         best: Optional[ExecutionStats] = None
         adjoint = b""
         for _ in range(max(1, runs)):
-            adjoint, stats = execute(strategy, ops, state0, backend, fuse=fuse, timeline=timeline_path is not None)
+            adjoint, stats = execute(strategy, ops, state0, backend, fuse=fuse, timeline=timeline_path is not None,
+                                    graph=graph)
             if best is None or stats.wall_seconds < best.wall_seconds:
                 best = stats
         if timeline_path is not None:

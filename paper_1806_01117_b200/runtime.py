@@ -217,9 +217,19 @@ class _Engine:
 
     def __init__(self, op: N.Operator, owner=None):
         self.owner = owner
+        self.plan_key = None
+        self._stable = {}
         h = C.c_void_p()
         N.check(N.lib.ackpt_engine_create(C.byref(op), C.byref(h)))
         self.handle = h.value
+
+    def stable(self, name: str, like: torch.Tensor) -> torch.Tensor:
+        """Engine-owned device buffer shaped like `like`, reused across calls."""
+        buf = self._stable.get(name)
+        if buf is None or buf.shape != like.shape or buf.dtype != like.dtype or buf.device != like.device:
+            buf = torch.empty_like(like, memory_format=torch.contiguous_format)
+            self._stable[name] = buf
+        return buf
 
     def __del__(self):
         try:
@@ -353,6 +363,7 @@ def execute(
     fuse: bool = False,
     sample_kernels: int = 0,
     timeline: bool = False,
+    graph: bool = False,
 ):
     """One forward/backward pass; returns (step-0 adjoint, stats).
 
@@ -363,7 +374,11 @@ def execute(
     (runtime.py:355-363).  ``timeline=True`` also records the measured event
     timeline (``stats.timeline``: simulator.TimelineEvent list, seconds since
     the run's start; one compute event per launch) at two CUDA events per
-    launch -- a reporting mode, not for headline timing.
+    launch -- a reporting mode, not for headline timing.  ``graph=True``
+    replays the pass as a captured CUDA graph (captured on the second call
+    with the same plan; inputs and outputs go through engine-owned buffers):
+    for launch-bound passes such as the per-step contract on small states.
+    Native operator pairs only.
     """
     if nbytes_of(initial_state) != ops.state_size:
         raise SizeMismatch(
@@ -383,12 +398,26 @@ def execute(
     else:
         raise TypeError(f"unknown strategy {strategy!r}")
     engine, cb = _engine_for(ops)
-    N.check(N.lib.ackpt_engine_set_kernel_sampling(engine.handle, int(sample_kernels)))
-    N.check(N.lib.ackpt_engine_set_timeline(engine.handle, 1 if timeline else 0))
+    if graph and cb is not None:
+        raise ValueError("graph=True needs a native operator pair")
+    # fusion first (calibrate may have changed it), then re-plan only when the
+    # plan changed: a prepare drops a captured graph
     N.check(N.lib.ackpt_engine_set_fusion(engine.handle, 1 if fuse else 0))
-    _prepare(engine, code, slots, interval, tier)
-    state = _device_state(initial_state)
-    out = _output_like(initial_state)
+    plan_key = (code, slots, interval, tier, int(sample_kernels), bool(timeline), bool(fuse))
+    if getattr(engine, "plan_key", None) != plan_key:
+        N.check(N.lib.ackpt_engine_set_kernel_sampling(engine.handle, int(sample_kernels)))
+        N.check(N.lib.ackpt_engine_set_timeline(engine.handle, 1 if timeline else 0))
+        _prepare(engine, code, slots, interval, tier)
+        engine.plan_key = plan_key
+    N.check(N.lib.ackpt_engine_set_graph(engine.handle, 1 if graph else 0))
+    if graph:  # stable buffers: a captured graph holds their addresses
+        src = _device_state(initial_state)
+        state = engine.stable("in", src)
+        state.copy_(src)
+        out = engine.stable("out", _output_like(initial_state))
+    else:
+        state = _device_state(initial_state)
+        out = _output_like(initial_state)
     seed_ptr, seed_keep = _seed_ptr(ops, cb)
     st = N.Stats()
     rc = N.lib.ackpt_engine_run(engine.handle, state.data_ptr(), seed_ptr, out.data_ptr(), C.byref(st), _stream())
@@ -398,7 +427,7 @@ def execute(
     stats = _stats_from(st)
     if timeline:
         stats.timeline = _timeline(engine)
-    return _finish(out, initial_state), stats
+    return _finish(out.clone() if graph else out, initial_state), stats
 
 
 def _timeline(engine: _Engine) -> list:
@@ -417,6 +446,7 @@ def _sweep_engine(plan: MultistagePlan, ops: OperatorPair, backend) -> _Engine:
         raise ValueError("fallback plans have no Level-2 phase; use execute()")
     engine, cb = _engine_for(ops)
     _prepare(engine, N.MULTISTAGE, plan.s, plan.interval, _tier(backend, ops.state_size))
+    engine.plan_key = None  # execute() re-plans
     return engine, cb
 
 

@@ -440,3 +440,66 @@ def test_large_d_executions_match_oracle(P, d):
             assert torch.equal(full, rev) and torch.equal(full, ms), fuse
             assert L.rel_l2(full.double().cpu().numpy(), ref) <= 1e-5, (fuse, L.rel_l2(full.double().cpu().numpy(), ref))
             assert st.forward_evals == pkg.forward_cost(n, 5) and stm.forward_evals == 2 * n
+
+
+def _stats_tuple(st):
+    return (st.forward_evals, st.backward_evals, st.stores_issued, st.prefetches_issued, st.peak_l1_bytes)
+
+
+@pytest.mark.parametrize("dtype,batch", [("f64", 1), ("f32", 1 << 12)])
+def test_graph_replay_matches_eager(P, dtype, batch):
+    # graph=True: call 1 eager, call 2 captured, later calls replayed; every
+    # call's adjoint bit-identical to the eager pass with the same counters,
+    # for in-HBM and tiered strategies, per-step and fused, and a new input
+    # state goes through the graph's stable buffer
+    pkg, lstm, _ = P
+    d, n = 8, 40
+    cell = lstm.random_cell(d, n, 11)
+    ops = lstm.operator_pair(cell, batch, dtype)
+    mk = (lambda seed: lstm.random_state(d, seed)) if batch == 1 else (lambda seed: lstm.random_states(d, seed, batch, dtype))
+    s0, s1 = mk(12), mk(13)
+    eq = (lambda a, b: a == b) if batch == 1 else torch.equal
+    with pkg.PinnedHostBackend() as pinned:
+        for strat, backend in ((pkg.FullStorage(), None), (pkg.Revolve(5), None),
+                               (pkg.Multistage(5, interval=6), pinned)):
+            for fuse in (False, True):
+                want0, st0 = pkg.execute(strat, ops, s0, backend, fuse=fuse)
+                want1, _ = pkg.execute(strat, ops, s1, backend, fuse=fuse)
+                for i in range(4):
+                    s, want = (s0, want0) if i % 2 == 0 else (s1, want1)
+                    got, st = pkg.execute(strat, ops, s, backend, fuse=fuse, graph=True)
+                    assert eq(got, want), (strat, fuse, i)
+                    assert _stats_tuple(st) == _stats_tuple(st0), (strat, fuse, i)
+                # switching back to eager on the same engine stays correct
+                got, _ = pkg.execute(strat, ops, s0, backend, fuse=fuse)
+                assert eq(got, want0)
+
+
+def test_graph_replay_file_tier(P, tmp_path):
+    pkg, lstm, _ = P
+    d, n = 8, 60
+    cell = lstm.random_cell(d, n, 21)
+    ops = lstm.operator_pair(cell)
+    s0 = lstm.random_state(d, 22)
+    want, _ = pkg.execute(pkg.FullStorage(), ops, s0)
+    with pkg.FileBackend(str(tmp_path)) as fb:
+        for fuse in (False, True):
+            for _ in range(4):
+                got, st = pkg.execute(pkg.Multistage(4, interval=8), ops, s0, fb, fuse=fuse, graph=True)
+                assert got == want, fuse
+                assert st.stores_issued > 0 and st.prefetches_issued == st.stores_issued
+
+
+def test_graph_rejects_callback_operators(P):
+    pkg, lstm, _ = P
+    cell = lstm.random_cell(4, 6, 2)
+    dc = lstm.device_cell(cell, 1, "f64")
+    ops = pkg.OperatorPair(
+        forward_step=lambda k, s: dc.forward(k, s.view(torch.float64)),
+        backward_step=lambda k, s, a: dc.backward(k, s.view(torch.float64), a.view(torch.float64)),
+        state_size=dc.state_bytes,
+        n_steps=6,
+        adjoint_seed=lambda fin: dc.seed(fin.view(torch.float64)),
+    )
+    with pytest.raises(ValueError):
+        pkg.execute(pkg.Revolve(2), ops, lstm.random_state(4, 3), graph=True)
