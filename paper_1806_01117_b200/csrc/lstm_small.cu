@@ -13,7 +13,11 @@
 // shared copy of W has row stride d+1 so both the row-per-thread gate product
 // and the column-per-thread transposed product are bank-conflict free, and the
 // next step's bias (and, in reverse, state) is loaded during the current step
-// so no global-load latency sits on the step's dependency chain.  Same
+// so no global-load latency sits on the step's dependency chain.  Launches
+// are programmatic dependent launches: a kernel lets the next one start at
+// once, and the next stages W and its first bias (constants) before
+// `griddepcontrol.wait`, overlapping its prologue with this one's steps --
+// the per-step contract is a chain of such launches.  Same
 // formulas and math-library calls as the generic kernels (lstm_generic.cu),
 // so float64 results stay within 1e-12 of the reference.
 #include <cuda_runtime.h>
@@ -34,6 +38,9 @@ __device__ __forceinline__ double tanh_(double z) { return tanh(z); }
 // gates f, i, o: sigmoid; candidate g: tanh (lstm.py:120-126)
 template <typename T>
 __device__ __forceinline__ T act(T z, bool cand) { return cand ? tanh_(z) : sigmoid(z); }
+
+__device__ __forceinline__ void pdl_launch_next() { asm volatile("griddepcontrol.launch_dependents;"); }
+__device__ __forceinline__ void pdl_wait_prev() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
 struct Ptrs {
   const void* p[ACKPT_MAX_FUSED];
@@ -84,14 +91,16 @@ __global__ void fwd(const T* __restrict__ in, T* __restrict__ out, int64_t B, in
   T* h = reinterpret_cast<T*>(raw);
   T* c = h + d;
   T* a = c + d;  // 4d
+  pdl_launch_next();
   const WView<T> w = stage_w(a + 4 * d, w_smem, wh, wht, d);
   const int64_t b = blockIdx.x;
   const int n = threadIdx.x;
+  T xb = __ldg(xb_all + from * 4 * d + n);
+  pdl_wait_prev();  // the input state is the previous launch's output
   if (n < d) {
     h[n] = in[int64_t(n) * B + b];
     c[n] = in[int64_t(d + n) * B + b];
   }
-  T xb = __ldg(xb_all + from * 4 * d + n);
   __syncthreads();
   for (int i = 0; i < count; ++i) {
     const T xb_next = i + 1 < count ? __ldg(xb_all + (from + i + 1) * 4 * d + n) : T(0);
@@ -129,15 +138,18 @@ __global__ void rev(const T* __restrict__ adj_in, T* __restrict__ adj_out, int64
   T* dc = dh + d;
   T* a = dc + d;      // 4d gate pre-activations, then the 4 per-gate partial dh
   T* da = a + 4 * d;  // 4d gate adjoints
+  pdl_launch_next();
   const WView<T> w = stage_w(da + 4 * d, w_smem, wh, wht, d);
   const int64_t b = blockIdx.x;
   const int n = threadIdx.x;
+  T xb = __ldg(xb_all + (from + count - 1) * 4 * d + n);
+  pdl_wait_prev();
   if (n < d) {
     dh[n] = adj_in[int64_t(n) * B + b];
     dc[n] = adj_in[int64_t(d + n) * B + b];
   }
   // step i's state and bias in registers, step i-1's loaded during step i
-  T hs = T(0), cs = T(0), xb = __ldg(xb_all + (from + count - 1) * 4 * d + n);
+  T hs = T(0), cs = T(0);
   if (n < d) {
     const T* st = static_cast<const T*>(states.p[count - 1]);
     hs = st[int64_t(n) * B + b];
@@ -192,6 +204,27 @@ __global__ void rev(const T* __restrict__ adj_in, T* __restrict__ adj_out, int64
   }
 }
 
+// grid = one CTA per sequence, 4d threads; programmatic stream serialisation
+// unless ACKPT_PDL=0
+struct Launch {
+  cudaLaunchConfig_t cfg{};
+  cudaLaunchAttribute attr[1];
+  Launch(const ackpt_lstm* c, size_t smem, cudaStream_t s) {
+    static const bool pdl = [] {
+      const char* e = std::getenv("ACKPT_PDL");
+      return !(e && e[0] == '0');
+    }();
+    cfg.gridDim = dim3(unsigned(c->B));
+    cfg.blockDim = dim3(unsigned(4 * c->d));
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl ? 1 : 0;
+  }
+};
+
 }  // namespace sb
 
 bool sb_ok(const ackpt_lstm* c) {
@@ -228,9 +261,11 @@ void sb_forward(const ackpt_lstm* c, int64_t from, int count, const void* in, vo
   const bool w_smem = base + wbytes <= kSmallWBytes;
   const size_t smem = base + (w_smem ? wbytes : 0);
   if (smem > 48 * 1024) cudaFuncSetAttribute(sb::fwd<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-  sb::fwd<T><<<unsigned(c->B), unsigned(4 * c->d), smem, s>>>(
-      static_cast<const T*>(in), static_cast<T*>(out), c->B, c->d, static_cast<const T*>(c->d_wh),
-      static_cast<const T*>(c->d_wht), static_cast<const T*>(c->d_xb), from, count, outs != nullptr, w_smem, o);
+  sb::Launch L(c, smem, s);
+  ACKPT_CUDA_CHECK(cudaLaunchKernelEx(
+      &L.cfg, sb::fwd<T>, static_cast<const T*>(in), static_cast<T*>(out), c->B, c->d,
+      static_cast<const T*>(c->d_wh), static_cast<const T*>(c->d_wht), static_cast<const T*>(c->d_xb), from, count,
+      outs != nullptr, w_smem, o));
 }
 
 template <typename T>
@@ -244,9 +279,11 @@ void sb_reverse(const ackpt_lstm* c, int64_t from, int count, const void* const*
   const bool w_smem = base + wbytes <= kSmallWBytes;
   const size_t smem = base + (w_smem ? wbytes : 0);
   if (smem > 48 * 1024) cudaFuncSetAttribute(sb::rev<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-  sb::rev<T><<<unsigned(c->B), unsigned(4 * c->d), smem, s>>>(
-      static_cast<const T*>(adj_in), static_cast<T*>(adj_out), c->B, c->d, static_cast<const T*>(c->d_wh),
-      static_cast<const T*>(c->d_wht), static_cast<const T*>(c->d_xb), from, count, w_smem, p);
+  sb::Launch L(c, smem, s);
+  ACKPT_CUDA_CHECK(cudaLaunchKernelEx(
+      &L.cfg, sb::rev<T>, static_cast<const T*>(adj_in), static_cast<T*>(adj_out), c->B, c->d,
+      static_cast<const T*>(c->d_wh), static_cast<const T*>(c->d_wht), static_cast<const T*>(c->d_xb), from, count,
+      w_smem, p));
 }
 
 template void sb_forward<float>(const ackpt_lstm*, int64_t, int, const void*, void*, void* const*, cudaStream_t);
