@@ -9,6 +9,7 @@
 // for the key's last fetch event before overwriting the host bytes.
 // Worker exceptions surfaced at wait() (storage.py:271-278) map to a ticket
 // status returned by ackpt_tier_wait (MissingKey, StorageFull, SizeMismatch).
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <fcntl.h>
 #include <sys/stat.h>
@@ -18,6 +19,7 @@
 #include <atomic>
 #include <cerrno>
 #include <chrono>
+#include <condition_variable>
 #include <cstdio>
 #include <cstring>
 #include <deque>
@@ -55,6 +57,13 @@ struct TierTicket {
   int64_t len = 0;
 };
 
+// One file-stage transfer handed to a tier I/O thread (stream-memop path).
+struct IoJob {
+  TierTicket* tk = nullptr;
+  uint32_t seq = 0;   // store / fetch sequence number (1, 2, ...)
+  uint32_t need = 0;  // store: fetch seq that must have read the old file; fetch: store seq that wrote it
+};
+
 struct KeyEntry {
   int64_t slot = -1;
   unsigned char* big = nullptr;  // dedicated pinned buffer for payloads > slot_bytes
@@ -64,6 +73,8 @@ struct KeyEntry {
   cudaEvent_t last_store = nullptr;
   cudaEvent_t last_fetch = nullptr;
   bool stored = false, fetched = false;
+  uint32_t file_store_seq = 0;  // last I/O-thread store of this key (0: none)
+  uint32_t file_fetch_seq = 0;  // last I/O-thread fetch of this key
 };
 
 }  // namespace ackpt
@@ -91,7 +102,31 @@ struct ackpt_tier {
   unsigned char* stage_out = nullptr;
   unsigned char* stage_in = nullptr;
   int64_t stage_cap = 0;
+  // File-stage I/O threads.  A store's D2H copy lands in stage_out and the
+  // GPU bumps flag kCopied; the store thread then writes the CKPT file and
+  // bumps kWritten, which the D2H stream waits on (stream memory operations)
+  // before the ticket's event and the next store's copy.  A fetch's file is
+  // read into stage_in by the fetch thread as soon as its store is written
+  // and the previous fetch's H2D copy consumed stage_in (kConsumed); the H2D
+  // stream waits on kStaged before copying.  A host function on the stream
+  // would cost ~60-260 us of callback latency per transfer on the box; a
+  // stream wait on a host-written flag ~10 us.  Under CUDA-graph capture the
+  // host-function path is used (the threads are fed at enqueue time).
+  CUresult (*wait_value)(CUstream, CUdeviceptr, cuuint32_t, unsigned) = nullptr;
+  CUresult (*write_value)(CUstream, CUdeviceptr, cuuint32_t, unsigned) = nullptr;
+  uint32_t* flags = nullptr;  // pinned + mapped, one 64-byte line per flag
+  uint32_t store_seq = 0, fetch_seq = 0;  // issued (under mu)
+  std::mutex qmu;
+  std::condition_variable qcv;
+  std::deque<ackpt::IoJob> store_q, fetch_q;
+  int busy = 0;  // jobs popped and not finished
+  bool stop = false;
+  std::thread store_thr, fetch_thr;
 };
+
+namespace ackpt {
+enum Flag { kCopied = 0, kWritten = 16, kConsumed = 32, kStaged = 48 };
+}
 
 namespace ackpt {
 namespace {
@@ -241,10 +276,11 @@ uint32_t payload_io(int fd, unsigned char* buf, int64_t len, uint32_t reg, bool 
   return reg;
 }
 
-// Host function on the D2H stream, after the payload landed in stage_out:
-// tmp file + rename (write_checkpoint_file, storage.py:109-118).
-void CUDART_CB file_store_cb(void* arg) {
-  auto* tk = static_cast<TierTicket*>(arg);
+// Write stage_out as the ticket's CKPT file: tmp file + rename
+// (write_checkpoint_file, storage.py:109-118).  Errors go to tk->async.  The
+// replaced file's second name is returned in `*retired` for the caller to
+// unlink off the critical path (null: a detached thread unlinks it).
+void write_ckpt(TierTicket* tk, std::string* retired_out = nullptr) {
   ackpt_tier* t = tk->tier;
   unsigned char header[kHeader];
   std::memcpy(header, "CKPT", 4);
@@ -284,21 +320,37 @@ void CUDART_CB file_store_cb(void* arg) {
     else retired.clear();  // no previous file
     if (std::rename(tmp.c_str(), path.c_str()) != 0) err = errno;
   }
-  if (!retired.empty()) std::thread([retired] { ::unlink(retired.c_str()); }).detach();
+  if (retired_out) *retired_out = retired;
+  else if (!retired.empty()) std::thread([retired] { ::unlink(retired.c_str()); }).detach();
   if (trace) {
     const auto c3 = std::chrono::steady_clock::now();
     auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
-    std::fprintf(stderr, "ACKPT_FILE_TRACE store key=%lld open=%.2f io=%.2f close+rename=%.2f ms\n",
+    std::fprintf(stderr, "ACKPT_FILE_TRACE store key=%lld open=%.3f io=%.3f close+rename=%.3f ms\n",
                  (long long)tk->key, ms(c0, c1), ms(c1, c2), ms(c2, c3));
   }
   if (err) failed(err);
 }
 
-// Host function on the H2D stream: read + verify into stage_in
-// (decode_checkpoint / read_checkpoint_file, storage.py:83-127).
-void CUDART_CB file_fetch_cb(void* arg) {
-  auto* tk = static_cast<TierTicket*>(arg);
+// Host function on the D2H stream (graph-capture path), after the payload
+// landed in stage_out.
+void CUDART_CB file_store_cb(void* arg) { write_ckpt(static_cast<TierTicket*>(arg)); }
+
+// Read + verify the ticket's CKPT file into stage_in (decode_checkpoint /
+// read_checkpoint_file, storage.py:83-127).  Errors go to tk->async.
+void read_ckpt(TierTicket* tk) {
   ackpt_tier* t = tk->tier;
+  static const bool trace = std::getenv("ACKPT_FILE_TRACE") != nullptr;
+  const auto c0 = std::chrono::steady_clock::now();
+  struct Trace {
+    bool on;
+    int64_t key;
+    std::chrono::steady_clock::time_point c0;
+    ~Trace() {
+      if (on)
+        std::fprintf(stderr, "ACKPT_FILE_TRACE fetch key=%lld total=%.3f ms\n", (long long)key,
+                     std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - c0).count());
+    }
+  } tr{trace, tk->key, c0};
   const std::string path = ckpt_path(t, tk->key);
   const int fd = ::open(path.c_str(), O_RDONLY | O_CLOEXEC);
   if (fd < 0) {
@@ -337,6 +389,168 @@ void CUDART_CB file_fetch_cb(void* arg) {
   tk->step = int64_t(step);
 }
 
+// Host function on the H2D stream (graph-capture path).
+void CUDART_CB file_fetch_cb(void* arg) { read_ckpt(static_cast<TierTicket*>(arg)); }
+
+volatile uint32_t& flag(ackpt_tier* t, Flag f) { return reinterpret_cast<volatile uint32_t*>(t->flags)[f]; }
+
+// Wait until a flag the GPU bumps reaches `seq` (cyclic compare): spin, then yield.
+void wait_flag(ackpt_tier* t, Flag f, uint32_t seq) {
+  for (int i = 0; int32_t(flag(t, f) - seq) < 0; ++i)
+    if (i > 4096) std::this_thread::yield();
+  std::atomic_thread_fence(std::memory_order_acquire);
+}
+void set_flag(ackpt_tier* t, Flag f, uint32_t seq) {
+  std::atomic_thread_fence(std::memory_order_release);
+  flag(t, f) = seq;
+}
+
+// Store thread: jobs in issue order; a job's file is written once its copy
+// landed and every earlier fetch of the key has read the previous file.
+void store_worker(ackpt_tier* t) {
+  for (;;) {
+    IoJob job;
+    {
+      std::unique_lock<std::mutex> lk(t->qmu);
+      t->qcv.wait(lk, [&] { return t->stop || !t->store_q.empty(); });
+      if (t->store_q.empty()) return;
+      job = t->store_q.front();
+      t->store_q.pop_front();
+      ++t->busy;
+    }
+    wait_flag(t, kCopied, job.seq);
+    if (job.need) {
+      std::unique_lock<std::mutex> lk(t->qmu);
+      t->qcv.wait(lk, [&] { return int32_t(flag(t, kStaged) - job.need) >= 0; });
+    }
+    std::string retired;
+    write_ckpt(job.tk, &retired);
+    {
+      std::lock_guard<std::mutex> lk(t->qmu);
+      set_flag(t, kWritten, job.seq);  // always, so the D2H stream never hangs
+    }
+    t->qcv.notify_all();
+    if (!retired.empty()) ::unlink(retired.c_str());
+    {
+      std::lock_guard<std::mutex> lk(t->qmu);
+      --t->busy;
+    }
+    t->qcv.notify_all();
+  }
+}
+
+// Fetch thread: reads a job's file into stage_in once the store that wrote
+// it is done and the previous fetch's H2D copy has consumed stage_in.
+void fetch_worker(ackpt_tier* t) {
+  for (;;) {
+    IoJob job;
+    {
+      std::unique_lock<std::mutex> lk(t->qmu);
+      t->qcv.wait(lk, [&] { return t->stop || !t->fetch_q.empty(); });
+      if (t->fetch_q.empty()) return;
+      job = t->fetch_q.front();
+      t->fetch_q.pop_front();
+      ++t->busy;
+    }
+    if (job.need) {
+      std::unique_lock<std::mutex> lk(t->qmu);
+      t->qcv.wait(lk, [&] { return int32_t(flag(t, kWritten) - job.need) >= 0; });
+    }
+    wait_flag(t, kConsumed, job.seq - 1);
+    read_ckpt(job.tk);
+    {
+      std::lock_guard<std::mutex> lk(t->qmu);
+      set_flag(t, kStaged, job.seq);  // always, so the H2D stream never hangs
+      --t->busy;
+    }
+    t->qcv.notify_all();
+  }
+}
+
+// Stream-memop path available (driver entry points resolved, flags mapped)?
+bool io_threads_on(ackpt_tier* t) {
+  if (t->flags) return true;
+  static const bool env_off = [] {
+    const char* e = std::getenv("ACKPT_FILE_HOSTFN");
+    return e && e[0] == '1';
+  }();
+  if (env_off) return false;
+  void* w = nullptr;
+  void* v = nullptr;
+  cudaDriverEntryPointQueryResult q1, q2;
+  if (cudaGetDriverEntryPoint("cuStreamWaitValue32", &w, cudaEnableDefault, &q1) != cudaSuccess ||
+      cudaGetDriverEntryPoint("cuStreamWriteValue32", &v, cudaEnableDefault, &q2) != cudaSuccess ||
+      q1 != cudaDriverEntryPointSuccess || q2 != cudaDriverEntryPointSuccess || !w || !v) {
+    cudaGetLastError();
+    return false;
+  }
+  uint32_t* f = nullptr;
+  if (cudaHostAlloc(reinterpret_cast<void**>(&f), 256, cudaHostAllocMapped) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  std::memset(f, 0, 256);
+  t->wait_value = reinterpret_cast<CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned)>(w);
+  t->write_value = reinterpret_cast<CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned)>(v);
+  t->flags = f;
+  t->store_thr = std::thread(store_worker, t);
+  t->fetch_thr = std::thread(fetch_worker, t);
+  return true;
+}
+
+CUdeviceptr flag_dev(ackpt_tier* t, Flag f) {
+  void* d = nullptr;
+  ACKPT_CUDA_CHECK(cudaHostGetDevicePointer(&d, t->flags + f, 0));
+  return CUdeviceptr(reinterpret_cast<uintptr_t>(d));
+}
+void stream_wait(ackpt_tier* t, cudaStream_t s, Flag f, uint32_t seq) {
+  if (t->wait_value(reinterpret_cast<CUstream>(s), flag_dev(t, f), seq, CU_STREAM_WAIT_VALUE_GEQ) != CUDA_SUCCESS)
+    fail(ACKPT_CUDA_ERROR, "cuStreamWaitValue32 failed");
+}
+void stream_write(ackpt_tier* t, cudaStream_t s, Flag f, uint32_t seq) {
+  if (t->write_value(reinterpret_cast<CUstream>(s), flag_dev(t, f), seq, CU_STREAM_WRITE_VALUE_DEFAULT) !=
+      CUDA_SUCCESS)
+    fail(ACKPT_CUDA_ERROR, "cuStreamWriteValue32 failed");
+}
+void enqueue_job(ackpt_tier* t, bool store, const IoJob& job) {
+  {
+    std::lock_guard<std::mutex> lk(t->qmu);
+    (store ? t->store_q : t->fetch_q).push_back(job);
+  }
+  t->qcv.notify_all();
+}
+// Block until the I/O threads have no queued or running job.
+void io_drain(ackpt_tier* t) {
+  if (!t->flags) return;
+  std::unique_lock<std::mutex> lk(t->qmu);
+  t->qcv.wait(lk, [&] { return t->store_q.empty() && t->fetch_q.empty() && t->busy == 0; });
+}
+void io_stop(ackpt_tier* t) {
+  if (!t->flags) return;
+  {
+    std::lock_guard<std::mutex> lk(t->qmu);
+    t->stop = true;
+  }
+  t->qcv.notify_all();
+  if (t->store_thr.joinable()) t->store_thr.join();
+  if (t->fetch_thr.joinable()) t->fetch_thr.join();
+}
+
+// File-stage transfers go through the I/O threads unless the enqueue is being
+// captured into a CUDA graph (or a throttle needs the host-function hold).
+bool use_io_threads(ackpt_tier* t, void* after_stream) {
+  if (t->latency_s > 0 || t->bandwidth > 0) return false;
+  if (after_stream) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(static_cast<cudaStream_t>(after_stream), &cs) != cudaSuccess) {
+      cudaGetLastError();
+      return false;
+    }
+    if (cs != cudaStreamCaptureStatusNone) return false;
+  }
+  return io_threads_on(t);
+}
+
 // Length of an existing CKPT file (header only), -1 when absent / unreadable.
 int64_t file_payload_len(const ackpt_tier* t, int64_t key) {
   FILE* f = std::fopen(ckpt_path(t, key).c_str(), "rb");
@@ -351,6 +565,7 @@ void ensure_stage(ackpt_tier* t, int64_t bytes) {
   if (bytes <= t->stage_cap) return;
   ACKPT_CUDA_CHECK(cudaStreamSynchronize(t->d2h));
   ACKPT_CUDA_CHECK(cudaStreamSynchronize(t->h2d));
+  io_drain(t);
   if (t->stage_out) cudaFreeHost(t->stage_out);
   if (t->stage_in) cudaFreeHost(t->stage_in);
   t->stage_out = t->stage_in = nullptr;
@@ -451,6 +666,7 @@ void tier_quiesce(ackpt_tier* t) {
   std::lock_guard<std::mutex> lk(t->mu);
   ACKPT_CUDA_CHECK(cudaStreamSynchronize(t->d2h));
   ACKPT_CUDA_CHECK(cudaStreamSynchronize(t->h2d));
+  io_drain(t);
   for (auto& kv : t->keys) kv.second.fetched = false;
 }
 void tier_set_timing(ackpt_tier* t, bool on) {
@@ -512,6 +728,8 @@ ACKPT_API int ackpt_tier_destroy(ackpt_tier* t) {
     if (!t) return;
     if (t->d2h) cudaStreamSynchronize(t->d2h);
     if (t->h2d) cudaStreamSynchronize(t->h2d);
+    ackpt::io_stop(t);
+    if (t->flags) cudaFreeHost(t->flags);
     for (auto e : t->all_events) cudaEventDestroy(e);
     for (auto& kv : t->keys) {
       if (kv.second.last_store) cudaEventDestroy(kv.second.last_store);
@@ -551,11 +769,17 @@ ACKPT_API int ackpt_tier_begin_store(ackpt_tier* t, int64_t key, int64_t step, c
       // function on the same stream (stores serialise on the D2H stream).
       ackpt::ensure_stage(t, bytes);
       ackpt::KeyEntry& ke = t->keys[key];
+      const bool threads = ackpt::use_io_threads(t, after_stream);
       if (after_stream) {
         ACKPT_CUDA_CHECK(cudaEventRecord(t->after, static_cast<cudaStream_t>(after_stream)));
         ACKPT_CUDA_CHECK(cudaStreamWaitEvent(t->d2h, t->after, 0));
       }
       if (ke.fetched) ACKPT_CUDA_CHECK(cudaStreamWaitEvent(t->d2h, ke.last_fetch, 0));
+      uint32_t seq = 0;
+      if (threads) {  // stage_out is free once the previous store's file is written
+        seq = ++t->store_seq;
+        ackpt::stream_wait(t, t->d2h, ackpt::kWritten, seq - 1);
+      }
       cudaEvent_t m0 = ackpt::mark(t, t->d2h);
       if (bytes > 0)
         ACKPT_CUDA_CHECK(cudaMemcpyAsync(t->stage_out, src, size_t(bytes), cudaMemcpyDeviceToHost, t->d2h));
@@ -566,7 +790,15 @@ ACKPT_API int ackpt_tier_begin_store(ackpt_tier* t, int64_t key, int64_t step, c
       ref.tier = t;
       ref.len = bytes;
       ref.async = std::make_shared<ackpt::AsyncStatus>();
-      ACKPT_CUDA_CHECK(cudaLaunchHostFunc(t->d2h, ackpt::file_store_cb, &ref));
+      if (threads) {
+        ackpt::stream_write(t, t->d2h, ackpt::kCopied, seq);
+        ackpt::enqueue_job(t, true, {&ref, seq, ke.file_fetch_seq});
+        ackpt::stream_wait(t, t->d2h, ackpt::kWritten, seq);
+        ke.file_store_seq = seq;
+      } else {
+        ACKPT_CUDA_CHECK(cudaLaunchHostFunc(t->d2h, ackpt::file_store_cb, &ref));
+        ke.file_store_seq = 0;
+      }
       ackpt::hold(t, t->d2h, ref, bytes);
       ref.done = ackpt::new_event(t);
       ACKPT_CUDA_CHECK(cudaEventRecord(ref.done, t->d2h));
@@ -645,20 +877,32 @@ ACKPT_API int ackpt_tier_begin_fetch(ackpt_tier* t, int64_t key, void* dst, int6
       ackpt::ensure_stage(t, len);
       ackpt::KeyEntry& ke = t->keys[key];
       tk.step = ke.stored ? ke.step : key;
+      const bool threads = ackpt::use_io_threads(t, after_stream);
       if (after_stream) {
         ACKPT_CUDA_CHECK(cudaEventRecord(t->after, static_cast<cudaStream_t>(after_stream)));
         ACKPT_CUDA_CHECK(cudaStreamWaitEvent(t->h2d, t->after, 0));
       }
-      if (ke.stored) ACKPT_CUDA_CHECK(cudaStreamWaitEvent(t->h2d, ke.last_store, 0));
+      // (I/O-thread path: the fetch thread orders itself after the key's store)
+      if (ke.stored && !threads) ACKPT_CUDA_CHECK(cudaStreamWaitEvent(t->h2d, ke.last_store, 0));
       cudaEvent_t m0 = ackpt::mark(t, t->h2d);
       ackpt_ticket id = ackpt::add_ticket(t, std::move(tk));
       ackpt::TierTicket& ref = t->tickets[size_t(id)];
       ref.tier = t;
       ref.len = len;
       ref.async = std::make_shared<ackpt::AsyncStatus>();
-      ACKPT_CUDA_CHECK(cudaLaunchHostFunc(t->h2d, ackpt::file_fetch_cb, &ref));
-      if (len > 0)
-        ACKPT_CUDA_CHECK(cudaMemcpyAsync(dst, t->stage_in, size_t(len), cudaMemcpyHostToDevice, t->h2d));
+      if (threads) {
+        const uint32_t seq = ++t->fetch_seq;
+        ackpt::enqueue_job(t, false, {&ref, seq, ke.file_store_seq});
+        ke.file_fetch_seq = seq;
+        ackpt::stream_wait(t, t->h2d, ackpt::kStaged, seq);
+        if (len > 0)
+          ACKPT_CUDA_CHECK(cudaMemcpyAsync(dst, t->stage_in, size_t(len), cudaMemcpyHostToDevice, t->h2d));
+        ackpt::stream_write(t, t->h2d, ackpt::kConsumed, seq);
+      } else {
+        ACKPT_CUDA_CHECK(cudaLaunchHostFunc(t->h2d, ackpt::file_fetch_cb, &ref));
+        if (len > 0)
+          ACKPT_CUDA_CHECK(cudaMemcpyAsync(dst, t->stage_in, size_t(len), cudaMemcpyHostToDevice, t->h2d));
+      }
       ackpt::hold(t, t->h2d, ref, len);
       ref.done = ackpt::new_event(t);
       ACKPT_CUDA_CHECK(cudaEventRecord(ref.done, t->h2d));
@@ -801,6 +1045,7 @@ ACKPT_API int ackpt_tier_clear(ackpt_tier* t) {
   return ackpt::guard([&] {
     ACKPT_CUDA_CHECK(cudaStreamSynchronize(t->d2h));
     ACKPT_CUDA_CHECK(cudaStreamSynchronize(t->h2d));
+    ackpt::io_drain(t);
     std::lock_guard<std::mutex> lk(t->mu);
     for (auto& kv : t->keys) {
       if (kv.second.slot >= 0) t->free_slots.push_back(kv.second.slot);
