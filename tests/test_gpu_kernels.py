@@ -183,10 +183,11 @@ def test_c2_shape_kernels_on_sampled_rows(P):
     assert L.rel_l2(g[:, :, idx].cpu().numpy(), L.backward_step(ocell, 2, xs, a_ref)) <= F32_TOL
 
 
-@pytest.mark.parametrize("d,batch", [(16, 4096), (16, 130), (32, 1000), (32, 128)])
+@pytest.mark.parametrize("d,batch", [(16, 4096), (16, 2178), (32, 2100), (32, 4224)])
 def test_large_d_tensor_core_fused(P, d, batch):
-    # d in {16, 32}: tcgen05 kernels (lstm_f32_tcd.cuh) for the per-step
-    # operators and the fused advance / tape / reverse launches
+    # d in {16, 32}, B > 2048 (below, the CTA-per-sequence kernels win):
+    # tcgen05 kernels (lstm_f32_tcd.cuh) for the per-step operators and the
+    # fused advance / tape / reverse launches, full and ragged tiles
     cell, ocell = _cells(P, d, 40, 30 + d)
     x = torch.from_numpy(_states(d, 31, batch).astype(np.float32)).cuda()
     a = torch.from_numpy(_states(d, 32, batch).astype(np.float32)).cuda()
@@ -215,10 +216,14 @@ def test_large_d_tensor_core_fused(P, d, batch):
     assert torch.equal(chain.cpu(), torch.from_numpy(fused))
 
 
-@pytest.mark.parametrize("d,batch,dtype", [(32, 1, "f64"), (16, 3, "f64"), (5, 37, "f32"), (8, 1, "f32"), (128, 2, "f64")])
+@pytest.mark.parametrize("d,batch,dtype", [(32, 1, "f64"), (16, 3, "f64"), (5, 37, "f32"), (8, 1, "f32"),
+                                           (128, 2, "f64"), (128, 3, "f32"), (96, 2, "f64"), (8, 3000, "f64"),
+                                           (24, 2100, "f32"), (32, 64, "f32"), (8, 512, "f32")])
 def test_small_batch_kernels(P, d, batch, dtype):
-    # B <= 1024 outside the fp32 fast paths: one CTA per sequence
-    # (lstm_small.cu), per-step and fused launches, float64 within 1e-12
+    # one CTA per sequence (lstm_small.cu): every fp32 batch <= 2048 and every
+    # shape outside the fp32 fast paths; W in shared memory (padded rows) or,
+    # for d = 96 / 128, read from global memory (transposed copy); per-step
+    # (programmatic dependent launches) and fused launches, float64 within 1e-12
     cell, ocell = _cells(P, d, 30, 40 + d)
     npdt = np.float64 if dtype == "f64" else np.float32
     tol = 1e-12 if dtype == "f64" else F32_TOL
