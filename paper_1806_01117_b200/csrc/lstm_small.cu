@@ -59,20 +59,27 @@ struct WView {
   int prs;
 };
 
-// a[n] = xb + W[n] . h for this thread's gate row n (n < 4d)
+// a[n] = xb + W[n] . h for this thread's gate row n (n < 4d): two
+// interleaved accumulators (even / odd k) halve the dependent FMA chain
 template <typename T>
 __device__ __forceinline__ T gate_row(const WView<T>& w, T xb, const T* h, int d, int n) {
   const T* row = w.g + int64_t(n) * w.grs;
-  T acc = xb;
+  T acc0 = xb, acc1 = T(0);
+  int k = 0;
 #pragma unroll 4
-  for (int k = 0; k < d; ++k) acc = fma(row[int64_t(k) * w.gcs], h[k], acc);
-  return acc;
+  for (; k + 1 < d; k += 2) {
+    acc0 = fma(row[int64_t(k) * w.gcs], h[k], acc0);
+    acc1 = fma(row[int64_t(k + 1) * w.gcs], h[k + 1], acc1);
+  }
+  if (k < d) acc0 = fma(row[int64_t(k) * w.gcs], h[k], acc0);
+  return acc0 + acc1;
 }
 
-template <typename T>
-__device__ __forceinline__ WView<T> stage_w(T* ws, bool in_smem, const T* __restrict__ wh,
-                                            const T* __restrict__ wht, int d) {
-  if (!in_smem) return {wht, 1, 4 * d, wh, d};
+// (W's location is a template parameter so the products compile to LDS /
+// LDG rather than generic loads)
+template <bool kSmemW, typename T>
+__device__ __forceinline__ WView<T> stage_w(T* ws, const T* __restrict__ wh, const T* __restrict__ wht, int d) {
+  if (!kSmemW) return {wht, 1, 4 * d, wh, d};
   // blockDim = 4d: thread n copies column n % d of rows n / d + 4 t (coalesced reads)
   const int r0 = int(threadIdx.x) / d, k = int(threadIdx.x) - r0 * d;
 #pragma unroll 8
@@ -83,16 +90,16 @@ __device__ __forceinline__ WView<T> stage_w(T* ws, bool in_smem, const T* __rest
 
 // Forward over `count` steps from `from`.  tape != null: store every step's
 // state to tape[i]; otherwise the final state to `out`.
-template <typename T>
+template <typename T, bool kSmemW>
 __global__ void fwd(const T* __restrict__ in, T* __restrict__ out, int64_t B, int d, const T* __restrict__ wh,
-                    const T* __restrict__ wht, const T* __restrict__ xb_all, int64_t from, int count, bool tape, bool w_smem,
+                    const T* __restrict__ wht, const T* __restrict__ xb_all, int64_t from, int count, bool tape,
                     const __grid_constant__ Ptrs outs) {
   extern __shared__ __align__(16) unsigned char raw[];
   T* h = reinterpret_cast<T*>(raw);
   T* c = h + d;
   T* a = c + d;  // 4d
   pdl_launch_next();
-  const WView<T> w = stage_w(a + 4 * d, w_smem, wh, wht, d);
+  const WView<T> w = stage_w<kSmemW>(a + 4 * d, wh, wht, d);
   const int64_t b = blockIdx.x;
   const int n = threadIdx.x;
   T xb = __ldg(xb_all + from * 4 * d + n);
@@ -126,80 +133,92 @@ __global__ void fwd(const T* __restrict__ in, T* __restrict__ out, int64_t B, in
   }
 }
 
-// Reverse over steps from+count-1 .. from; states.p[i] is the state of step from+i.
-template <typename T>
+// Reverse over steps from+count-1 .. from; states.p[i] is the state of step
+// from+i.  Software-pipelined across steps: the transposed product of step i
+// (needs step i's gate adjoints) and the gate rows of step i-1 (need only
+// step i-1's state) are independent, so each thread runs them as interleaved
+// chains in one phase -- two barriers per step.
+template <typename T, bool kSmemW>
 __global__ void rev(const T* __restrict__ adj_in, T* __restrict__ adj_out, int64_t B, int d, const T* __restrict__ wh,
-                    const T* __restrict__ wht, const T* __restrict__ xb_all, int64_t from, int count, bool w_smem,
+                    const T* __restrict__ wht, const T* __restrict__ xb_all, int64_t from, int count,
                     const __grid_constant__ Ptrs states) {
   extern __shared__ __align__(16) unsigned char raw[];
-  T* h = reinterpret_cast<T*>(raw);
-  T* c = h + d;
-  T* dh = c + d;
-  T* dc = dh + d;
-  T* a = dc + d;      // 4d gate pre-activations, then the 4 per-gate partial dh
-  T* da = a + 4 * d;  // 4d gate adjoints
+  T* hb = reinterpret_cast<T*>(raw);  // [2][d] h of the step being reversed / the next one
+  T* cb = hb + 2 * d;                 // [2][d] c, same
+  T* dc = cb + 2 * d;                 // d
+  T* a = dc + d;                      // 4d activated gates of the step being reversed
+  T* da = a + 4 * d;                  // 4d gate adjoints
+  T* part = da + 4 * d;               // 4d per-gate partial dh
   pdl_launch_next();
-  const WView<T> w = stage_w(da + 4 * d, w_smem, wh, wht, d);
+  const WView<T> w = stage_w<kSmemW>(part + 4 * d, wh, wht, d);
   const int64_t b = blockIdx.x;
   const int n = threadIdx.x;
-  T xb = __ldg(xb_all + (from + count - 1) * 4 * d + n);
+  const int g = n / d, m = n - g * d;
+  const T xb_top = __ldg(xb_all + (from + count - 1) * 4 * d + n);
+  T xbn = count > 1 ? __ldg(xb_all + (from + count - 2) * 4 * d + n) : T(0);
   pdl_wait_prev();
+  T dhn = T(0), hs = T(0), cs = T(0);  // threads n < d: dh[n]; state of the step after next
   if (n < d) {
-    dh[n] = adj_in[int64_t(n) * B + b];
+    dhn = adj_in[int64_t(n) * B + b];
     dc[n] = adj_in[int64_t(d + n) * B + b];
-  }
-  // step i's state and bias in registers, step i-1's loaded during step i
-  T hs = T(0), cs = T(0);
-  if (n < d) {
     const T* st = static_cast<const T*>(states.p[count - 1]);
-    hs = st[int64_t(n) * B + b];
-    cs = st[int64_t(d + n) * B + b];
-  }
-  for (int i = count - 1; i >= 0; --i) {
-    if (n < d) {
-      h[n] = hs;
-      c[n] = cs;
+    hb[n] = st[int64_t(n) * B + b];
+    cb[n] = st[int64_t(d + n) * B + b];
+    if (count > 1) {
+      st = static_cast<const T*>(states.p[count - 2]);
+      hs = st[int64_t(n) * B + b];
+      cs = st[int64_t(d + n) * B + b];
     }
-    const T xb_i = xb;
-    if (i > 0) {
-      xb = __ldg(xb_all + (from + i - 1) * 4 * d + n);
-      if (n < d) {
-        const T* st = static_cast<const T*>(states.p[i - 1]);
-        hs = st[int64_t(n) * B + b];
-        cs = st[int64_t(d + n) * B + b];
+  }
+  __syncthreads();
+  a[n] = act(gate_row(w, xb_top, hb, d, n), n >= 3 * d);
+  __syncthreads();
+  int cur = 0;
+  for (int i = count - 1; i >= 0; --i) {
+    const int nxt = cur ^ 1;
+    if (n < d) {
+      const T* cc = cb + cur * d;
+      const T f = a[n], ig = a[d + n], o = a[2 * d + n], gg = a[3 * d + n];
+      const T cn = f * cc[n] + ig * gg;
+      const T t = tanh_(cn);
+      const T dco = dc[n] + dhn * o * (T(1) - t * t);  // lstm.py:143
+      da[n] = dco * cc[n] * f * (T(1) - f);           // lstm.py:144
+      da[d + n] = dco * gg * ig * (T(1) - ig);        // lstm.py:145
+      da[2 * d + n] = dhn * t * o * (T(1) - o);       // lstm.py:142,146
+      da[3 * d + n] = dco * ig * (T(1) - gg * gg);    // lstm.py:147
+      dc[n] = dco * f;                                // lstm.py:151
+      if (i > 0) {
+        hb[nxt * d + n] = hs;
+        cb[nxt * d + n] = cs;
+        if (i > 1) {
+          const T* st = static_cast<const T*>(states.p[i - 2]);
+          hs = st[int64_t(n) * B + b];
+          cs = st[int64_t(d + n) * B + b];
+        }
       }
     }
     __syncthreads();
-    a[n] = act(gate_row(w, xb_i, h, d, n), n >= 3 * d);
-    __syncthreads();
-    if (n < d) {
-      const T f = a[n], ig = a[d + n], o = a[2 * d + n], g = a[3 * d + n];
-      const T cn = f * c[n] + ig * g;
-      const T t = tanh_(cn);
-      const T dhn = dh[n];
-      const T dco = dc[n] + dhn * o * (T(1) - t * t);  // lstm.py:143
-      da[n] = dco * c[n] * f * (T(1) - f);            // lstm.py:144
-      da[d + n] = dco * g * ig * (T(1) - ig);         // lstm.py:145
-      da[2 * d + n] = dhn * t * o * (T(1) - o);       // lstm.py:142,146
-      da[3 * d + n] = dco * ig * (T(1) - g * g);      // lstm.py:147
-      dc[n] = dco * f;                                // lstm.py:151
-    }
-    __syncthreads();
-    {  // lstm.py:149-150: dh = sum_g W_g^T da_g; thread (g, m) sums gate g, then a fixed-order reduction
-      const int g = n / d, m = n - g * d;
+    {
+      // lstm.py:149-150: dh = sum_g W_g^T da_g; thread (g, m) sums gate g
+      // (then a fixed-order reduction); interleaved with step i-1's gate row
+      // (computed unconditionally so the two chains share one basic block;
+      // unused when i == 0)
       const T* wg = w.p + int64_t(g) * d * w.prs + m;
       const T* dg = da + g * d;
       T acc = T(0);
 #pragma unroll 4
       for (int j = 0; j < d; ++j) acc = fma(wg[int64_t(j) * w.prs], dg[j], acc);
-      a[n] = acc;  // gate pre-activations are dead by now
+      const T an = act(gate_row(w, xbn, hb + nxt * d, d, n), n >= 3 * d);
+      part[n] = acc;
+      a[n] = an;
+      if (i > 1) xbn = __ldg(xb_all + (from + i - 2) * 4 * d + n);
     }
     __syncthreads();
-    if (n < d) dh[n] = (a[n] + a[d + n]) + (a[2 * d + n] + a[3 * d + n]);
-    __syncthreads();
+    if (n < d) dhn = (part[n] + part[d + n]) + (part[2 * d + n] + part[3 * d + n]);
+    cur = nxt;
   }
   if (n < d) {
-    adj_out[int64_t(n) * B + b] = dh[n];
+    adj_out[int64_t(n) * B + b] = dhn;
     adj_out[int64_t(d + n) * B + b] = dc[n];
   }
 }
@@ -260,12 +279,12 @@ void sb_forward(const ackpt_lstm* c, int64_t from, int count, const void* in, vo
   // memory touches one cache line per thread per load (uncoalesced)
   const bool w_smem = base + wbytes <= kSmallWBytes;
   const size_t smem = base + (w_smem ? wbytes : 0);
-  if (smem > 48 * 1024) cudaFuncSetAttribute(sb::fwd<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+  auto kern = w_smem ? sb::fwd<T, true> : sb::fwd<T, false>;
+  if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
   sb::Launch L(c, smem, s);
-  ACKPT_CUDA_CHECK(cudaLaunchKernelEx(
-      &L.cfg, sb::fwd<T>, static_cast<const T*>(in), static_cast<T*>(out), c->B, c->d,
-      static_cast<const T*>(c->d_wh), static_cast<const T*>(c->d_wht), static_cast<const T*>(c->d_xb), from, count,
-      outs != nullptr, w_smem, o));
+  ACKPT_CUDA_CHECK(cudaLaunchKernelEx(&L.cfg, kern, static_cast<const T*>(in), static_cast<T*>(out), c->B, c->d,
+                                      static_cast<const T*>(c->d_wh), static_cast<const T*>(c->d_wht),
+                                      static_cast<const T*>(c->d_xb), from, count, outs != nullptr, o));
 }
 
 template <typename T>
@@ -273,17 +292,17 @@ void sb_reverse(const ackpt_lstm* c, int64_t from, int count, const void* const*
                 void* adj_out, cudaStream_t s) {
   sb::Ptrs p{};
   for (int i = 0; i < count; ++i) p.p[i] = states[i];
-  const size_t base = size_t(12) * c->d * sizeof(T), wbytes = size_t(4) * c->d * (c->d + 1) * sizeof(T);
+  const size_t base = size_t(17) * c->d * sizeof(T), wbytes = size_t(4) * c->d * (c->d + 1) * sizeof(T);
   // staged even for one step: the row-per-thread product straight from global
   // memory touches one cache line per thread per load (uncoalesced)
   const bool w_smem = base + wbytes <= kSmallWBytes;
   const size_t smem = base + (w_smem ? wbytes : 0);
-  if (smem > 48 * 1024) cudaFuncSetAttribute(sb::rev<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+  auto kern = w_smem ? sb::rev<T, true> : sb::rev<T, false>;
+  if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
   sb::Launch L(c, smem, s);
-  ACKPT_CUDA_CHECK(cudaLaunchKernelEx(
-      &L.cfg, sb::rev<T>, static_cast<const T*>(adj_in), static_cast<T*>(adj_out), c->B, c->d,
-      static_cast<const T*>(c->d_wh), static_cast<const T*>(c->d_wht), static_cast<const T*>(c->d_xb), from, count,
-      w_smem, p));
+  ACKPT_CUDA_CHECK(cudaLaunchKernelEx(&L.cfg, kern, static_cast<const T*>(adj_in), static_cast<T*>(adj_out), c->B,
+                                      c->d, static_cast<const T*>(c->d_wh), static_cast<const T*>(c->d_wht),
+                                      static_cast<const T*>(c->d_xb), from, count, p));
 }
 
 template void sb_forward<float>(const ackpt_lstm*, int64_t, int, const void*, void*, void* const*, cudaStream_t);
