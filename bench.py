@@ -313,7 +313,31 @@ def run_c1(pkg, lstm) -> dict:
                          "graph_speedup_vs_reference_cpu": C1_REFERENCE_MS[name] / (graphed.wall_seconds * 1e3)}
     finally:
         shutil.rmtree(scratch, ignore_errors=True)
+    out["cpu_port_same_box"] = c1_cpu_port()
     return out
+
+
+def c1_cpu_port() -> dict:
+    """Config 1 on THIS box's host: the oracle's numpy restatement of the
+    reference executor (oracle/runtime_oracle.py, one thread, fp64, B=1,
+    d=32, n=1000), min of 3 -- the same-box counterpart of the reference's
+    own `bench` numbers (measured in the build container: the reference
+    cannot travel to the GPU box).  Multistage keeps its boundary states in
+    memory (no CKPT files) with I = 11 (the reference's zero-latency
+    `--interval 11` case)."""
+    import numpy as np
+
+    from oracle import lstm_oracle as L
+    from oracle import runtime_oracle as R
+
+    cell = L.random_cell(32, 1000, 0)
+    s0 = L.random_states(32, 1, 1)
+    res = {"cores": 1, "kind": "port", "sample": "oracle/runtime_oracle.execute, n=1000, d=32, B=1 float64, min of 3"}
+    for name, kw in (("full", {}), ("revolve", {"slots": 10}),
+                     ("multistage", {"slots": 10, "interval": 11})):
+        best = min(R.execute(name, cell, np.ascontiguousarray(s0), **kw)[1]["wall_seconds"] for _ in range(3))
+        res[name + "_ms"] = best * 1e3  # executor wall, plan excluded (runtime.py:359-363)
+    return res
 
 
 def workload_config(args, interval, slots) -> dict:

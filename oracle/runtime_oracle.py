@@ -111,13 +111,19 @@ def execute(kind, cell, state0, *, slots=0, interval=None, dtype=np.float64, see
     seed_fn = (lambda fin: L.seed(cell, fin).astype(dtype)) if seed is None else (lambda fin: seed)
     ex = _Exec(cell, n, S, dtype, seed_fn)
     state0 = state0.astype(dtype)
-    t0 = time.perf_counter()
+    # plans are built outside the timed window, like runtime.py:359-363
     if kind == "full":
-        ex.run_schedule(SO.taped(n), 0, state0, 0)
+        acts = SO.taped(n)
     elif kind == "revolve":
-        ex.run_schedule(SO.revolve(n, slots), 0, state0, slots)
+        acts = SO.revolve(n, slots)
     elif kind == "multistage":
         bounds, segs, fallback = SO.plan_multistage(n, slots, interval)
+    t0 = time.perf_counter()
+    if kind == "full":
+        ex.run_schedule(acts, 0, state0, 0)
+    elif kind == "revolve":
+        ex.run_schedule(acts, 0, state0, slots)
+    elif kind == "multistage":
         if fallback:
             ex.run_schedule(segs[0][2], 0, state0, slots)
         else:
