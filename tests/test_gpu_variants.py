@@ -13,6 +13,7 @@ pytestmark = pytest.mark.gpu
 HERE = os.path.dirname(os.path.abspath(__file__))
 
 VARIANTS = [
+    # d = 8 families at B > 2048 (below that the CTA-per-sequence kernels run)
     ({"ACKPT_TC": "0"}, 8, 4096),                       # FFMA2 fused family
     ({"ACKPT_TC": "2"}, 8, 4096),                       # mixed
     ({"ACKPT_TC": "3"}, 8, 4096),                       # mma.sync register fragments
@@ -21,14 +22,18 @@ VARIANTS = [
     ({"ACKPT_TC_REV": "2"}, 8, 4096),                   # both matvecs on tcgen05
     ({"ACKPT_TC_REV": "2nr"}, 8, 4096),
     ({"ACKPT_TC_REV": "3"}, 8, 4096),                   # ping-pong TMEM-A reverse
-    ({"ACKPT_TC_REV": "sp"}, 8, 1000),                  # software-pipelined reverse, ragged tail
+    ({"ACKPT_TC_REV": "sp"}, 8, 4000),                  # software-pipelined reverse, ragged tail
     ({"ACKPT_TC_FWD": "pp"}, 8, 4096),                  # ping-pong forward
-    ({"ACKPT_TC_P": "2"}, 8, 1002),                     # two pairs per thread, ragged tail
+    ({"ACKPT_TC_P": "2"}, 8, 4002),                     # two pairs per thread, ragged tail
     ({"ACKPT_TC_NO_PF": "1"}, 8, 4096),                 # reverse without the bulk prefetch
     ({"ACKPT_KERNEL_VARIANT": "tma"}, 8, 4096),         # TMA per-step kernels
     ({"ACKPT_KERNEL_VARIANT": "ldg3"}, 8, 4096),
-    ({"ACKPT_TCD": "0"}, 16, 1024),                     # generic kernels for d = 16
-    ({}, 32, 1000),                                     # tensor-core d = 32, ragged tile
+    ({"ACKPT_TCD": "0"}, 16, 4096),                     # CTA-per-sequence kernels for d = 16 at large B
+    ({"ACKPT_SB_MAX": "0", "ACKPT_TCD": "0"}, 16, 4096),  # thread-per-sequence generic kernels
+    ({}, 32, 4100),                                     # tensor-core d = 32, ragged tile
+    ({"ACKPT_SB_FIRST": "0"}, 32, 1000),                # tensor-core d = 32 below the crossover
+    ({"ACKPT_PDL": "0"}, 32, 3),                        # CTA-per-sequence without dependent launches
+    ({"ACKPT_SB_FIRST": "0"}, 8, 1000),                 # tcgen05 d = 8 family below the crossover
 ]
 
 
@@ -40,3 +45,12 @@ def test_variant_parity(env, d, batch):
     assert out.returncode == 0, out.stderr[-2000:]
     errs = json.loads(out.stdout.strip().splitlines()[-1])
     assert max(errs.values()) <= 1e-5, errs
+
+
+def test_file_stage_host_function_path(tmp_path):
+    # ACKPT_FILE_HOSTFN=1: the file stage through cudaLaunchHostFunc instead
+    # of the tier I/O threads -- same adjoints and counters
+    out = subprocess.run([sys.executable, os.path.join(HERE, "file_stage_check.py"), str(tmp_path)],
+                         env=dict(os.environ, ACKPT_FILE_HOSTFN="1"), capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0, out.stderr[-2000:]
+    assert json.loads(out.stdout.strip().splitlines()[-1])["ok"]
