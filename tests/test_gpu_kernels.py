@@ -35,10 +35,12 @@ def _states(d, seed, batch, scale=1.0):
 
 @pytest.mark.parametrize(
     "d,batch",
-    # 4096/4100/516: TMA tiles (full, partial last tile, tiny); 2/1002: float2
-    # kernels; odd B and other d: generic kernels
+    # B <= 2048: CTA-per-sequence kernels; above: 4096/4100 float2 kernels
+    # (full / partial last tile), 2052/4098 ragged float2 tails, 4101 odd
+    # (CTA per sequence), d = 16 / 32 tensor-core tiles (2500, 3000 ragged)
     [(8, 4096), (8, 4100), (8, 516), (8, 2), (8, 1002), (4, 1024), (8, 1001), (5, 64), (16, 300), (32, 17),
-     (16, 4096), (32, 1000), (32, 256), (64, 40)],
+     (16, 4096), (32, 1000), (32, 256), (64, 40), (8, 2052), (8, 4098), (8, 4101), (4, 4100), (16, 2500),
+     (32, 3000)],
 )
 def test_forward_backward_f32_vs_oracle(P, d, batch):
     cell, ocell = _cells(P, d, 6, 11 + d)
@@ -110,11 +112,14 @@ def family(request, P):
 
 
 def _tensor_core_family(P, d, batch, dtype):
-    # fused d=8 fp32 forward launches (even batch) run on tcgen05 with the 3xTF32 split
-    return P.kernel_family() in ("tcgen05", "mixed", "mma") and d == 8 and dtype == "f32" and batch % 2 == 0
+    # fused d=8 fp32 forward launches (even batch above the CTA-per-sequence
+    # crossover, B > 2048) run on tcgen05 / mma with the 3xTF32 split
+    return (P.kernel_family() in ("tcgen05", "mixed", "mma") and d == 8 and dtype == "f32" and batch % 2 == 0
+            and batch > 2048)
 
 
-@pytest.mark.parametrize("d,batch,dtype", [(8, 4096, "f32"), (4, 512, "f32"), (8, 7, "f32"), (6, 64, "f64")])
+@pytest.mark.parametrize("d,batch,dtype", [(8, 4096, "f32"), (4, 512, "f32"), (8, 7, "f32"), (6, 64, "f64"),
+                                           (4, 4100, "f32"), (8, 2306, "f32")])
 def test_fused_advance(P, family, d, batch, dtype):
     cell, ocell = _cells(P, d, 12, 21)
     npdt = np.float64 if dtype == "f64" else np.float32
@@ -135,7 +140,8 @@ def test_fused_advance(P, family, d, batch, dtype):
         assert torch.equal(fused, chain)  # identical arithmetic per step
 
 
-@pytest.mark.parametrize("d,batch", [(8, 4096), (4, 512), (8, 1002), (8, 300), (8, 2), (8, 258)])
+@pytest.mark.parametrize("d,batch", [(8, 4096), (4, 512), (8, 1002), (8, 300), (8, 2), (8, 258),
+                                     (4, 4100), (8, 4098), (8, 2300), (8, 2050), (8, 2306)])
 def test_fused_tape_and_reverse(P, family, d, batch):
     cell, ocell = _cells(P, d, 70, 22)
     x = torch.from_numpy(_states(d, 9, batch).astype(np.float32)).cuda()
