@@ -22,8 +22,12 @@
 // so float64 results stay within 1e-12 of the reference.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdlib>
+#include <mutex>
+#include <unordered_map>
+#include <utility>
 
 #include "lstm_cell.h"
 
@@ -88,22 +92,13 @@ __device__ __forceinline__ WView<T> stage_w(T* ws, const T* __restrict__ wh, con
   return {ws, d + 1, 1, ws, d + 1};
 }
 
-// Forward over `count` steps from `from`.  tape != null: store every step's
-// state to tape[i]; otherwise the final state to `out`.
-template <typename T, bool kSmemW>
-__global__ void fwd(const T* __restrict__ in, T* __restrict__ out, int64_t B, int d, const T* __restrict__ wh,
-                    const T* __restrict__ wht, const T* __restrict__ xb_all, int64_t from, int count, bool tape,
-                    const __grid_constant__ Ptrs outs) {
-  extern __shared__ __align__(16) unsigned char raw[];
-  T* h = reinterpret_cast<T*>(raw);
-  T* c = h + d;
-  T* a = c + d;  // 4d
-  pdl_launch_next();
-  const WView<T> w = stage_w<kSmemW>(a + 4 * d, wh, wht, d);
-  const int64_t b = blockIdx.x;
+// Forward over `count` steps from `from` for sequence b.  tape: store every
+// step's state to outs.p[i]; otherwise the final state to `out`.
+template <typename T>
+__device__ __forceinline__ void fwd_seq(const T* __restrict__ in, T* __restrict__ out, int64_t B, int d,
+                                        const WView<T>& w, const T* __restrict__ xb_all, int64_t from, int count,
+                                        bool tape, const Ptrs& outs, T* h, T* c, T* a, T xb, int64_t b) {
   const int n = threadIdx.x;
-  T xb = __ldg(xb_all + from * 4 * d + n);
-  pdl_wait_prev();  // the input state is the previous launch's output
   if (n < d) {
     h[n] = in[int64_t(n) * B + b];
     c[n] = in[int64_t(d + n) * B + b];
@@ -133,30 +128,43 @@ __global__ void fwd(const T* __restrict__ in, T* __restrict__ out, int64_t B, in
   }
 }
 
-// Reverse over steps from+count-1 .. from; states.p[i] is the state of step
-// from+i.  Software-pipelined across steps: the transposed product of step i
-// (needs step i's gate adjoints) and the gate rows of step i-1 (need only
-// step i-1's state) are independent, so each thread runs them as interleaved
-// chains in one phase -- two barriers per step.
-template <typename T, bool kSmemW>
-__global__ void rev(const T* __restrict__ adj_in, T* __restrict__ adj_out, int64_t B, int d, const T* __restrict__ wh,
-                    const T* __restrict__ wht, const T* __restrict__ xb_all, int64_t from, int count,
-                    const __grid_constant__ Ptrs states) {
+// kPersist: CTAs loop over sequences (W staged once per CTA); else one
+// sequence per CTA.
+template <typename T, bool kSmemW, bool kPersist>
+__global__ void fwd(const T* __restrict__ in, T* __restrict__ out, int64_t B, int d, const T* __restrict__ wh,
+                    const T* __restrict__ wht, const T* __restrict__ xb_all, int64_t from, int count, bool tape,
+                    const __grid_constant__ Ptrs outs) {
   extern __shared__ __align__(16) unsigned char raw[];
-  T* hb = reinterpret_cast<T*>(raw);  // [2][d] h of the step being reversed / the next one
-  T* cb = hb + 2 * d;                 // [2][d] c, same
-  T* dc = cb + 2 * d;                 // d
-  T* a = dc + d;                      // 4d activated gates of the step being reversed
-  T* da = a + 4 * d;                  // 4d gate adjoints
-  T* part = da + 4 * d;               // 4d per-gate partial dh
+  T* h = reinterpret_cast<T*>(raw);
+  T* c = h + d;
+  T* a = c + d;  // 4d
   pdl_launch_next();
-  const WView<T> w = stage_w<kSmemW>(part + 4 * d, wh, wht, d);
-  const int64_t b = blockIdx.x;
+  const WView<T> w = stage_w<kSmemW>(a + 4 * d, wh, wht, d);
+  const T xb = __ldg(xb_all + from * 4 * d + threadIdx.x);
+  pdl_wait_prev();  // the input state is the previous launch's output
+  if (kPersist) {
+    for (int64_t b = blockIdx.x; b < B; b += gridDim.x) {
+      fwd_seq(in, out, B, d, w, xb_all, from, count, tape, outs, h, c, a, xb, b);
+      __syncthreads();
+    }
+  } else {
+    fwd_seq(in, out, B, d, w, xb_all, from, count, tape, outs, h, c, a, xb, int64_t(blockIdx.x));
+  }
+}
+
+// Reverse over steps from+count-1 .. from for sequence b; states.p[i] is the
+// state of step from+i.  Software-pipelined across steps: the transposed
+// product of step i (needs step i's gate adjoints) and the gate rows of step
+// i-1 (need only step i-1's state) are independent, so each thread runs them
+// as interleaved chains in one phase -- two barriers per step.
+template <typename T>
+__device__ __forceinline__ void rev_seq(const T* __restrict__ adj_in, T* __restrict__ adj_out, int64_t B, int d,
+                                        const WView<T>& w, const T* __restrict__ xb_all, int64_t from, int count,
+                                        const Ptrs& states, T* hb, T* cb, T* dc, T* a, T* da, T* part, T xb_top,
+                                        T xbn_first, int64_t b) {
+  T xbn = xbn_first;
   const int n = threadIdx.x;
   const int g = n / d, m = n - g * d;
-  const T xb_top = __ldg(xb_all + (from + count - 1) * 4 * d + n);
-  T xbn = count > 1 ? __ldg(xb_all + (from + count - 2) * 4 * d + n) : T(0);
-  pdl_wait_prev();
   T dhn = T(0), hs = T(0), cs = T(0);  // threads n < d: dh[n]; state of the step after next
   if (n < d) {
     dhn = adj_in[int64_t(n) * B + b];
@@ -223,17 +231,72 @@ __global__ void rev(const T* __restrict__ adj_in, T* __restrict__ adj_out, int64
   }
 }
 
+template <typename T, bool kSmemW, bool kPersist>
+__global__ void rev(const T* __restrict__ adj_in, T* __restrict__ adj_out, int64_t B, int d, const T* __restrict__ wh,
+                    const T* __restrict__ wht, const T* __restrict__ xb_all, int64_t from, int count,
+                    const __grid_constant__ Ptrs states) {
+  extern __shared__ __align__(16) unsigned char raw[];
+  T* hb = reinterpret_cast<T*>(raw);  // [2][d] h of the step being reversed / the next one
+  T* cb = hb + 2 * d;                 // [2][d] c, same
+  T* dc = cb + 2 * d;                 // d
+  T* a = dc + d;                      // 4d activated gates of the step being reversed
+  T* da = a + 4 * d;                  // 4d gate adjoints
+  T* part = da + 4 * d;               // 4d per-gate partial dh
+  pdl_launch_next();
+  const WView<T> w = stage_w<kSmemW>(part + 4 * d, wh, wht, d);
+  const int n = threadIdx.x;
+  const T xb_top = __ldg(xb_all + (from + count - 1) * 4 * d + n);
+  const T xbn_first = count > 1 ? __ldg(xb_all + (from + count - 2) * 4 * d + n) : T(0);
+  pdl_wait_prev();
+  if (kPersist) {  // as in fwd
+    for (int64_t b = blockIdx.x; b < B; b += gridDim.x) {
+      rev_seq(adj_in, adj_out, B, d, w, xb_all, from, count, states, hb, cb, dc, a, da, part, xb_top, xbn_first, b);
+      __syncthreads();  // the next sequence reuses the shared state
+    }
+  } else {
+    rev_seq(adj_in, adj_out, B, d, w, xb_all, from, count, states, hb, cb, dc, a, da, part, xb_top, xbn_first,
+            int64_t(blockIdx.x));
+  }
+}
+
 // grid = one CTA per sequence, 4d threads; programmatic stream serialisation
 // unless ACKPT_PDL=0
+// Grid: one CTA per sequence up to what the SMs hold at once; beyond that the
+// CTAs loop over sequences (W staged once per CTA, not once per sequence).
+template <class K>
+unsigned seq_grid(K kernel, int threads, size_t smem, int64_t B) {
+  static std::mutex mu;
+  static std::unordered_map<const void*, std::pair<size_t, unsigned>> cache;
+  unsigned cap = 0;
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = cache.find(reinterpret_cast<const void*>(kernel));
+    if (it != cache.end() && it->second.first == smem) cap = it->second.second;
+  }
+  if (!cap) {
+    int dev = 0, sms = 0, per_sm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, smem) != cudaSuccess) {
+      cudaGetLastError();
+      per_sm = 1;
+    }
+    cap = unsigned(std::max(1, per_sm) * std::max(1, sms));
+    std::lock_guard<std::mutex> lk(mu);
+    cache[reinterpret_cast<const void*>(kernel)] = {smem, cap};
+  }
+  return unsigned(std::min<int64_t>(B, cap));
+}
+
 struct Launch {
   cudaLaunchConfig_t cfg{};
   cudaLaunchAttribute attr[1];
-  Launch(const ackpt_lstm* c, size_t smem, cudaStream_t s) {
+  Launch(const ackpt_lstm* c, size_t smem, cudaStream_t s, unsigned grid) {
     static const bool pdl = [] {
       const char* e = std::getenv("ACKPT_PDL");
       return !(e && e[0] == '0');
     }();
-    cfg.gridDim = dim3(unsigned(c->B));
+    cfg.gridDim = dim3(grid);
     cfg.blockDim = dim3(unsigned(4 * c->d));
     cfg.dynamicSmemBytes = smem;
     cfg.stream = s;
@@ -279,9 +342,23 @@ void sb_forward(const ackpt_lstm* c, int64_t from, int count, const void* in, vo
   // memory touches one cache line per thread per load (uncoalesced)
   const bool w_smem = base + wbytes <= kSmallWBytes;
   const size_t smem = base + (w_smem ? wbytes : 0);
-  auto kern = w_smem ? sb::fwd<T, true> : sb::fwd<T, false>;
-  if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-  sb::Launch L(c, smem, s);
+  // one CTA per sequence while the SMs hold them all (or W is read from
+  // global memory: nothing to amortise); beyond that persistent CTAs
+  auto one = w_smem ? sb::fwd<T, true, false> : sb::fwd<T, false, false>;
+  if (smem > 48 * 1024) cudaFuncSetAttribute(one, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+  unsigned grid = unsigned(c->B);
+  auto kern = one;
+  if (w_smem) {
+    // short launches (per-step operators) are bound by staging W once per
+    // sequence; long fused runs amortise it and run faster one sequence per CTA
+    const unsigned cap = count < 8 ? sb::seq_grid(one, 4 * c->d, smem, c->B) : grid;
+    if (cap < grid) {
+      kern = sb::fwd<T, true, true>;
+      if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+      grid = sb::seq_grid(kern, 4 * c->d, smem, c->B);
+    }
+  }
+  sb::Launch L(c, smem, s, grid);
   ACKPT_CUDA_CHECK(cudaLaunchKernelEx(&L.cfg, kern, static_cast<const T*>(in), static_cast<T*>(out), c->B, c->d,
                                       static_cast<const T*>(c->d_wh), static_cast<const T*>(c->d_wht),
                                       static_cast<const T*>(c->d_xb), from, count, outs != nullptr, o));
@@ -297,9 +374,19 @@ void sb_reverse(const ackpt_lstm* c, int64_t from, int count, const void* const*
   // memory touches one cache line per thread per load (uncoalesced)
   const bool w_smem = base + wbytes <= kSmallWBytes;
   const size_t smem = base + (w_smem ? wbytes : 0);
-  auto kern = w_smem ? sb::rev<T, true> : sb::rev<T, false>;
-  if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-  sb::Launch L(c, smem, s);
+  auto one = w_smem ? sb::rev<T, true, false> : sb::rev<T, false, false>;  // as in sb_forward
+  if (smem > 48 * 1024) cudaFuncSetAttribute(one, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+  unsigned grid = unsigned(c->B);
+  auto kern = one;
+  if (w_smem) {
+    const unsigned cap = count < 8 ? sb::seq_grid(one, 4 * c->d, smem, c->B) : grid;  // as in sb_forward
+    if (cap < grid) {
+      kern = sb::rev<T, true, true>;
+      if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+      grid = sb::seq_grid(kern, 4 * c->d, smem, c->B);
+    }
+  }
+  sb::Launch L(c, smem, s, grid);
   ACKPT_CUDA_CHECK(cudaLaunchKernelEx(&L.cfg, kern, static_cast<const T*>(adj_in), static_cast<T*>(adj_out), c->B,
                                       c->d, static_cast<const T*>(c->d_wh), static_cast<const T*>(c->d_wht),
                                       static_cast<const T*>(c->d_xb), from, count, p));
