@@ -157,7 +157,7 @@ __global__ void fwd(const T* __restrict__ in, T* __restrict__ out, int64_t B, in
 // product of step i (needs step i's gate adjoints) and the gate rows of step
 // i-1 (need only step i-1's state) are independent, so each thread runs them
 // as interleaved chains in one phase -- two barriers per step.
-template <typename T>
+template <typename T, bool kSmemW>
 __device__ __forceinline__ void rev_seq(const T* __restrict__ adj_in, T* __restrict__ adj_out, int64_t B, int d,
                                         const WView<T>& w, const T* __restrict__ xb_all, int64_t from, int count,
                                         const Ptrs& states, T* hb, T* cb, T* dc, T* a, T* da, T* part, T xb_top,
@@ -216,9 +216,13 @@ __device__ __forceinline__ void rev_seq(const T* __restrict__ adj_in, T* __restr
       T acc = T(0);
 #pragma unroll 4
       for (int j = 0; j < d; ++j) acc = fma(wg[int64_t(j) * w.prs], dg[j], acc);
-      const T an = act(gate_row(w, xbn, hb + nxt * d, d, n), n >= 3 * d);
+      // (with W in global memory -- d = 96, 128 -- the unused i == 0 row
+      // would cost a full pass over W, so it is skipped there)
+      if (kSmemW || i > 0) {
+        const T an = act(gate_row(w, xbn, hb + nxt * d, d, n), n >= 3 * d);
+        a[n] = an;
+      }
       part[n] = acc;
-      a[n] = an;
       if (i > 1) xbn = __ldg(xb_all + (from + i - 2) * 4 * d + n);
     }
     __syncthreads();
@@ -250,12 +254,13 @@ __global__ void rev(const T* __restrict__ adj_in, T* __restrict__ adj_out, int64
   pdl_wait_prev();
   if (kPersist) {  // as in fwd
     for (int64_t b = blockIdx.x; b < B; b += gridDim.x) {
-      rev_seq(adj_in, adj_out, B, d, w, xb_all, from, count, states, hb, cb, dc, a, da, part, xb_top, xbn_first, b);
+      rev_seq<T, kSmemW>(adj_in, adj_out, B, d, w, xb_all, from, count, states, hb, cb, dc, a, da, part, xb_top,
+                         xbn_first, b);
       __syncthreads();  // the next sequence reuses the shared state
     }
   } else {
-    rev_seq(adj_in, adj_out, B, d, w, xb_all, from, count, states, hb, cb, dc, a, da, part, xb_top, xbn_first,
-            int64_t(blockIdx.x));
+    rev_seq<T, kSmemW>(adj_in, adj_out, B, d, w, xb_all, from, count, states, hb, cb, dc, a, da, part, xb_top,
+                       xbn_first, int64_t(blockIdx.x));
   }
 }
 
