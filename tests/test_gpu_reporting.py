@@ -82,3 +82,16 @@ def test_cli_bench_on_device(tmp_path):
     with contextlib.redirect_stdout(out):
         assert cli.main(["bench", "--strategy", "revolve", "--n", "30", "--d", "8", "--s", "4", "--runs", "1"]) == 0
     assert json.loads(out.getvalue())["forward_evals"] == pkg.forward_cost(30, 4)
+
+
+def test_cli_bench_graph_same_checksum():
+    # --graph replays the pass as a CUDA graph: same counters and gradient checksum
+    reps = []
+    for extra in ([], ["--graph"]):
+        out = io.StringIO()
+        with contextlib.redirect_stdout(out):
+            assert cli.main(["bench", "--strategy", "revolve", "--n", "40", "--d", "32", "--s", "5", "--runs", "3"]
+                            + extra) == 0
+        reps.append(json.loads(out.getvalue()))
+    assert reps[0]["gradient_checksum"] == reps[1]["gradient_checksum"]
+    assert reps[0]["forward_evals"] == reps[1]["forward_evals"] == pkg.forward_cost(40, 5)
