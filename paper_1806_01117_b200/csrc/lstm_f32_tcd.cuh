@@ -172,8 +172,11 @@ __device__ __forceinline__ void setup(float* sm, uint64_t* bars, uint32_t* tmem_
   }
   *reinterpret_cast<float4*>(sm + L::one + kofs<8>(tid, 0)) = make_float4(1.f, 0.f, 0.f, 0.f);
   *reinterpret_cast<float4*>(sm + L::one + kofs<8>(tid, 4)) = make_float4(0.f, 0.f, 0.f, 0.f);
+  // each warp writes one (8-row, 4-k) core-matrix block per iteration: the
+  // 32 lanes hit 32 distinct banks (row-major order was an 8-way conflict)
   for (int idx = tid; idx < 4 * D * D; idx += kThreads) {
-    const int n = idx / D, k = idx % D;
+    const int q = idx & 31, blk = idx >> 5;
+    const int n = (blk / (D / 4)) * 8 + (q >> 2), k = (blk % (D / 4)) * 4 + (q & 3);
     int gi, j;
     gate_of(n, gi, j);
     const float x = __ldg(ws + (gi * D + j) * D + k);
