@@ -336,8 +336,9 @@ __global__ void __launch_bounds__(kThreads)
   setup<D>(sm, bars, tslot, ws, kCols, 2);
   const uint32_t tmem = tmem_base(tslot);
   // B2[m][n] = s_gate W_gate[j(n)][m], K = 4D (gate-row order), tf32 hi/lo
-  for (int idx = threadIdx.x; idx < 4 * D * D; idx += kThreads) {
-    const int m = idx / (4 * D), n = idx % (4 * D);
+  for (int idx = threadIdx.x; idx < 4 * D * D; idx += kThreads) {  // conflict-free order, as in setup
+    const int q = idx & 31, blk = idx >> 5;
+    const int m = (blk / D) * 8 + (q >> 2), n = (blk % D) * 4 + (q & 3);
     int gi, j;
     gate_of(n, gi, j);
     const float x = __ldg(ws + (gi * D + j) * D + m);
