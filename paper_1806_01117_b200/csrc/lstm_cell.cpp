@@ -169,7 +169,7 @@ ACKPT_API int ackpt_lstm_create(int32_t d, int64_t n_steps, int64_t batch, int32
       ACKPT_CUDA_CHECK(cudaMalloc(&c->d_wht, wt.size()));
       ACKPT_CUDA_CHECK(cudaMemcpy(c->d_wht, wt.data(), wt.size(), cudaMemcpyHostToDevice));
     }
-    if (dtype == ACKPT_F32 && d <= 32) {
+    if (dtype == ACKPT_F32 && (d <= 32 || d == 64)) {
       // per-gate pre-scaled projections for the fused fp32 advance (lstm_f32_math.cuh)
       const float scale[4] = {-1.4426950408889634f, -1.4426950408889634f, -1.4426950408889634f,
                               2.0f * 1.4426950408889634f};
@@ -183,7 +183,7 @@ ACKPT_API int ackpt_lstm_create(int32_t d, int64_t n_steps, int64_t batch, int32
       ACKPT_CUDA_CHECK(cudaMalloc(&c->d_xbs, xbs.size() * sizeof(float)));
       ACKPT_CUDA_CHECK(cudaMemcpy(c->d_xbs, xbs.data(), xbs.size() * sizeof(float), cudaMemcpyHostToDevice));
       if (d == 8) ackpt::hm_tables(c.get());
-      if (d == 16 || d == 32) {  // pre-scaled W for the tensor-core kernels
+      if (d == 16 || d == 32 || d == 64) {  // pre-scaled W for the tensor-core kernels
         std::vector<float> ws(size_t(4) * D * D);
         for (size_t g = 0; g < 4; ++g)
           for (size_t j = 0; j < D; ++j)
@@ -307,7 +307,7 @@ ACKPT_API int ackpt_lstm_backward(const ackpt_lstm* cell, int64_t step, const vo
         case ackpt::Variant::kTmaBwd2: ackpt::tma_launch<8, 1, 256, 2>(cell, step, x, a, o, s); break;
         default: ackpt::tma_launch<8, 1, 256, 3>(cell, step, x, a, o, s);
       }
-    } else if (ackpt::tcd_ok(cell, {state, adjoint_in, adjoint_out})) {
+    } else if (ackpt::tcd_rev_ok(cell, {state, adjoint_in, adjoint_out})) {
       const float* st = static_cast<const float*>(state);
       ackpt::tcd_reverse(cell, step, 1, &st, static_cast<const float*>(adjoint_in), static_cast<float*>(adjoint_out),
                          s);
@@ -388,7 +388,7 @@ ACKPT_API int ackpt_lstm_backward_many(const ackpt_lstm* cell, int64_t from_step
     if (from_step < 0 || from_step + count > cell->n) ackpt::fail(ACKPT_VALUE_ERROR, "steps out of range");
     auto s = static_cast<cudaStream_t>(stream);
     const bool sbf = ackpt::sb_first(cell);
-    bool tcd = !sbf && ackpt::tcd_ok(cell, {adjoint_in, adjoint_out});
+    bool tcd = !sbf && ackpt::tcd_rev_ok(cell, {adjoint_in, adjoint_out});
     for (int64_t i = 0; i < count; ++i) tcd = tcd && !(reinterpret_cast<uintptr_t>(states[i]) & 3u);
     if (tcd) {
       ackpt::tcd_reverse(cell, from_step, int(count), reinterpret_cast<const float* const*>(states),

@@ -84,7 +84,8 @@ template <typename T>
 void sb_reverse(const ackpt_lstm* c, int64_t from, int count, const void* const* states, const void* adj_in,
                 void* adj_out, cudaStream_t s);
 // Tensor-core kernels for d in {16, 32} (lstm_f32_tcd.cu); per-step = count 1.
-bool tcd_ok(const ackpt_lstm* c, std::initializer_list<const void*> ptrs);
+bool tcd_ok(const ackpt_lstm* c, std::initializer_list<const void*> ptrs);      // forward kernels
+bool tcd_rev_ok(const ackpt_lstm* c, std::initializer_list<const void*> ptrs);  // reverse kernels
 void tcd_forward(const ackpt_lstm* c, int64_t from, int count, const float* in, float* out, float* const* outs,
                  cudaStream_t s);
 void tcd_reverse(const ackpt_lstm* c, int64_t from, int count, const float* const* states, const float* adj_in,

@@ -87,21 +87,35 @@ void rev_launch(const ackpt_lstm* c, int64_t from, int count, const float* const
 
 }  // namespace
 
-bool tcd_ok(const ackpt_lstm* c, std::initializer_list<const void*> ptrs) {
+namespace {
+bool tcd_common(const ackpt_lstm* c, std::initializer_list<const void*> ptrs) {
   static const bool on = [] {
     const char* e = std::getenv("ACKPT_TCD");
     return !(e && std::string(e) == "0");
   }();
-  if (!on || c->dtype != ACKPT_F32 || (c->d != 16 && c->d != 32) || !c->d_ws || !c->d_xbs) return false;
+  if (!on || c->dtype != ACKPT_F32 || !c->d_ws || !c->d_xbs) return false;
   for (const void* p : ptrs)
     if (reinterpret_cast<uintptr_t>(p) & 3u) return false;
   return true;
+}
+}  // namespace
+
+// Forward kernels: d in {16, 32, 64} (d = 64: A + W hi/lo + bias = 212 KB of
+// shared memory, 256 TMEM columns, one CTA per SM).
+bool tcd_ok(const ackpt_lstm* c, std::initializer_list<const void*> ptrs) {
+  return (c->d == 16 || c->d == 32 || c->d == 64) && tcd_common(c, ptrs);
+}
+// Reverse kernels: d in {16, 32} (d = 64 would also need W^T next to W: the
+// CTA-per-sequence kernels run its reverse).
+bool tcd_rev_ok(const ackpt_lstm* c, std::initializer_list<const void*> ptrs) {
+  return (c->d == 16 || c->d == 32) && tcd_common(c, ptrs);
 }
 
 void tcd_forward(const ackpt_lstm* c, int64_t from, int count, const float* in, float* out, float* const* outs,
                  cudaStream_t s) {
   if (c->d == 16) fwd_launch<16>(c, from, count, in, out, outs, s);
-  else fwd_launch<32>(c, from, count, in, out, outs, s);
+  else if (c->d == 32) fwd_launch<32>(c, from, count, in, out, outs, s);
+  else fwd_launch<64>(c, from, count, in, out, outs, s);
 }
 
 void tcd_reverse(const ackpt_lstm* c, int64_t from, int count, const float* const* states, const float* adj_in,

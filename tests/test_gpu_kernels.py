@@ -40,7 +40,7 @@ def _states(d, seed, batch, scale=1.0):
     # (CTA per sequence), d = 16 / 32 tensor-core tiles (2500, 3000 ragged)
     [(8, 4096), (8, 4100), (8, 516), (8, 2), (8, 1002), (4, 1024), (8, 1001), (5, 64), (16, 300), (32, 17),
      (16, 4096), (32, 1000), (32, 256), (64, 40), (8, 2052), (8, 4098), (8, 4101), (4, 4100), (16, 2500),
-     (32, 3000)],
+     (32, 3000), (64, 3000)],
 )
 def test_forward_backward_f32_vs_oracle(P, d, batch):
     cell, ocell = _cells(P, d, 6, 11 + d)
@@ -189,11 +189,12 @@ def test_c2_shape_kernels_on_sampled_rows(P):
     assert L.rel_l2(g[:, :, idx].cpu().numpy(), L.backward_step(ocell, 2, xs, a_ref)) <= F32_TOL
 
 
-@pytest.mark.parametrize("d,batch", [(16, 4096), (16, 2178), (32, 2100), (32, 4224)])
+@pytest.mark.parametrize("d,batch", [(16, 4096), (16, 2178), (32, 2100), (32, 4224), (64, 2200), (64, 4096)])
 def test_large_d_tensor_core_fused(P, d, batch):
-    # d in {16, 32}, B > 2048 (below, the CTA-per-sequence kernels win):
+    # d in {16, 32, 64}, B > 2048 (below, the CTA-per-sequence kernels win):
     # tcgen05 kernels (lstm_f32_tcd.cuh) for the per-step operators and the
-    # fused advance / tape / reverse launches, full and ragged tiles
+    # fused advance / tape / reverse launches (d = 64: forward kernels only,
+    # its reverse runs CTA per sequence), full and ragged tiles
     cell, ocell = _cells(P, d, 40, 30 + d)
     x = torch.from_numpy(_states(d, 31, batch).astype(np.float32)).cuda()
     a = torch.from_numpy(_states(d, 32, batch).astype(np.float32)).cuda()
