@@ -207,6 +207,7 @@ ACKPT_API int ackpt_lstm_destroy(ackpt_lstm* cell) {
     if (cell->d_frag_hm) cudaFree(cell->d_frag_hm);
     if (cell->d_xbs_hm) cudaFree(cell->d_xbs_hm);
     if (cell->d_ws) cudaFree(cell->d_ws);
+    if (cell->d_scratch) cudaFree(cell->d_scratch);
     delete cell;
   });
 }

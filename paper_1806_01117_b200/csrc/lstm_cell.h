@@ -23,7 +23,9 @@ struct ackpt_lstm {
   void* d_xbs = nullptr;  // n x 4 x d fp32, pre-scaled per gate (fp32 fast path, d <= 16)
   void* d_frag_hm = nullptr;  // d = 8 fp32: per-lane mma.sync B fragments (lstm_f32_hm.cu)
   void* d_xbs_hm = nullptr;   // d = 8 fp32: n x 4 x 8 per-thread scaled step biases
-  void* d_ws = nullptr;       // fp32 d in {16, 32}: 4 x d x d pre-scaled W (lstm_f32_tcd.cu)
+  void* d_ws = nullptr;       // fp32 d in {16, 32, 64}: 4 x d x d pre-scaled W (lstm_f32_tcd.cu)
+  void* d_scratch = nullptr;  // fp32 d = 64 reverse: gate-adjoint table [4d][B] (allocated on first use)
+  size_t scratch_bytes = 0;
 };
 
 namespace ackpt {

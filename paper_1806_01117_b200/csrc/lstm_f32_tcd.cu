@@ -85,6 +85,51 @@ void rev_launch(const ackpt_lstm* c, int64_t from, int count, const float* const
       ai, ao, c->B, static_cast<const float*>(c->d_xbs), static_cast<const float*>(c->d_ws), from, count, sp);
 }
 
+// d = 64 reverse: per step rev_gates_tcd (tcgen05 gates + gate adjoints) then
+// rev_tmatvec (CUDA-core transposed product), the adjoint updated in place in
+// adj_out; da scratch [4D][B] fp32 cached on the cell.
+void rev64_launch(const ackpt_lstm* c, int64_t from, int count, const float* const* states, const float* ai,
+                  float* ao, cudaStream_t s) {
+  constexpr int D = 64;
+  using L = tcd::Layout<D>;
+  static int sms = [] {
+    int dev = 0, n = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    return n;
+  }();
+  static bool attr = [] {
+    cudaFuncSetAttribute(tcd::rev_gates_tcd<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(L::fwd_bytes));
+    cudaFuncSetAttribute(tcd::rev_gates_tcd<D>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    cudaFuncSetAttribute(tcd::rev_tmatvec<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * D * D * 4);
+    return true;
+  }();
+  (void)attr;
+  auto* cell = const_cast<ackpt_lstm*>(c);
+  const size_t da_bytes = size_t(4) * D * size_t(c->B) * sizeof(float);
+  if (cell->scratch_bytes < da_bytes) {
+    if (cell->d_scratch) cudaFree(cell->d_scratch);
+    cell->d_scratch = nullptr;
+    cell->scratch_bytes = 0;
+    ACKPT_CUDA_CHECK(cudaMalloc(&cell->d_scratch, da_bytes));
+    cell->scratch_bytes = da_bytes;
+  }
+  float* da = static_cast<float*>(cell->d_scratch);
+  const auto xbs = static_cast<const float*>(c->d_xbs);
+  const auto ws = static_cast<const float*>(c->d_ws);
+  const unsigned g1 = tcd_grid(c->B, 1, tcd::rev_gates_tcd<D>, L::fwd_bytes, true, tcd::tmem_cols(4 * D));
+  int per_sm = 1;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tcd::rev_tmatvec<D>, 256, 4 * D * D * 4);
+  const unsigned g2 = unsigned(std::min<int64_t>((c->B + 255) / 256, int64_t(std::max(1, per_sm)) * sms));
+  const float* in = ai;
+  for (int i = count - 1; i >= 0; --i) {
+    tcd::rev_gates_tcd<D><<<g1, tcd::kThreads, L::fwd_bytes, s>>>(states[i], in, ao, da, c->B,
+                                                                   xbs + (from + i) * 4 * D, ws);
+    tcd::rev_tmatvec<D><<<g2, 256, 4 * D * D * 4, s>>>(da, ao, c->B, ws);
+    in = ao;  // in place from here on
+  }
+}
+
 }  // namespace
 
 namespace {
@@ -105,10 +150,10 @@ bool tcd_common(const ackpt_lstm* c, std::initializer_list<const void*> ptrs) {
 bool tcd_ok(const ackpt_lstm* c, std::initializer_list<const void*> ptrs) {
   return (c->d == 16 || c->d == 32 || c->d == 64) && tcd_common(c, ptrs);
 }
-// Reverse kernels: d in {16, 32} (d = 64 would also need W^T next to W: the
-// CTA-per-sequence kernels run its reverse).
+// Reverse kernels: d in {16, 32} (one fused kernel), d = 64 (two kernels per
+// step, rev64_launch).
 bool tcd_rev_ok(const ackpt_lstm* c, std::initializer_list<const void*> ptrs) {
-  return (c->d == 16 || c->d == 32) && tcd_common(c, ptrs);
+  return (c->d == 16 || c->d == 32 || c->d == 64) && tcd_common(c, ptrs);
 }
 
 void tcd_forward(const ackpt_lstm* c, int64_t from, int count, const float* in, float* out, float* const* outs,
@@ -121,7 +166,8 @@ void tcd_forward(const ackpt_lstm* c, int64_t from, int count, const float* in, 
 void tcd_reverse(const ackpt_lstm* c, int64_t from, int count, const float* const* states, const float* adj_in,
                  float* adj_out, cudaStream_t s) {
   if (c->d == 16) rev_launch<16>(c, from, count, states, adj_in, adj_out, s);
-  else rev_launch<32>(c, from, count, states, adj_in, adj_out, s);
+  else if (c->d == 32) rev_launch<32>(c, from, count, states, adj_in, adj_out, s);
+  else rev64_launch(c, from, count, states, adj_in, adj_out, s);
 }
 
 }  // namespace ackpt

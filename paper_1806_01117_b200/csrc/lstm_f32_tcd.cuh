@@ -444,5 +444,112 @@ __global__ void __launch_bounds__(kThreads)
   if (threadIdx.x < 32) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kCols));
 }
 
+// ---- d = 64 reverse: two kernels per step ---------------------------------
+// W and Wᵀ do not both fit next to the A tiles at d = 64, so a reverse step
+// is split: rev_gates_tcd computes the gates on tcgen05 (as the forward), the
+// gate adjoints (bwd_unit) and the new dc, writing the adjoints da to a
+// scratch table [4D][B]; rev_tmatvec then forms dh = W_sᵀ da on the CUDA
+// cores (fp32, W_s from shared memory, float2-paired outputs).  The adjoint
+// is updated in place (each thread reads its own sequence's dh / dc before
+// writing them), so a Reverse run needs only the da table as scratch.
+__device__ __forceinline__ float2 ld_pair(const float* __restrict__ x, int64_t B, int64_t b, int row) {
+  return make_float2(ldg_nc(x + int64_t(row) * B + b), ldg_nc(x + int64_t(row + 1) * B + b));
+}
+
+template <int D>
+__global__ void __launch_bounds__(kThreads)
+    rev_gates_tcd(const float* __restrict__ state, const float* adj_in, float* adj_out, float* __restrict__ da_out,
+                  int64_t B, const float* __restrict__ xbs_k, const float* __restrict__ ws) {
+  using L = Layout<D>;
+  extern __shared__ __align__(128) float sm[];
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sm + L::fwd_end);
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 2);
+  setup<D>(sm, bars, tslot, ws, tmem_cols(4 * D), 1);
+  const uint32_t tmem = tmem_base(tslot);
+  const uint32_t lane = uint32_t((threadIdx.x >> 5) * 32) << 16;
+  uint32_t ph = 0;
+  for (int64_t tile = blockIdx.x; tile * kThreads < B; tile += gridDim.x, ++ph) {
+    const int64_t b = tile * kThreads + threadIdx.x;
+    const bool live = b < B;
+    {
+      float2 h[D / 2];
+      if (live) {
+        load_rows<D>(state, B, b, 0, h);
+      } else {
+#pragma unroll
+        for (int p = 0; p < D / 2; ++p) h[p] = make_float2(0.f, 0.f);
+      }
+      stage<D>(sm, h, xbs_k);
+    }
+    publish();
+    if (threadIdx.x == 0) issue_gates<D>(sm, tmem, bars);
+    wait_bar(bars, ph & 1u);
+#pragma unroll 1
+    for (int p0 = 0; p0 < D / 2; p0 += 4) {
+      float g[4][8];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) ld8(tmem + lane + uint32_t(8 * (p0 + q)), g[q]);
+      ld_wait();
+      if (!live) continue;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int p = p0 + q;
+        const float2 c = ld_pair(state, B, b, D + 2 * p);
+        const float2 dh = make_float2(adj_in[int64_t(2 * p) * B + b], adj_in[int64_t(2 * p + 1) * B + b]);
+        const float2 dc = make_float2(adj_in[int64_t(D + 2 * p) * B + b], adj_in[int64_t(D + 2 * p + 1) * B + b]);
+        float2 da[4], dcn;
+        bwd_unit(make_float2(g[q][0], g[q][1]), make_float2(g[q][2], g[q][3]), make_float2(g[q][4], g[q][5]),
+                 make_float2(g[q][6], g[q][7]), c, dh, dc, da[0], da[1], da[2], da[3], dcn);
+#pragma unroll
+        for (int gi = 0; gi < 4; ++gi) {
+          da_out[int64_t(gi * D + 2 * p) * B + b] = da[gi].x;
+          da_out[int64_t(gi * D + 2 * p + 1) * B + b] = da[gi].y;
+        }
+        adj_out[int64_t(D + 2 * p) * B + b] = dcn.x;
+        adj_out[int64_t(D + 2 * p + 1) * B + b] = dcn.y;
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (threadIdx.x < 32)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(tmem_cols(4 * D)));
+}
+
+// dh[m] = sum_n W_s[n][m] da[n] (n = gate * D + unit, lstm.py:149-150 with
+// the scaled weights / adjoints of bwd_unit); thread per sequence, outputs
+// paired for FFMA2, W_s broadcast from shared memory.  (A float2 pair of
+// sequences per thread, halving the shared-memory reads per sequence,
+// measured no faster: 197 registers, one CTA per SM.)
+template <int D>
+__global__ void __launch_bounds__(256)
+    rev_tmatvec(const float* __restrict__ da, float* __restrict__ adj_out, int64_t B, const float* __restrict__ ws) {
+  extern __shared__ __align__(16) float w[];  // [4D][D]
+  for (int i = threadIdx.x; i < 4 * D * D / 4; i += blockDim.x)
+    reinterpret_cast<float4*>(w)[i] = __ldg(reinterpret_cast<const float4*>(ws) + i);
+  __syncthreads();
+  for (int64_t b = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; b < B; b += int64_t(gridDim.x) * blockDim.x) {
+    float2 acc[D / 2];
+#pragma unroll
+    for (int m = 0; m < D / 2; ++m) acc[m] = make_float2(0.f, 0.f);
+#pragma unroll 2
+    for (int n = 0; n < 4 * D; ++n) {
+      const float2 a = bc(ldg_nc(da + int64_t(n) * B + b));
+      const float4* row = reinterpret_cast<const float4*>(w + n * D);
+#pragma unroll
+      for (int m4 = 0; m4 < D / 4; ++m4) {
+        const float4 wv = row[m4];
+        acc[2 * m4] = fma2(make_float2(wv.x, wv.y), a, acc[2 * m4]);
+        acc[2 * m4 + 1] = fma2(make_float2(wv.z, wv.w), a, acc[2 * m4 + 1]);
+      }
+    }
+#pragma unroll
+    for (int m = 0; m < D / 2; ++m) {
+      adj_out[int64_t(2 * m) * B + b] = acc[m].x;
+      adj_out[int64_t(2 * m + 1) * B + b] = acc[m].y;
+    }
+  }
+}
+
 }  // namespace tcd
 }  // namespace ackpt
