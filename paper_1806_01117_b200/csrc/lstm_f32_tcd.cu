@@ -101,7 +101,7 @@ void rev64_launch(const ackpt_lstm* c, int64_t from, int count, const float* con
   static bool attr = [] {
     cudaFuncSetAttribute(tcd::rev_gates_tcd<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(L::fwd_bytes));
     cudaFuncSetAttribute(tcd::rev_gates_tcd<D>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-    cudaFuncSetAttribute(tcd::rev_tmatvec<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * D * D * 4);
+    cudaFuncSetAttribute(tcd::rev_tmatvec<D, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * D * D * 4);
     return true;
   }();
   (void)attr;
@@ -119,13 +119,13 @@ void rev64_launch(const ackpt_lstm* c, int64_t from, int count, const float* con
   const auto ws = static_cast<const float*>(c->d_ws);
   const unsigned g1 = tcd_grid(c->B, 1, tcd::rev_gates_tcd<D>, L::fwd_bytes, true, tcd::tmem_cols(4 * D));
   int per_sm = 1;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tcd::rev_tmatvec<D>, 256, 4 * D * D * 4);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tcd::rev_tmatvec<D, 1>, 256, 4 * D * D * 4);
   const unsigned g2 = unsigned(std::min<int64_t>((c->B + 255) / 256, int64_t(std::max(1, per_sm)) * sms));
   const float* in = ai;
   for (int i = count - 1; i >= 0; --i) {
     tcd::rev_gates_tcd<D><<<g1, tcd::kThreads, L::fwd_bytes, s>>>(states[i], in, ao, da, c->B,
                                                                    xbs + (from + i) * 4 * D, ws);
-    tcd::rev_tmatvec<D><<<g2, 256, 4 * D * D * 4, s>>>(da, ao, c->B, ws);
+    tcd::rev_tmatvec<D, 1><<<g2, 256, 4 * D * D * 4, s>>>(da, ao, c->B, ws);
     in = ao;  // in place from here on
   }
 }

@@ -483,20 +483,41 @@ __global__ void __launch_bounds__(kThreads)
     }
     publish();
     if (threadIdx.x == 0) issue_gates<D>(sm, tmem, bars);
+    // c, dh, dc of a group of 4 unit pairs are loaded one group ahead (the
+    // first group while the gate MMAs run)
+    float2 cq[4], dhq[4], dcq[4];
+    auto load_group = [&](int p0) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int p = p0 + q;
+        if (live) {
+          cq[q] = ld_pair(state, B, b, D + 2 * p);
+          dhq[q] = make_float2(adj_in[int64_t(2 * p) * B + b], adj_in[int64_t(2 * p + 1) * B + b]);
+          dcq[q] = make_float2(adj_in[int64_t(D + 2 * p) * B + b], adj_in[int64_t(D + 2 * p + 1) * B + b]);
+        }
+      }
+    };
+    load_group(0);
     wait_bar(bars, ph & 1u);
 #pragma unroll 1
     for (int p0 = 0; p0 < D / 2; p0 += 4) {
       float g[4][8];
 #pragma unroll
       for (int q = 0; q < 4; ++q) ld8(tmem + lane + uint32_t(8 * (p0 + q)), g[q]);
+      float2 cc[4], dhc[4], dcc[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        cc[q] = cq[q];
+        dhc[q] = dhq[q];
+        dcc[q] = dcq[q];
+      }
+      if (p0 + 4 < D / 2) load_group(p0 + 4);
       ld_wait();
       if (!live) continue;
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         const int p = p0 + q;
-        const float2 c = ld_pair(state, B, b, D + 2 * p);
-        const float2 dh = make_float2(adj_in[int64_t(2 * p) * B + b], adj_in[int64_t(2 * p + 1) * B + b]);
-        const float2 dc = make_float2(adj_in[int64_t(D + 2 * p) * B + b], adj_in[int64_t(D + 2 * p + 1) * B + b]);
+        const float2 c = cc[q], dh = dhc[q], dc = dcc[q];
         float2 da[4], dcn;
         bwd_unit(make_float2(g[q][0], g[q][1]), make_float2(g[q][2], g[q][3]), make_float2(g[q][4], g[q][5]),
                  make_float2(g[q][6], g[q][7]), c, dh, dc, da[0], da[1], da[2], da[3], dcn);
@@ -517,36 +538,41 @@ __global__ void __launch_bounds__(kThreads)
 }
 
 // dh[m] = sum_n W_s[n][m] da[n] (n = gate * D + unit, lstm.py:149-150 with
-// the scaled weights / adjoints of bwd_unit); thread per sequence, outputs
-// paired for FFMA2, W_s broadcast from shared memory.  (A float2 pair of
-// sequences per thread, halving the shared-memory reads per sequence,
-// measured no faster: 197 registers, one CTA per SM.)
-template <int D>
+// the scaled weights / adjoints of bwd_unit).  kParts threads per sequence
+// (adjacent lanes, D / kParts outputs each), outputs paired for FFMA2, W_s
+// broadcast from shared memory.  Measured at d = 64, B = 65536: kParts = 1
+// is fastest (reverse step 147 us; 2: 212, 4: 351 -- the extra da loads and
+// shorter FFMA2 runs cost more than the added warps gain).
+template <int D, int kParts>
 __global__ void __launch_bounds__(256)
     rev_tmatvec(const float* __restrict__ da, float* __restrict__ adj_out, int64_t B, const float* __restrict__ ws) {
+  constexpr int kM = D / kParts;
   extern __shared__ __align__(16) float w[];  // [4D][D]
   for (int i = threadIdx.x; i < 4 * D * D / 4; i += blockDim.x)
     reinterpret_cast<float4*>(w)[i] = __ldg(reinterpret_cast<const float4*>(ws) + i);
   __syncthreads();
-  for (int64_t b = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; b < B; b += int64_t(gridDim.x) * blockDim.x) {
-    float2 acc[D / 2];
+  const int part = threadIdx.x % kParts;
+  for (int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; t < B * kParts;
+       t += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t b = t / kParts;
+    float2 acc[kM / 2];
 #pragma unroll
-    for (int m = 0; m < D / 2; ++m) acc[m] = make_float2(0.f, 0.f);
-#pragma unroll 2
+    for (int m = 0; m < kM / 2; ++m) acc[m] = make_float2(0.f, 0.f);
+#pragma unroll 4
     for (int n = 0; n < 4 * D; ++n) {
       const float2 a = bc(ldg_nc(da + int64_t(n) * B + b));
-      const float4* row = reinterpret_cast<const float4*>(w + n * D);
+      const float4* row = reinterpret_cast<const float4*>(w + n * D + part * kM);
 #pragma unroll
-      for (int m4 = 0; m4 < D / 4; ++m4) {
+      for (int m4 = 0; m4 < kM / 4; ++m4) {
         const float4 wv = row[m4];
         acc[2 * m4] = fma2(make_float2(wv.x, wv.y), a, acc[2 * m4]);
         acc[2 * m4 + 1] = fma2(make_float2(wv.z, wv.w), a, acc[2 * m4 + 1]);
       }
     }
 #pragma unroll
-    for (int m = 0; m < D / 2; ++m) {
-      adj_out[int64_t(2 * m) * B + b] = acc[m].x;
-      adj_out[int64_t(2 * m + 1) * B + b] = acc[m].y;
+    for (int m = 0; m < kM / 2; ++m) {
+      adj_out[int64_t(part * kM + 2 * m) * B + b] = acc[m].x;
+      adj_out[int64_t(part * kM + 2 * m + 1) * B + b] = acc[m].y;
     }
   }
 }
