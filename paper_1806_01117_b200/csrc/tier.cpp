@@ -121,6 +121,7 @@ struct ackpt_tier {
   std::deque<ackpt::IoJob> store_q, fetch_q;
   int busy = 0;  // jobs popped and not finished
   bool stop = false;
+  std::atomic<bool> abort{false};  // destroy: stop waiting on flags a failed stream never bumps
   std::thread store_thr, fetch_thr;
 };
 
@@ -394,11 +395,15 @@ void CUDART_CB file_fetch_cb(void* arg) { read_ckpt(static_cast<TierTicket*>(arg
 
 volatile uint32_t& flag(ackpt_tier* t, Flag f) { return reinterpret_cast<volatile uint32_t*>(t->flags)[f]; }
 
-// Wait until a flag the GPU bumps reaches `seq` (cyclic compare): spin, then yield.
-void wait_flag(ackpt_tier* t, Flag f, uint32_t seq) {
-  for (int i = 0; int32_t(flag(t, f) - seq) < 0; ++i)
+// Wait until a flag the GPU bumps reaches `seq` (cyclic compare): spin, then
+// yield.  False when the tier is being torn down instead.
+bool wait_flag(ackpt_tier* t, Flag f, uint32_t seq) {
+  for (int i = 0; int32_t(flag(t, f) - seq) < 0; ++i) {
+    if (t->abort.load(std::memory_order_relaxed)) return false;
     if (i > 4096) std::this_thread::yield();
+  }
   std::atomic_thread_fence(std::memory_order_acquire);
+  return true;
 }
 void set_flag(ackpt_tier* t, Flag f, uint32_t seq) {
   std::atomic_thread_fence(std::memory_order_release);
@@ -418,13 +423,14 @@ void store_worker(ackpt_tier* t) {
       t->store_q.pop_front();
       ++t->busy;
     }
-    wait_flag(t, kCopied, job.seq);
-    if (job.need) {
+    bool ok = wait_flag(t, kCopied, job.seq);
+    if (ok && job.need) {
       std::unique_lock<std::mutex> lk(t->qmu);
-      t->qcv.wait(lk, [&] { return int32_t(flag(t, kStaged) - job.need) >= 0; });
+      t->qcv.wait(lk, [&] { return t->abort.load() || int32_t(flag(t, kStaged) - job.need) >= 0; });
+      ok = !t->abort.load();
     }
     std::string retired;
-    write_ckpt(job.tk, &retired);
+    if (ok) write_ckpt(job.tk, &retired);  // (never publish a file whose copy did not land)
     {
       std::lock_guard<std::mutex> lk(t->qmu);
       set_flag(t, kWritten, job.seq);  // always, so the D2H stream never hangs
@@ -452,12 +458,14 @@ void fetch_worker(ackpt_tier* t) {
       t->fetch_q.pop_front();
       ++t->busy;
     }
+    bool ok = true;
     if (job.need) {
       std::unique_lock<std::mutex> lk(t->qmu);
-      t->qcv.wait(lk, [&] { return int32_t(flag(t, kWritten) - job.need) >= 0; });
+      t->qcv.wait(lk, [&] { return t->abort.load() || int32_t(flag(t, kWritten) - job.need) >= 0; });
+      ok = !t->abort.load();
     }
-    wait_flag(t, kConsumed, job.seq - 1);
-    read_ckpt(job.tk);
+    if (ok) ok = wait_flag(t, kConsumed, job.seq - 1);
+    if (ok) read_ckpt(job.tk);
     {
       std::lock_guard<std::mutex> lk(t->qmu);
       set_flag(t, kStaged, job.seq);  // always, so the H2D stream never hangs
@@ -530,6 +538,7 @@ void io_stop(ackpt_tier* t) {
   {
     std::lock_guard<std::mutex> lk(t->qmu);
     t->stop = true;
+    t->abort.store(true);  // the streams were drained: only a failed stream leaves a flag behind
   }
   t->qcv.notify_all();
   if (t->store_thr.joinable()) t->store_thr.join();
