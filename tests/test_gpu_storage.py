@@ -192,3 +192,32 @@ def test_bench_file_backend_round_trip(pkg, tmp_path):
         assert (tmp_path / f"ckpt_{k}.bin").exists()
     base = lstm.bench(pkg.FullStorage(), n=24, d=4, s=3, seed=4, runs=1)
     assert rep.gradient_checksum == base.gradient_checksum
+
+
+@pytest.mark.timeout(180)
+def test_file_stage_write_failure_surfaces_without_hanging(pkg, tmp_path):
+    # the CKPT directory disappears before a pass: every store's file write
+    # fails on the tier's I/O thread; the copy streams must still drain and
+    # the run must raise (not hang), and the backend must close cleanly
+    import shutil
+
+    import paper_1806_01117_b200.lstm as lstm
+
+    cell = lstm.random_cell(8, 40, 3)
+    ops = lstm.operator_pair(cell, 4096, "f32")
+    s0 = lstm.random_states(8, 4, 4096, "f32")
+    d = tmp_path / "gone"
+    d.mkdir()
+    b = pkg.FileBackend(d)
+    try:
+        shutil.rmtree(d)
+        for fuse in (False, True):
+            with pytest.raises((pkg.ExecutionError, pkg.MissingKey, pkg.StorageFull, pkg.ChecksumMismatch)):
+                pkg.execute(pkg.Multistage(5, interval=8), ops, s0, b, fuse=fuse)
+        # the engine and tier stay usable once the directory is back
+        d.mkdir()
+        ref, _ = pkg.execute(pkg.FullStorage(), ops, s0, fuse=True)
+        adj, _ = pkg.execute(pkg.Multistage(5, interval=8), ops, s0, b, fuse=True)
+        assert torch.equal(adj, ref)
+    finally:
+        b.close()
