@@ -43,7 +43,7 @@ struct TargetParams {
 };
 
 constexpr int kMaxD = 128;
-constexpr int64_t kSmallBatch = (int64_t(1) << 31) - 1;// CTA-per-sequence kernels (lstm_small.cu): grid-x limit
+constexpr int64_t kSmallBatch = (int64_t(1) << 31) - 1;  // CTA-per-sequence kernels (lstm_small.cu): grid-x limit
 constexpr int64_t kSbFirstBatch = 2048;   // ... preferred over the batch-tiled fp32 kernels up to this one
 
 // fp32 fast path, d in {4, 8}: float2-paired kernels (lstm_f32_d*.cu).

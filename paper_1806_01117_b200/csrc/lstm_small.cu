@@ -1,13 +1,16 @@
-// Small-batch LSTM kernels (B <= kSmallBatch, any d <= 128, f32 or f64):
-// the reference's own workload is a single sequence (B = 1, float64 byte
-// image, lstm.py:99-107), where one thread per sequence would run all 4 d^2
-// products serially.  Here a CTA owns one sequence and its 4d threads own
+// CTA-per-sequence LSTM kernels (any B, any d <= 128, f32 or f64; the path
+// for every fp32 batch <= 2048 and every shape outside the batch-tiled fp32
+// kernels): the reference's own workload is a single sequence (B = 1,
+// float64 byte image, lstm.py:99-107), where one thread per sequence would
+// run all 4 d^2 products serially.  Here a CTA owns one sequence (or, for
+// short launches at large B, loops over sequences) and its 4d threads own
 // the gate rows:
 //   phase 1  thread n = gate row (g, j): a[n] = act_g(xb_k[n] + sum_k W[n][k] h[k])
 //            (the gate activation is applied by the row's own thread)
-//   phase 2  thread j < d: the activations, c' and h' (forward), or the
-//            gate adjoints da[g][j] and dc (reverse, lstm.py:141-151)
-//   phase 3  (reverse) thread m < d: dh[m] = sum_{g,j} W[g][j][m] da[g][j]
+//   phase 2  thread j < d: c' and h' (forward), or the gate adjoints
+//            da[g][j] and dc (reverse, lstm.py:141-151)
+//   phase 3  (reverse) all 4d threads: dh[m] = sum_{g,j} W[g][j][m] da[g][j],
+//            one gate each, then a fixed-order sum
 // with __syncthreads between phases and the state in shared memory across
 // steps, so a fused Advance / TapeForward / Reverse run is one launch.  The
 // shared copy of W has row stride d+1 so both the row-per-thread gate product
