@@ -422,12 +422,14 @@ def test_callback_engine_not_leaked(P):
     assert eng() is None
 
 
-@pytest.mark.parametrize("d", [16, 32])
-def test_large_d_executions_match_oracle(P, d):
-    # tensor-core kernels for d in {16, 32}: every strategy, per-step and
-    # fused, equal to the float64 oracle executor; strategies bit-identical
+@pytest.mark.parametrize("d,batch", [(16, 512), (32, 512), (16, 2600), (32, 2100), (64, 2200)])
+def test_large_d_executions_match_oracle(P, d, batch):
+    # d in {16, 32, 64}: CTA-per-sequence kernels (B <= 2048) and the
+    # tcgen05 kernels above (d = 64: two-kernel reverse); every strategy,
+    # per-step and fused, equal to the float64 oracle executor and
+    # bit-identical across strategies
     pkg, lstm, _ = P
-    n, batch = 30, 512
+    n = 30
     cell = lstm.random_cell(d, n, 4)
     ops = lstm.operator_pair(cell, batch, "f32")
     s0 = lstm.random_states(d, 5, batch, "f32")
