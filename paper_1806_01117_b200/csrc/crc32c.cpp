@@ -13,6 +13,7 @@
 // * crc32c_parallel splits a buffer over worker threads the same way.
 // Without SSE4.2 a slicing-by-8 table is used.
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <thread>
 #include <vector>
@@ -145,8 +146,12 @@ uint32_t crc32c_raw(const void* data, int64_t len, uint32_t reg) {
 
 int io_threads(int64_t len) {
   static const int hw = int(std::thread::hardware_concurrency());
+  static const int cap = [] {  // ACKPT_IO_THREADS: probe override of the worker cap
+    const char* e = std::getenv("ACKPT_IO_THREADS");
+    return e ? std::max(1, std::atoi(e)) : 8;
+  }();
   const int64_t by_size = len / (int64_t(4) << 20);  // >= 4 MiB per worker
-  return int(std::max<int64_t>(1, std::min<int64_t>({by_size, 8, hw > 0 ? hw : 1})));
+  return int(std::max<int64_t>(1, std::min<int64_t>({by_size, int64_t(cap), hw > 0 ? hw : 1})));
 }
 
 uint32_t crc32c_shift(uint32_t reg, int64_t len) { return len > 0 ? Tables::mulmod(x8n(len), reg) : reg; }
