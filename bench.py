@@ -43,7 +43,8 @@ def parse_args(argv=None):
     p.add_argument("--steps", type=int, default=5)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    p.add_argument("--n", type=int, default=10_000)
+    p.add_argument("--n", "--n-steps", dest="n", type=int, default=10_000,
+                   help="pass length (--n-steps under torchrun, whose parser claims --n)")
     p.add_argument("--d", type=int, default=8)
     p.add_argument("--batch", type=int, default=1 << 20, help="sequences per GPU")
     p.add_argument("--memory-ratio", type=float, default=0.1)
