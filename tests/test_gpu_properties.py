@@ -1,0 +1,58 @@
+"""Randomised end-to-end parity (hypothesis) on the GPU: random hidden size,
+batch, dtype, length, strategy, tier and execution mode -- every run equal to
+the float64 oracle executor (counters exact, peak_l1_bytes scaled to the
+state size, adjoint within the dtype's tolerance), so every kernel family
+the dispatcher can pick (CTA per sequence, FFMA2 / tcgen05 d=8, tcgen05
+d=16/32/64, generic) is exercised through the engine."""
+import numpy as np
+import pytest
+import torch
+from hypothesis import HealthCheck, given, settings
+from hypothesis import strategies as st
+
+from oracle import lstm_oracle as L
+from oracle import runtime_oracle as RO
+
+pytestmark = pytest.mark.gpu
+
+
+@settings(max_examples=40, deadline=None, derandomize=True, suppress_health_check=[HealthCheck.too_slow, HealthCheck.data_too_large])
+@given(
+    d=st.sampled_from([3, 4, 8, 16, 24, 32, 64]),
+    batch=st.sampled_from([1, 2, 7, 300, 2100, 4096]),
+    dtype=st.sampled_from(["f32", "f64"]),
+    n=st.integers(4, 40),
+    kind=st.sampled_from(["full", "revolve", "multistage"]),
+    slots=st.integers(1, 6),
+    interval=st.integers(2, 12),
+    fuse=st.booleans(),
+    seed=st.integers(0, 1000),
+)
+def test_random_configs_match_oracle(d, batch, dtype, n, kind, slots, interval, fuse, seed):
+    import paper_1806_01117_b200 as pkg
+    import paper_1806_01117_b200.lstm as lstm
+
+    if d * batch > 64 * 4096:
+        batch = 300  # keep the float64 oracle quick
+    cell = lstm.random_cell(d, n, seed)
+    ops = lstm.operator_pair(cell, batch, dtype)
+    s0 = lstm.random_states(d, seed + 1, batch, dtype)
+    ref_s0 = s0.double().cpu().numpy()
+    ocell = L.random_cell(d, n, seed)
+    okw = {"full": {}, "revolve": {"slots": slots}, "multistage": {"slots": slots, "interval": interval}}[kind]
+    strat = {"full": pkg.FullStorage(), "revolve": pkg.Revolve(slots),
+             "multistage": pkg.Multistage(slots, interval=interval)}[kind]
+    backend = pkg.PinnedHostBackend() if kind == "multistage" else None
+    try:
+        adj, st_ = pkg.execute(strat, ops, s0, backend, fuse=fuse)
+    finally:
+        if backend is not None:
+            backend.close()
+    ref, ost = RO.execute(kind, ocell, ref_s0, **okw)
+    for key in ("forward_evals", "backward_evals", "stores_issued", "prefetches_issued"):
+        assert getattr(st_, key) == ost[key], key
+    assert st_.peak_l1_bytes * 8 == ost["peak_l1_bytes"] * (4 if dtype == "f32" else 8)
+    tol = 1e-5 if dtype == "f32" else 1e-12
+    err = L.rel_l2(adj.double().cpu().numpy(), ref)
+    if np.linalg.norm(ref) > 1e-30:  # fp32 adjoints of long chains decay toward denormals
+        assert err <= tol, (d, batch, dtype, n, kind, fuse, err)

@@ -13,7 +13,7 @@ from oracle import schedule_oracle as S
 from paper_1806_01117_b200 import schedule as MS
 from paper_1806_01117_b200.perfmodel import interval_length
 
-SETTINGS = settings(max_examples=40, deadline=None, suppress_health_check=[HealthCheck.too_slow])
+SETTINGS = settings(max_examples=40, deadline=None, derandomize=True, suppress_health_check=[HealthCheck.too_slow])
 
 
 @SETTINGS
