@@ -3,7 +3,7 @@ batch, dtype, length, strategy, tier and execution mode -- every run equal to
 the float64 oracle executor (counters exact, peak_l1_bytes scaled to the
 state size, adjoint within the dtype's tolerance), so every kernel family
 the dispatcher can pick (CTA per sequence, FFMA2 / tcgen05 d=8, tcgen05
-d=16/32/64, generic) is exercised through the engine."""
+d=16/32/64) is exercised through the engine, eagerly and as a CUDA graph."""
 import numpy as np
 import pytest
 import torch
@@ -26,9 +26,10 @@ pytestmark = pytest.mark.gpu
     slots=st.integers(1, 6),
     interval=st.integers(2, 12),
     fuse=st.booleans(),
+    graph=st.booleans(),
     seed=st.integers(0, 1000),
 )
-def test_random_configs_match_oracle(d, batch, dtype, n, kind, slots, interval, fuse, seed):
+def test_random_configs_match_oracle(d, batch, dtype, n, kind, slots, interval, fuse, graph, seed):
     import paper_1806_01117_b200 as pkg
     import paper_1806_01117_b200.lstm as lstm
 
@@ -45,6 +46,10 @@ def test_random_configs_match_oracle(d, batch, dtype, n, kind, slots, interval, 
     backend = pkg.PinnedHostBackend() if kind == "multistage" else None
     try:
         adj, st_ = pkg.execute(strat, ops, s0, backend, fuse=fuse)
+        if graph:  # eager, captured, replayed: bit-identical with the same counters
+            for _ in range(3):
+                adj_g, st_g = pkg.execute(strat, ops, s0, backend, fuse=fuse, graph=True)
+                assert torch.equal(adj_g, adj) and st_g.forward_evals == st_.forward_evals
     finally:
         if backend is not None:
             backend.close()
