@@ -1,9 +1,12 @@
 """Randomised end-to-end parity (hypothesis) on the GPU: random hidden size,
-batch, dtype, length, strategy, tier and execution mode -- every run equal to
+batch, dtype, length, strategy, tier (pinned host / CKPT files) and execution mode -- every run equal to
 the float64 oracle executor (counters exact, peak_l1_bytes scaled to the
 state size, adjoint within the dtype's tolerance), so every kernel family
 the dispatcher can pick (CTA per sequence, FFMA2 / tcgen05 d=8, tcgen05
 d=16/32/64) is exercised through the engine, eagerly and as a CUDA graph."""
+import shutil
+import tempfile
+
 import numpy as np
 import pytest
 import torch
@@ -27,9 +30,10 @@ pytestmark = pytest.mark.gpu
     interval=st.integers(2, 12),
     fuse=st.booleans(),
     graph=st.booleans(),
+    tier=st.sampled_from(["pinned", "file"]),
     seed=st.integers(0, 1000),
 )
-def test_random_configs_match_oracle(d, batch, dtype, n, kind, slots, interval, fuse, graph, seed):
+def test_random_configs_match_oracle(d, batch, dtype, n, kind, slots, interval, fuse, graph, tier, seed):
     import paper_1806_01117_b200 as pkg
     import paper_1806_01117_b200.lstm as lstm
 
@@ -43,7 +47,10 @@ def test_random_configs_match_oracle(d, batch, dtype, n, kind, slots, interval, 
     okw = {"full": {}, "revolve": {"slots": slots}, "multistage": {"slots": slots, "interval": interval}}[kind]
     strat = {"full": pkg.FullStorage(), "revolve": pkg.Revolve(slots),
              "multistage": pkg.Multistage(slots, interval=interval)}[kind]
-    backend = pkg.PinnedHostBackend() if kind == "multistage" else None
+    scratch = tempfile.mkdtemp(prefix="ackpt_prop_")
+    backend = None
+    if kind == "multistage":
+        backend = pkg.PinnedHostBackend() if tier == "pinned" else pkg.FileBackend(scratch)
     try:
         adj, st_ = pkg.execute(strat, ops, s0, backend, fuse=fuse)
         if graph:  # eager, captured, replayed: bit-identical with the same counters
@@ -53,6 +60,7 @@ def test_random_configs_match_oracle(d, batch, dtype, n, kind, slots, interval, 
     finally:
         if backend is not None:
             backend.close()
+        shutil.rmtree(scratch, ignore_errors=True)
     ref, ost = RO.execute(kind, ocell, ref_s0, **okw)
     for key in ("forward_evals", "backward_evals", "stores_issued", "prefetches_issued"):
         assert getattr(st_, key) == ost[key], key
