@@ -221,3 +221,19 @@ def test_file_stage_write_failure_surfaces_without_hanging(pkg, tmp_path):
         assert torch.equal(adj, ref)
     finally:
         b.close()
+
+
+def test_file_stage_enospc_maps_to_storage_full(pkg, tmp_path):
+    # storage.py:109-118 + errors: a full device surfaces as StorageFull at
+    # wait.  The native file stage writes <key>.tmp first: pointing that name
+    # at /dev/full (every write fails with ENOSPC) exercises the real path.
+    if not os.path.exists("/dev/full"):
+        pytest.skip("no /dev/full")
+    with pkg.FileBackend(tmp_path) as b:
+        os.symlink("/dev/full", tmp_path / "ckpt_5.bin.tmp")
+        with pytest.raises(pkg.StorageFull):
+            b.wait(b.begin_store(5, pkg.CheckpointPayload(5, b"x" * 4096)))
+        assert not (tmp_path / "ckpt_5.bin").exists()
+        # the tier keeps working for other keys
+        b.wait(b.begin_store(6, pkg.CheckpointPayload(6, b"y" * 64)))
+        assert _host(b.wait(b.begin_fetch(6))) == b"y" * 64
