@@ -259,3 +259,31 @@ def test_small_batch_kernels(P, d, batch, dtype):
     for i, k in reversed(list(enumerate(range(3, 23)))):
         per_step = dc.backward(k, states[i], per_step)
     assert torch.equal(per_step, fused)
+
+
+@pytest.mark.parametrize("batch", [1 << 24, (1 << 24) + 6])
+def test_c4_per_gpu_shape_on_sampled_rows(P, batch):
+    # BASELINE config 4's per-GPU shard (8 GiB over 8 GPUs: d=8, B=2^24 fp32,
+    # 1 GiB states) and a ragged variant: 64-bit indexing at scale through the
+    # per-step and fused kernels, checked on sampled rows (incl. the last)
+    d = 8
+    cell, ocell = _cells(P, d, 6, 1)
+    x = P.random_states(d, 1, batch, "f32")
+    dc = P.device_cell(cell, batch, "f32")
+    idx = torch.tensor([0, 1, 777, batch // 3, batch // 2 + 1, batch - 2, batch - 1], device="cuda")
+    xs = x[:, :, idx].double().cpu().numpy()
+    y = dc.forward(1, x)
+    assert L.rel_l2(y[:, :, idx].cpu().numpy(), L.forward_step(ocell, 1, xs)) <= F32_TOL
+    a = dc.seed(y)
+    g = dc.backward(1, x, a)
+    a_s = a[:, :, idx].double().cpu().numpy()
+    assert L.rel_l2(g[:, :, idx].cpu().numpy(), L.backward_step(ocell, 1, xs, a_s)) <= F32_TOL
+    del g
+    outs = dc.forward_many(1, 2, x)
+    adv = dc.advance(1, 3, x)
+    ref2 = L.forward_step(ocell, 2, L.forward_step(ocell, 1, xs))
+    assert L.rel_l2(outs[1][:, :, idx].cpu().numpy(), ref2) <= F32_TOL
+    assert torch.equal(outs[1], adv)
+    rev = dc.backward_many(1, [x, outs[0]], a)
+    want = L.backward_step(ocell, 1, xs, L.backward_step(ocell, 2, outs[0][:, :, idx].double().cpu().numpy(), a_s))
+    assert L.rel_l2(rev[:, :, idx].cpu().numpy(), want) <= F32_TOL
