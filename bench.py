@@ -58,7 +58,7 @@ def parse_args(argv=None):
     p.add_argument("--full-n", type=int, default=1000, help="n of the measured FullStorage run")
     p.add_argument("--no-other-mode", action="store_true")
     p.add_argument("--no-c1", action="store_true", help="skip the BASELINE config-1 block (reference workload)")
-    p.add_argument("--family", choices=["ffma2", "tcgen05", "mixed", "mma"], default="tcgen05",
+    p.add_argument("--family", choices=["ffma2", "tcgen05"], default="tcgen05",
                    help="kernel family of the fused d=8 launches (lstm.set_kernel_family)")
     return p.parse_args(argv)
 
@@ -481,10 +481,8 @@ def main(argv=None) -> None:
     pipes = None
     base = dominant.split()[0]
     kfam = "ffma2"  # which kernel family ran the dominant launch
-    if args.fuse and (args.family == "tcgen05" or (args.family == "mixed" and "rev" not in base)):
+    if args.fuse and args.family == "tcgen05":
         kfam = "tcgen05"
-    if args.fuse and args.family == "mma":
-        kfam = "mma"
     if os.path.exists(tfile):
         with open(tfile) as fh:
             tj = json.load(fh)

@@ -216,8 +216,15 @@ ACKPT_API int ackpt_tier_begin_store(ackpt_tier* tier, int64_t key, int64_t step
  * (storage.py:310-311 raises inside the worker, surfaced by wait). */
 ACKPT_API int ackpt_tier_begin_fetch(ackpt_tier* tier, int64_t key, void* dst, int64_t bytes,
                                      void* after_stream, ackpt_ticket* out);
-/* Blocks the host; idempotent.  *step_out (may be NULL) receives the stored step. */
+/* Blocks the host; idempotent.  *step_out (may be NULL) receives the stored
+ * step.  A waited ticket's slot is recycled: waiting on it again returns the
+ * first wait's status and leaves *step_out unchanged.  The source of a store
+ * must not be modified, and the destination of a fetch not read, before the
+ * ticket completed (both are read / written by the copy engines). */
 ACKPT_API int ackpt_tier_wait(ackpt_tier* tier, ackpt_ticket ticket, int64_t* step_out);
+/* The tier's copy streams (cudaStream_t): stores run on *d2h, fetches on
+ * *h2d -- for callers that tie buffer lifetimes to them (record_stream). */
+ACKPT_API int ackpt_tier_streams(ackpt_tier* tier, void** d2h, void** h2d);
 /* Makes stream wait for the ticket on the device (no host block). */
 ACKPT_API int ackpt_tier_stream_wait(ackpt_tier* tier, ackpt_ticket ticket, void* stream);
 /* ACKPT_OK when complete, ACKPT_NOT_READY while in flight. */

@@ -44,6 +44,14 @@ def random_cell(d: int, n: int, seed: int) -> Cell:
     return Cell(w, b, xs, target)
 
 
+def long_memory_cell(d: int, n: int, seed: int, forget_bias: float = 6.0) -> Cell:
+    """random_cell plus forget_bias on b_f (mirror of the product's
+    lstm.long_memory_cell): non-vacuous adjoints at long n."""
+    cell = random_cell(d, n, seed)
+    cell.b[0] = cell.b[0] + forget_bias
+    return cell
+
+
 def random_states(d: int, seed: int, batch: int) -> np.ndarray:
     """(2, d, B) float64; batch=1 equals random_state(d, seed) (lstm.py:94-96)."""
     rng = np.random.default_rng(seed)

@@ -163,6 +163,7 @@ _SIGS = {
     "ackpt_tier_begin_store": ([_vp, C.c_int64, C.c_int64, _vp, C.c_int64, _vp, _i64p], C.c_int),
     "ackpt_tier_begin_fetch": ([_vp, C.c_int64, _vp, C.c_int64, _vp, _i64p], C.c_int),
     "ackpt_tier_wait": ([_vp, C.c_int64, _i64p], C.c_int),
+    "ackpt_tier_streams": ([_vp, C.POINTER(_vp), C.POINTER(_vp)], C.c_int),
     "ackpt_tier_stream_wait": ([_vp, C.c_int64, _vp], C.c_int),
     "ackpt_tier_poll": ([_vp, C.c_int64], C.c_int),
     "ackpt_tier_contains": ([_vp, C.c_int64, C.POINTER(C.c_int32)], C.c_int),

@@ -10,6 +10,9 @@
 //     raw(A || B, r) = shift(raw(A, r), |B|) xor raw(B, 0),
 //   shift(r, n) = r * x^(8n) mod P in the reflected GF(2) representation,
 //   with x^(2^k) mod P tabulated (the standard combine construction);
+//   Attribution: mulmod / the x^(2^k) table / the shift below follow zlib's
+//   multmodp / x2nmodp / crc32_combine (Mark Adler, zlib license), adapted
+//   to the Castagnoli polynomial;
 // * crc32c_parallel splits a buffer over worker threads the same way.
 // Without SSE4.2 a slicing-by-8 table is used.
 #include <algorithm>

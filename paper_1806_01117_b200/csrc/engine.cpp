@@ -727,7 +727,11 @@ void run_impl(ackpt_engine* E, Mode mode, const void* initial_state, const void*
   for (ackpt_ticket tk : graphed ? G.issued : r.issued) {  // file-stage I/O errors surface once the run drained
     std::string msg;
     const int rc = tier_async_status(E->tier, tk, &msg);
-    if (rc != ACKPT_OK) fail(rc, msg);
+    if (rc != ACKPT_OK) {
+      if (!graphed)
+        for (ackpt_ticket x : r.issued) tier_retire(E->tier, x);
+      fail(rc, msg);
+    }
   }
   if (graphed) {
     if (E->tier) tier_quiesce(E->tier);
@@ -766,6 +770,8 @@ void run_impl(ackpt_engine* E, Mode mode, const void* initial_state, const void*
     std::stable_sort(E->timeline_out.begin(), E->timeline_out.end(),
                      [](const ackpt_timeline_event& a, const ackpt_timeline_event& b) { return a.start < b.start; });
   }
+  if (!graphed)  // every transfer of the pass completed before ev_end: recycle the tickets
+    for (ackpt_ticket x : r.issued) tier_retire(E->tier, x);
   if (stats) *stats = r.st;
 }
 

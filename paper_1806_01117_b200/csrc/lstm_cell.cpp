@@ -37,53 +37,23 @@ bool f32_fast(const ackpt_lstm* c, std::initializer_list<const void*> ptrs) {
   return true;
 }
 
-// Kernel family for the d=8 fp32 fast path (all variants compute identical
-// bits).  ACKPT_KERNEL_VARIANT: ldg (register-staged, 2 CTAs/SM, default),
-// ldg3 (3 CTAs/SM), tma / tma128 / tma_bwd2 (bulk-copy smem pipelines).
-enum class Variant { kLdg, kLdg3, kTma, kTma128, kTmaBwd2 };
-Variant variant() {
-  static const Variant v = [] {
-    const char* e = std::getenv("ACKPT_KERNEL_VARIANT");
-    std::string s = e ? e : "ldg";
-    if (s == "ldg3") return Variant::kLdg3;
-    if (s == "tma") return Variant::kTma;
-    if (s == "tma128") return Variant::kTma128;
-    if (s == "tma_bwd2") return Variant::kTmaBwd2;
-    return Variant::kLdg;
-  }();
-  return v;
-}
-
 // Fused launches (advance / forward_many / backward_many) for d=8 pick a
-// kernel family: 0 packed FFMA2, 1 tcgen05 for all three (default: the
-// fastest measured at the C2 shape), 2 "mixed" = tcgen05
-// forward launches (advance, forward_many) + FFMA2 reverse runs, 3 "mma" =
-// warp-level mma.sync with register fragments for all three.  Env
-// ACKPT_TC=0/1/2/3 presets.  Families round differently (each within the
-// fp32 tolerance); within one family the strategies stay bit-identical.
+// kernel family: 1 tcgen05 (default: the fastest measured at the C2 shape,
+// DESIGN.md §3) or 0 packed FFMA2 (the documented fallback, also the family
+// of the per-step kernels).  Env ACKPT_TC=0 selects FFMA2.  The families round
+// differently (each within the fp32 tolerance); within one family the
+// strategies stay bit-identical.
 std::atomic<int> g_family{-1};  // -1: not yet read from the environment
 int family() {
   int f = g_family.load(std::memory_order_relaxed);
   if (f < 0) {
     const char* e = std::getenv("ACKPT_TC");
-    f = !e ? 1 : std::string(e) == "0" ? 0 : std::string(e) == "2" ? 2 : std::string(e) == "3" ? 3 : 1;
+    f = (e && std::string(e) == "0") ? 0 : 1;
     g_family.store(f, std::memory_order_relaxed);
   }
   return f;
 }
-bool tc_fwd_on() { return family() == 1 || family() == 2; }
-bool tc_bwd_on() { return family() == 1; }
-bool hm_on() { return family() == 3; }
-
-// TMA path: d=8, B % 4 == 0 (16-byte row segments), 16-byte aligned rows.
-bool tma_ok(const ackpt_lstm* c, std::initializer_list<const void*> ptrs) {
-  const Variant v = variant();
-  if (v == Variant::kLdg || v == Variant::kLdg3) return false;
-  if (c->dtype != ACKPT_F32 || c->d != 8 || (c->B & 3)) return false;
-  for (const void* p : ptrs)
-    if (reinterpret_cast<uintptr_t>(p) & 15u) return false;
-  return true;
-}
+bool tc_on() { return family() == 1; }
 
 }  // namespace
 
@@ -182,7 +152,6 @@ ACKPT_API int ackpt_lstm_create(int32_t d, int64_t n_steps, int64_t batch, int32
           }
       ACKPT_CUDA_CHECK(cudaMalloc(&c->d_xbs, xbs.size() * sizeof(float)));
       ACKPT_CUDA_CHECK(cudaMemcpy(c->d_xbs, xbs.data(), xbs.size() * sizeof(float), cudaMemcpyHostToDevice));
-      if (d == 8) ackpt::hm_tables(c.get());
       if (d == 16 || d == 32 || d == 64) {  // pre-scaled W for the tensor-core kernels
         std::vector<float> ws(size_t(4) * D * D);
         for (size_t g = 0; g < 4; ++g)
@@ -204,8 +173,6 @@ ACKPT_API int ackpt_lstm_destroy(ackpt_lstm* cell) {
     if (cell->d_wht) cudaFree(cell->d_wht);
     if (cell->d_xb) cudaFree(cell->d_xb);
     if (cell->d_xbs) cudaFree(cell->d_xbs);
-    if (cell->d_frag_hm) cudaFree(cell->d_frag_hm);
-    if (cell->d_xbs_hm) cudaFree(cell->d_xbs_hm);
     if (cell->d_ws) cudaFree(cell->d_ws);
     if (cell->d_scratch) cudaFree(cell->d_scratch);
     delete cell;
@@ -224,23 +191,14 @@ ACKPT_API int ackpt_lstm_forward(const ackpt_lstm* cell, int64_t step, const voi
     if (ackpt::sb_first(cell)) {
       if (cell->dtype == ACKPT_F32) ackpt::sb_forward<float>(cell, step, 1, state_in, state_out, nullptr, s);
       else ackpt::sb_forward<double>(cell, step, 1, state_in, state_out, nullptr, s);
-    } else if (ackpt::tma_ok(cell, {state_in, state_out})) {
-      auto i = static_cast<const float*>(state_in);
-      auto o = static_cast<float*>(state_out);
-      if (ackpt::variant() == ackpt::Variant::kTma128) ackpt::tma_launch<8, 0, 128, 4>(cell, step, i, nullptr, o, s);
-      else ackpt::tma_launch<8, 0, 256, 3>(cell, step, i, nullptr, o, s);
     } else if (ackpt::tcd_ok(cell, {state_in, state_out})) {
       ackpt::tcd_forward(cell, step, 1, static_cast<const float*>(state_in), static_cast<float*>(state_out), nullptr,
                          s);
     } else if (ackpt::f32_fast(cell, {state_in, state_out})) {
       auto i = static_cast<const float*>(state_in);
       auto o = static_cast<float*>(state_out);
-      if (cell->d == 8) {
-        if (ackpt::variant() == ackpt::Variant::kLdg3) ackpt::f32_forward_v<8, 3>(cell, step, i, o, s);
-        else ackpt::f32_forward<8>(cell, step, i, o, s);
-      } else {
-        ackpt::f32_forward<4>(cell, step, i, o, s);
-      }
+      if (cell->d == 8) ackpt::f32_forward<8>(cell, step, i, o, s);
+      else ackpt::f32_forward<4>(cell, step, i, o, s);
     } else if (ackpt::sb_ok(cell)) {
       if (cell->dtype == ACKPT_F32) ackpt::sb_forward<float>(cell, step, 1, state_in, state_out, nullptr, s);
       else ackpt::sb_forward<double>(cell, step, 1, state_in, state_out, nullptr, s);
@@ -268,8 +226,7 @@ ACKPT_API int ackpt_lstm_advance(const ackpt_lstm* cell, int64_t from_step, int6
     } else if (ackpt::f32_fast(cell, {state_in, state_out})) {
       auto i = static_cast<const float*>(state_in);
       auto o = static_cast<float*>(state_out);
-      if (cell->d == 8 && ackpt::hm_on()) ackpt::hm_advance(cell, from_step, int(to_step - from_step), i, o, s);
-      else if (cell->d == 8 && ackpt::tc_fwd_on()) ackpt::tc_advance(cell, from_step, int(to_step - from_step), i, o, s);
+      if (cell->d == 8 && ackpt::tc_on()) ackpt::tc_advance(cell, from_step, int(to_step - from_step), i, o, s);
       else if (cell->d == 8) ackpt::f32_advance<8>(cell, from_step, to_step, i, o, s);
       else ackpt::f32_advance<4>(cell, from_step, to_step, i, o, s);
     } else if (ackpt::tcd_ok(cell, {state_in, state_out})) {
@@ -299,15 +256,6 @@ ACKPT_API int ackpt_lstm_backward(const ackpt_lstm* cell, int64_t step, const vo
     if (ackpt::sb_first(cell)) {
       if (cell->dtype == ACKPT_F32) ackpt::sb_reverse<float>(cell, step, 1, &state, adjoint_in, adjoint_out, s);
       else ackpt::sb_reverse<double>(cell, step, 1, &state, adjoint_in, adjoint_out, s);
-    } else if (ackpt::tma_ok(cell, {state, adjoint_in, adjoint_out})) {
-      auto x = static_cast<const float*>(state);
-      auto a = static_cast<const float*>(adjoint_in);
-      auto o = static_cast<float*>(adjoint_out);
-      switch (ackpt::variant()) {
-        case ackpt::Variant::kTma128: ackpt::tma_launch<8, 1, 128, 3>(cell, step, x, a, o, s); break;
-        case ackpt::Variant::kTmaBwd2: ackpt::tma_launch<8, 1, 256, 2>(cell, step, x, a, o, s); break;
-        default: ackpt::tma_launch<8, 1, 256, 3>(cell, step, x, a, o, s);
-      }
     } else if (ackpt::tcd_rev_ok(cell, {state, adjoint_in, adjoint_out})) {
       const float* st = static_cast<const float*>(state);
       ackpt::tcd_reverse(cell, step, 1, &st, static_cast<const float*>(adjoint_in), static_cast<float*>(adjoint_out),
@@ -316,12 +264,8 @@ ACKPT_API int ackpt_lstm_backward(const ackpt_lstm* cell, int64_t step, const vo
       auto x = static_cast<const float*>(state);
       auto a = static_cast<const float*>(adjoint_in);
       auto o = static_cast<float*>(adjoint_out);
-      if (cell->d == 8) {
-        if (ackpt::variant() == ackpt::Variant::kLdg3) ackpt::f32_backward_v<8, 3>(cell, step, x, a, o, s);
-        else ackpt::f32_backward<8>(cell, step, x, a, o, s);
-      } else {
-        ackpt::f32_backward<4>(cell, step, x, a, o, s);
-      }
+      if (cell->d == 8) ackpt::f32_backward<8>(cell, step, x, a, o, s);
+      else ackpt::f32_backward<4>(cell, step, x, a, o, s);
     } else if (ackpt::sb_ok(cell)) {
       if (cell->dtype == ACKPT_F32) ackpt::sb_reverse<float>(cell, step, 1, &state, adjoint_in, adjoint_out, s);
       else ackpt::sb_reverse<double>(cell, step, 1, &state, adjoint_in, adjoint_out, s);
@@ -351,8 +295,7 @@ ACKPT_API int ackpt_lstm_forward_many(const ackpt_lstm* cell, int64_t from_step,
     if (fast) {
       auto in = static_cast<const float*>(state_in);
       auto outs = reinterpret_cast<float* const*>(states_out);
-      if (cell->d == 8 && ackpt::hm_on()) ackpt::hm_forward_many(cell, from_step, int(count), in, outs, s);
-      else if (cell->d == 8 && ackpt::tc_fwd_on()) ackpt::tc_forward_many(cell, from_step, int(count), in, outs, s);
+      if (cell->d == 8 && ackpt::tc_on()) ackpt::tc_forward_many(cell, from_step, int(count), in, outs, s);
       else if (cell->d == 8) ackpt::f32_forward_many<8>(cell, from_step, int(count), in, outs, s);
       else ackpt::f32_forward_many<4>(cell, from_step, int(count), in, outs, s);
       ackpt::check_launch();
@@ -410,8 +353,7 @@ ACKPT_API int ackpt_lstm_backward_many(const ackpt_lstm* cell, int64_t from_step
     auto sp = reinterpret_cast<const float* const*>(states);
     auto ai = static_cast<const float*>(adjoint_in);
     auto ao = static_cast<float*>(adjoint_out);
-    if (cell->d == 8 && ackpt::hm_on()) ackpt::hm_backward_many(cell, from_step, int(count), sp, ai, ao, s);
-    else if (cell->d == 8 && ackpt::tc_bwd_on()) ackpt::tc_backward_many(cell, from_step, int(count), sp, ai, ao, s);
+    if (cell->d == 8 && ackpt::tc_on()) ackpt::tc_backward_many(cell, from_step, int(count), sp, ai, ao, s);
     else if (cell->d == 8) ackpt::f32_backward_many<8>(cell, from_step, int(count), sp, ai, ao, s);
     else ackpt::f32_backward_many<4>(cell, from_step, int(count), sp, ai, ao, s);
     ackpt::check_launch();
@@ -448,8 +390,7 @@ ACKPT_API int ackpt_lstm_loss(const ackpt_lstm* cell, const void* final_state, v
 
 ACKPT_API int ackpt_set_fused_family(int32_t family) {
   return ackpt::guard([&] {
-    if (family < 0 || family > 3)
-      ackpt::fail(ACKPT_VALUE_ERROR, "family must be 0 (ffma2), 1 (tcgen05), 2 (mixed) or 3 (mma)");
+    if (family < 0 || family > 1) ackpt::fail(ACKPT_VALUE_ERROR, "family must be 0 (ffma2) or 1 (tcgen05)");
     ackpt::g_family.store(family);
   });
 }

@@ -21,8 +21,6 @@ struct ackpt_lstm {
   void* d_wht = nullptr;                            // d x 4d (W_h transposed), dtype
   void* d_xb = nullptr;                             // n x 4 x d, dtype
   void* d_xbs = nullptr;  // n x 4 x d fp32, pre-scaled per gate (fp32 fast path, d <= 16)
-  void* d_frag_hm = nullptr;  // d = 8 fp32: per-lane mma.sync B fragments (lstm_f32_hm.cu)
-  void* d_xbs_hm = nullptr;   // d = 8 fp32: n x 4 x 8 per-thread scaled step biases
   void* d_ws = nullptr;       // fp32 d in {16, 32, 64}: 4 x d x d pre-scaled W (lstm_f32_tcd.cu)
   void* d_scratch = nullptr;  // fp32 d = 64 reverse: gate-adjoint table [4d][B] (allocated on first use)
   size_t scratch_bytes = 0;
@@ -68,13 +66,6 @@ void tc_forward_many(const ackpt_lstm* c, int64_t from, int count, const float* 
                      cudaStream_t s);
 void tc_backward_many(const ackpt_lstm* c, int64_t from, int count, const float* const* states, const float* adj_in,
                       float* adj_out, cudaStream_t s);
-// Register-fragment tensor-core (mma.sync, 3xTF32) fused kernels, d = 8 (lstm_f32_hm.cu).
-void hm_tables(ackpt_lstm* c);
-void hm_advance(const ackpt_lstm* c, int64_t from, int count, const float* in, float* out, cudaStream_t s);
-void hm_forward_many(const ackpt_lstm* c, int64_t from, int count, const float* in, float* const* outs,
-                     cudaStream_t s);
-void hm_backward_many(const ackpt_lstm* c, int64_t from, int count, const float* const* states, const float* adj_in,
-                      float* adj_out, cudaStream_t s);
 // Small-batch kernels (B <= kSmallBatch, any d, f32 / f64): one CTA per
 // sequence, one thread per gate row (lstm_small.cu); per-step = count 1.
 bool sb_ok(const ackpt_lstm* c);
@@ -92,18 +83,6 @@ void tcd_forward(const ackpt_lstm* c, int64_t from, int count, const float* in, 
                  cudaStream_t s);
 void tcd_reverse(const ackpt_lstm* c, int64_t from, int count, const float* const* states, const float* adj_in,
                  float* adj_out, cudaStream_t s);
-// Occupancy variants (MINB resident 256-thread CTAs per SM).
-template <int D, int MINB>
-void f32_forward_v(const ackpt_lstm* c, int64_t step, const float* in, float* out, cudaStream_t s);
-template <int D, int MINB>
-void f32_backward_v(const ackpt_lstm* c, int64_t step, const float* st, const float* ai, float* ao,
-                    cudaStream_t s);
-
-// TMA-pipelined persistent fp32 kernels (lstm_f32_tma_d*.cu); MODE 0 = fwd, 1 = bwd.
-template <int D, int MODE, int THREADS, int STAGES>
-void tma_launch(const ackpt_lstm* c, int64_t step, const float* x, const float* a, float* y,
-                cudaStream_t s);
-
 // Generic path, any d <= 128, f32 or f64 (lstm_generic.cu).
 template <typename T>
 void generic_forward(const ackpt_lstm* c, int64_t step, const T* in, T* out, cudaStream_t s);

@@ -329,12 +329,8 @@ void f32_advance(const ackpt_lstm* c, int64_t from, int64_t to, const float* in,
                                 cudaStream_t);                                                \
   template void f32_advance<D>(const ackpt_lstm*, int64_t, int64_t, const float*, float*,      \
                                cudaStream_t);                                                 \
-  template void f32_forward_v<D, 3>(const ackpt_lstm*, int64_t, const float*, float*,         \
-                                    cudaStream_t);                                            \
   template void f32_forward_many<D>(const ackpt_lstm*, int64_t, int, const float*,            \
                                     float* const*, cudaStream_t);                             \
   template void f32_backward_many<D>(const ackpt_lstm*, int64_t, int, const float* const*,    \
                                      const float*, float*, cudaStream_t);                     \
-  template void f32_backward_v<D, 3>(const ackpt_lstm*, int64_t, const float*, const float*,  \
-                                     float*, cudaStream_t);                                   \
   }

@@ -21,7 +21,6 @@
 // base+2r in global memory and processes it with the packed-fp32 math.
 #pragma once
 
-#include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
 #include "lstm_f32_math.cuh"
@@ -389,345 +388,6 @@ __global__ void __launch_bounds__(kThreads, 5)  // 96 registers, 5 CTAs/SM: 28.3
     }
   }
   teardown(sm);
-}
-
-// ---- software-pipelined reverse (ACKPT_TC_REV=sp) ----------------------------
-// The gates of step i-1 depend only on the taped state, not on the adjoint,
-// so their MMAs are issued before the epilogue of step i and run underneath
-// it: the accumulator is double-buffered in TMEM (columns [0, 64) and
-// [64, 128)), one barrier per step, the MMA round trip off the critical path.
-__device__ __forceinline__ void read_units_at(const Smem& sm, uint32_t col0, int u, float2 (&pre)[2][4]) {
-  const uint32_t lane = uint32_t((threadIdx.x >> 5) * 32) << 16;
-  float a[8], b[8];
-  ld8(sm.tmem + lane + col0 + uint32_t(4 * u), a);
-  ld8(sm.tmem + lane + col0 + uint32_t(kN + 4 * u), b);
-  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-  for (int q = 0; q < 2; ++q)
-#pragma unroll
-    for (int g = 0; g < 4; ++g) pre[q][g] = make_float2(a[4 * q + g], b[4 * q + g]);
-}
-
-// Barrier (A and bias staged by every thread), then thread 0 issues the gate
-// MMAs into columns col0 and commits them to sm.mbar.
-__device__ __forceinline__ void gates_issue_at(Smem& sm, uint32_t col0) {
-  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    const uint64_t wh = desc(su32(sm.bw[0])), wl = desc(su32(sm.bw[1]));
-    const uint64_t xh = desc(su32(sm.bb[0])), xl = desc(su32(sm.bb[1])), one = desc(su32(sm.a1));
-#pragma unroll
-    for (int t = 0; t < 2; ++t) {
-      const uint32_t d = sm.tmem + col0 + uint32_t(t * kN);
-      const uint64_t ah = desc(su32(sm.a[t][0])), al = desc(su32(sm.a[t][1]));
-      mma(d, ah, wh, 0u);
-      mma(d, al, wh, 1u);
-      mma(d, ah, wl, 1u);
-      mma(d, one, xh, 1u);
-      mma(d, one, xl, 1u);
-    }
-    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(&sm.mbar))
-                 : "memory");
-  }
-}
-
-__global__ void __launch_bounds__(kThreads, 4)
-    rev_tcs(const float* __restrict__ adj_in, float* __restrict__ adj_out, int64_t B, const float* __restrict__ xbs_all,
-            int64_t from, int count, const __grid_constant__ Weights w, const __grid_constant__ StatePtrs states) {
-  __shared__ __align__(128) RevSmem rs;
-  Smem& sm = rs.g;
-  const int64_t b0 = int64_t(blockIdx.x) * kTile + 2 * threadIdx.x;
-  const bool live = b0 < B;
-  const int64_t rem = B - int64_t(blockIdx.x) * kTile;
-  const uint32_t seg = uint32_t(rem < kTile ? rem : kTile) * 4u;
-  setup(sm, w, 128);
-  if (threadIdx.x == 0) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(&rs.mbar_st)));
-    asm volatile("fence.mbarrier_init.release.cluster;");
-    stage_state(rs, states.p[count - 1], B, seg);
-  }
-  __syncthreads();
-  float2 dh[kD], dc[kD], c[kD];
-#pragma unroll
-  for (int j = 0; j < kD; ++j) {
-    dh[j] = live ? ldg2(adj_in + b0 + int64_t(j) * B) : make_float2(0.f, 0.f);
-    dc[j] = live ? ldg2(adj_in + b0 + int64_t(kD + j) * B) : make_float2(0.f, 0.f);
-  }
-  // prologue: gates of the last step
-  uint32_t st_phase = 0;
-  {
-    mbar_wait(&rs.mbar_st, st_phase);
-    st_phase ^= 1u;
-    float2 h[kD];
-#pragma unroll
-    for (int j = 0; j < kD; ++j) {
-      h[j] = *reinterpret_cast<const float2*>(&rs.st[j][2 * threadIdx.x]);
-      c[j] = *reinterpret_cast<const float2*>(&rs.st[kD + j][2 * threadIdx.x]);
-    }
-    stage_operands(sm, h, load_bias(xbs_all, from + count - 1));
-    gates_issue_at(sm, 0);  // every thread has read rs.st
-    if (count > 1 && threadIdx.x == 0) stage_state(rs, states.p[count - 2], B, seg);
-  }
-  uint32_t g_phase = 0;
-  float xb = count > 1 ? load_bias(xbs_all, from + count - 2) : 0.f;
-  for (int i = count - 1; i >= 0; --i) {
-    const uint32_t cur = uint32_t((count - 1 - i) & 1) * 64u;
-    mbar_wait(&sm.mbar, g_phase);  // gates of step i are in TMEM
-    g_phase ^= 1u;
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    float2 cn[kD];
-    if (i > 0) {  // stage step i-1 and start its gate MMAs under this step's epilogue
-      mbar_wait(&rs.mbar_st, st_phase);
-      st_phase ^= 1u;
-      float2 h[kD];
-#pragma unroll
-      for (int j = 0; j < kD; ++j) {
-        h[j] = *reinterpret_cast<const float2*>(&rs.st[j][2 * threadIdx.x]);
-        cn[j] = *reinterpret_cast<const float2*>(&rs.st[kD + j][2 * threadIdx.x]);
-      }
-      stage_operands(sm, h, xb);
-      if (i > 1) xb = load_bias(xbs_all, from + i - 2);
-      gates_issue_at(sm, 64u - cur);
-      if (i > 1 && threadIdx.x == 0) stage_state(rs, states.p[i - 2], B, seg);
-    }
-    float2 acc[kD];
-#pragma unroll
-    for (int m = 0; m < kD; ++m) acc[m] = bc(0.0f);
-#pragma unroll
-    for (int u = 0; u < kD; u += 2) {
-      float2 pre[2][4];
-      read_units_at(sm, cur, u, pre);
-#pragma unroll
-      for (int q = 0; q < 2; ++q) {
-        const int j = u + q;
-        float2 daf, dai, dao, dag;
-        bwd_unit_u(pre[q][0], pre[q][1], pre[q][2], pre[q][3], c[j], dh[j], dc[j], daf, dai, dao, dag, dc[j]);
-#pragma unroll
-        for (int m = 0; m < kD; ++m) {
-          acc[m] = fma2(bc(w.wu[0][j][m]), daf, acc[m]);
-          acc[m] = fma2(bc(w.wu[1][j][m]), dai, acc[m]);
-          acc[m] = fma2(bc(w.wu[2][j][m]), dao, acc[m]);
-          acc[m] = fma2(bc(w.wu[3][j][m]), dag, acc[m]);
-        }
-      }
-    }
-#pragma unroll
-    for (int m = 0; m < kD; ++m) {
-      dh[m] = acc[m];
-      c[m] = cn[m];
-    }
-  }
-  if (live) {
-#pragma unroll
-    for (int j = 0; j < kD; ++j) {
-      stg2(adj_out + b0 + int64_t(j) * B, dh[j]);
-      stg2(adj_out + b0 + int64_t(kD + j) * B, dc[j]);
-    }
-  }
-  teardown(sm, 128);
-}
-
-// ---- reverse run with both matvecs on the tensor cores ---------------------
-// Step i: gates G = [h 1] . [W xb]^T as in rev_tc (MMA1, 3xTF32, TMEM cols
-// [0, 64)); each thread turns its rows' pre-activations into the scaled gate
-// adjoints da (bwd_unit) and writes them back into TMEM as the A operand of
-// the transposed matvec dh = da . B2^T, B2[m][4 j + g] = s_g W_g[j][m]:
-//   da_hi (tf32 bits) over G in place, da_lo = da - da_hi as packed bf16
-//   (even k in the low half) in cols [64, 96);
-//   MMA2: da_hi x B2_hi + da_hi x B2_lo (kind::tf32, 4 K-steps) + da_lo x B2
-//   (kind::f16, bf16, 2 K-steps) -> D2 (fp32) in cols [96, 128), 16 per tile.
-// da_lo carries <= 2^-11 |da| and its bf16 rounding adds <= 2^-20 |da|, the
-// order of the 3xTF32 split's own dropped term (tools/umma_ts_probe.cu:
-// rel. error 9.4e-7 vs 6.5e-7 for 3xTF32).  128 TMEM columns per CTA.
-constexpr uint32_t kN2 = 16;                   // MMA2 N (m = 0..7 real, 8..15 zero)
-constexpr uint32_t kLBO2 = 256, kSBO2 = 128;   // B2: K chunks of 16 B, 2 row groups each
-constexpr uint32_t kIdescT2 = (1u << 4) | (2u << 7) | (2u << 10) | ((kN2 >> 3) << 17) | ((128u >> 4) << 24);
-constexpr uint32_t kIdescB2 = (1u << 4) | (1u << 7) | (1u << 10) | ((kN2 >> 3) << 17) | ((128u >> 4) << 24);
-constexpr uint32_t kColLo = 64, kColD2 = 96, kCols2 = 128;
-
-struct Rev2Smem {
-  Smem g;
-  float st[2 * kD][kTile];                  // prefetched taped state
-  unsigned char b2h[kN2 * kN * 4];          // tf32 hi, K-major, (k/4)*LBO + (r/8)*SBO + (r%8)*16 + (k%4)*4
-  unsigned char b2l[kN2 * kN * 4];          // tf32 lo
-  unsigned char b2b[kN2 * kN * 2];          // bf16, (k/8)*LBO + (r/8)*SBO + (r%8)*16 + (k%8)*2
-  uint64_t mbar_st, mbar2;
-};
-
-__device__ __forceinline__ uint64_t desc2(uint32_t addr) {
-  return uint64_t((addr >> 4) & 0x3FFF) | (uint64_t((kLBO2 >> 4) & 0x3FFF) << 16) |
-         (uint64_t((kSBO2 >> 4) & 0x3FFF) << 32) | (uint64_t(1) << 46);
-}
-__device__ __forceinline__ void mma_ts(uint32_t d, uint32_t a_tmem, uint64_t b, uint32_t idesc, uint32_t acc,
-                                       bool f16) {
-  if (f16)
-    asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-                 "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d),
-                 "r"(a_tmem), "l"(b), "r"(idesc), "r"(acc));
-  else
-    asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-                 "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d),
-                 "r"(a_tmem), "l"(b), "r"(idesc), "r"(acc));
-}
-__device__ __forceinline__ uint32_t bf16x2(float even, float odd) {  // even k -> low half
-  uint32_t r;
-  asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(odd), "f"(even));
-  return r;
-}
-__device__ __forceinline__ void st8(uint32_t addr, const uint32_t (&v)[8]) {
-  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(addr), "r"(v[0]),
-               "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7])
-               : "memory");
-}
-__device__ __forceinline__ void st4(uint32_t addr, const uint32_t (&v)[4]) {
-  asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1,%2,%3,%4};" ::"r"(addr), "r"(v[0]), "r"(v[1]),
-               "r"(v[2]), "r"(v[3])
-               : "memory");
-}
-
-// B2 (constant): rows m < 8 = scaled W columns, rows 8..15 zero.
-__device__ __forceinline__ void setup_b2(Rev2Smem& rs, const Weights& w) {
-  for (int i = threadIdx.x; i < int(kN2) * kN; i += kThreads) {
-    const int m = i / kN, k = i % kN, j = k >> 2, g = k & 3;
-    const float x = m < kD ? w.ws[g][j][m] : 0.f;
-    const int o32 = (k / 4) * kLBO2 + (m / 8) * kSBO2 + (m % 8) * 16 + (k % 4) * 4;
-    const int o16 = (k / 8) * kLBO2 + (m / 8) * kSBO2 + (m % 8) * 16 + (k % 8) * 2;
-    *reinterpret_cast<float*>(rs.b2h + o32) = hi_part(x);
-    *reinterpret_cast<float*>(rs.b2l + o32) = x - hi_part(x);
-    *reinterpret_cast<__nv_bfloat16*>(rs.b2b + o16) = __float2bfloat16_rn(x);
-  }
-}
-
-// Gate adjoints of unit pair (u, u+1) -> TMEM A operand of both tiles.
-__device__ __forceinline__ void store_da(uint32_t tmem_lane, int u, const float2 (&v)[8]) {
-  float2 hi[8], lo[8];
-#pragma unroll
-  for (int q = 0; q < 8; ++q) {
-    hi[q] = make_float2(hi_part(v[q].x), hi_part(v[q].y));
-    lo[q] = sub2(v[q], hi[q]);
-  }
-  uint32_t h0[8], h1[8], l0[4], l1[4];
-#pragma unroll
-  for (int q = 0; q < 8; ++q) {
-    h0[q] = __float_as_uint(hi[q].x);
-    h1[q] = __float_as_uint(hi[q].y);
-  }
-#pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    l0[q] = bf16x2(lo[2 * q].x, lo[2 * q + 1].x);
-    l1[q] = bf16x2(lo[2 * q].y, lo[2 * q + 1].y);
-  }
-  st8(tmem_lane + uint32_t(4 * u), h0);
-  st8(tmem_lane + uint32_t(kN + 4 * u), h1);
-  st4(tmem_lane + kColLo + uint32_t(2 * u), l0);
-  st4(tmem_lane + kColLo + kN2 + uint32_t(2 * u), l1);
-}
-
-// Fused run of Reverse actions, both matvecs on the tensor cores (PF: taped
-// state streamed into shared memory one step ahead, as in rev_tc<true>).
-template <bool NR>
-__global__ void __launch_bounds__(kThreads, 4)
-    rev_tc2(const float* __restrict__ adj_in, float* __restrict__ adj_out, int64_t B,
-            const float* __restrict__ xbs_all, int64_t from, int count, const __grid_constant__ Weights w,
-            const __grid_constant__ StatePtrs states) {
-  __shared__ __align__(128) Rev2Smem rs;
-  Smem& sm = rs.g;
-  const int64_t b0 = int64_t(blockIdx.x) * kTile + 2 * threadIdx.x;
-  const bool live = b0 < B;
-  const int64_t rem = B - int64_t(blockIdx.x) * kTile;
-  const uint32_t seg = uint32_t(rem < kTile ? rem : kTile) * 4u;
-  setup(sm, w, kCols2);
-  setup_b2(rs, w);
-  if (threadIdx.x == 0) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(&rs.mbar_st)));
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(&rs.mbar2)));
-    asm volatile("fence.mbarrier_init.release.cluster;");
-    stage_state(rs, states.p[count - 1], B, seg);
-  }
-  __syncthreads();
-  const uint32_t lane = uint32_t((threadIdx.x >> 5) * 32) << 16;
-  float2 dh[kD], dc[kD];
-#pragma unroll
-  for (int j = 0; j < kD; ++j) {
-    dh[j] = live ? ldg2(adj_in + b0 + int64_t(j) * B) : make_float2(0.f, 0.f);
-    dc[j] = live ? ldg2(adj_in + b0 + int64_t(kD + j) * B) : make_float2(0.f, 0.f);
-  }
-  int phase = 0;
-  float xb = load_bias(xbs_all, from + count - 1);
-  for (int i = count - 1; i >= 0; --i, ++phase) {
-    float2 h[kD], c[kD];
-    mbar_wait(&rs.mbar_st, uint32_t(phase & 1));
-#pragma unroll
-    for (int j = 0; j < kD; ++j) {
-      h[j] = *reinterpret_cast<const float2*>(&rs.st[j][2 * threadIdx.x]);
-      c[j] = *reinterpret_cast<const float2*>(&rs.st[kD + j][2 * threadIdx.x]);
-    }
-    stage_operands(sm, h, xb);
-    if (i > 0) xb = load_bias(xbs_all, from + i - 1);
-    gates_issue(sm);  // after its barrier every thread has read rs.st
-    if (i > 0 && threadIdx.x == 0) stage_state(rs, states.p[i - 1], B, seg);
-    gates_wait(sm, uint32_t(phase & 1));
-#pragma unroll
-    for (int u = 0; u < kD; u += 2) {
-      float2 pre[2][4];
-      read_units(sm, u, pre);
-      float2 da[8];
-#pragma unroll
-      for (int q = 0; q < 2; ++q) {
-        const int j = u + q;
-        if (NR)
-          bwd_unit_nr(pre[q][0], pre[q][1], pre[q][2], pre[q][3], c[j], dh[j], dc[j], da[4 * q], da[4 * q + 1],
-                      da[4 * q + 2], da[4 * q + 3], dc[j]);
-        else
-          bwd_unit(pre[q][0], pre[q][1], pre[q][2], pre[q][3], c[j], dh[j], dc[j], da[4 * q], da[4 * q + 1],
-                   da[4 * q + 2], da[4 * q + 3], dc[j]);
-      }
-      store_da(sm.tmem + lane, u, da);
-    }
-    // MMA2: dh = da . B2^T per tile
-    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-#pragma unroll
-      for (int t = 0; t < 2; ++t) {
-        const uint32_t d2 = sm.tmem + kColD2 + uint32_t(t) * kN2;
-        const uint32_t ahi = sm.tmem + uint32_t(t * kN), alo = sm.tmem + kColLo + uint32_t(t) * kN2;
-#pragma unroll
-        for (int ks = 0; ks < 4; ++ks) {  // tf32: K = 8 per MMA
-          mma_ts(d2, ahi + 8 * ks, desc2(su32(rs.b2h) + ks * 2 * kLBO2), kIdescT2, ks ? 1u : 0u, false);
-          mma_ts(d2, ahi + 8 * ks, desc2(su32(rs.b2l) + ks * 2 * kLBO2), kIdescT2, 1u, false);
-        }
-#pragma unroll
-        for (int ks = 0; ks < 2; ++ks)  // bf16: K = 16 per MMA (8 packed columns)
-          mma_ts(d2, alo + 8 * ks, desc2(su32(rs.b2b) + ks * 2 * kLBO2), kIdescB2, 1u, true);
-      }
-      asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-                       su32(&rs.mbar2))
-                   : "memory");
-    }
-    mbar_wait(&rs.mbar2, uint32_t(phase & 1));
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    {
-      float a[8], b[8];
-      ld8(sm.tmem + lane + kColD2, a);
-      ld8(sm.tmem + lane + kColD2 + kN2, b);
-      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-      for (int m = 0; m < kD; ++m) dh[m] = make_float2(a[m], b[m]);
-    }
-  }
-  if (live) {
-#pragma unroll
-    for (int j = 0; j < kD; ++j) {
-      stg2(adj_out + b0 + int64_t(j) * B, dh[j]);
-      stg2(adj_out + b0 + int64_t(kD + j) * B, dc[j]);
-    }
-  }
-  teardown(sm, kCols2);
 }
 
 }  // namespace tc

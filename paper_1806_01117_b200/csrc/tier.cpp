@@ -51,6 +51,8 @@ struct TierTicket {
   bool complete = false;
   double hold_seconds = 0.0;  // throttle: host-func sleep on the copy stream
   cudaEvent_t t0 = nullptr, t1 = nullptr;  // timeline marks (copy start / done)
+  bool waited = false;    // waited / retired by its owner: the slot may be recycled
+  bool captured = false;  // enqueued under CUDA-graph capture: a graph node refers to it
   // file stage
   std::shared_ptr<AsyncStatus> async;
   ackpt_tier* tier = nullptr;
@@ -86,7 +88,13 @@ struct ackpt_tier {
   std::vector<unsigned char*> slot_ptr;
   std::vector<int64_t> free_slots;
   std::unordered_map<int64_t, ackpt::KeyEntry> keys;
-  std::deque<ackpt::TierTicket> tickets;
+  // Tickets by id (ids increase; node-based map, so references stay valid).
+  // Waited, uncaptured tickets are erased (compact_tickets), so a long-lived
+  // backend holds O(in-flight) tickets; a recycled ticket that failed keeps
+  // its error for a repeated wait (recycled_errors).
+  std::unordered_map<int64_t, ackpt::TierTicket> tickets;
+  int64_t next_ticket = 0;
+  std::unordered_map<int64_t, std::pair<int, std::string>> recycled_errors;
   std::vector<cudaEvent_t> event_pool;
   std::vector<cudaEvent_t> all_events;
   bool timing = false;                   // record timeline marks around transfers
@@ -184,14 +192,45 @@ void reserve_slots(ackpt_tier* t, int64_t count) {
   }
 }
 
-ackpt_ticket add_ticket(ackpt_tier* t, TierTicket&& tk) {
-  t->tickets.push_back(std::move(tk));
-  return ackpt_ticket(t->tickets.size() - 1);
+// Erase waited tickets (their events went back to the pool at retire; no I/O
+// job or graph node refers to them any more).
+void compact_tickets(ackpt_tier* t) {
+  for (auto it = t->tickets.begin(); it != t->tickets.end();) {
+    TierTicket& f = it->second;
+    if (!f.complete || !f.waited || f.captured) {
+      ++it;
+      continue;
+    }
+    int code = f.err;
+    std::string msg = f.msg;
+    if (code == ACKPT_OK && f.async) {
+      code = f.async->err.load(std::memory_order_acquire);
+      msg = f.async->msg;
+    }
+    if (code != ACKPT_OK) t->recycled_errors[it->first] = {code, msg};
+    it = t->tickets.erase(it);
+  }
 }
 
-TierTicket& get_ticket(ackpt_tier* t, ackpt_ticket id) {
-  if (id < 0 || size_t(id) >= t->tickets.size()) fail(ACKPT_VALUE_ERROR, "unknown transfer ticket");
-  return t->tickets[size_t(id)];
+ackpt_ticket add_ticket(ackpt_tier* t, TierTicket&& tk) {
+  static constexpr size_t kCompactAt = 256;
+  if (t->tickets.size() >= kCompactAt && t->next_ticket % kCompactAt == 0) compact_tickets(t);
+  const int64_t id = t->next_ticket++;
+  t->tickets.emplace(id, std::move(tk));
+  return ackpt_ticket(id);
+}
+
+// nullptr: a recycled ticket (waited before); see recycled_status.
+TierTicket* find_ticket(ackpt_tier* t, ackpt_ticket id) {
+  if (id < 0 || id >= t->next_ticket) fail(ACKPT_VALUE_ERROR, "unknown transfer ticket");
+  auto it = t->tickets.find(id);
+  return it == t->tickets.end() ? nullptr : &it->second;
+}
+int recycled_status(const ackpt_tier* t, ackpt_ticket id, std::string* msg) {
+  auto it = t->recycled_errors.find(id);
+  if (it == t->recycled_errors.end()) return ACKPT_OK;
+  if (msg) *msg = it->second.second;
+  return it->second.first;
 }
 
 void hold(ackpt_tier* t, cudaStream_t s, TierTicket& tk, int64_t bytes) {
@@ -308,18 +347,32 @@ void write_ckpt(TierTicket* tk, std::string* retired_out = nullptr) {
   put_le(trailer, reg ^ 0xFFFFFFFFu, 4);
   if (!err && ::pwrite(fd, trailer, kTrailer, off_t(kHeader + tk->len)) != kTrailer) err = errno ? errno : EIO;
   if (::close(fd) != 0 && !err) err = errno;
-  // Publish with tmp + rename like the reference (storage.py:109-118) so
-  // `path` never holds a partial checkpoint -- but never rename OVER an
-  // existing file: ext4 (auto_da_alloc) then forces writeback of the new
-  // file's data inside rename(), 15-25 ms per 64 MiB on the box, stalling
-  // the compute stream.  The previous file keeps a second name until the new
-  // one is in place and is deleted by a background thread.
+  // Publish atomically like the reference's tmp + os.replace
+  // (storage.py:109-118), so `path` always holds a complete checkpoint -- but
+  // never rename OVER an existing file: ext4 (auto_da_alloc) then forces
+  // writeback of the new file's data inside rename(), 15-25 ms per 64 MiB on
+  // the box, stalling the compute stream.  renameat2(RENAME_EXCHANGE) swaps
+  // the two names in one step instead; the tmp name then holds the previous
+  // checkpoint, which is unlinked off the critical path.  Without an existing
+  // file a plain rename publishes; on file systems without RENAME_EXCHANGE the
+  // old file is moved aside first and moved back if the rename fails.
   std::string retired;
   if (!err) {
-    retired = path + ".old." + std::to_string(reinterpret_cast<uintptr_t>(tk));
-    if (::link(path.c_str(), retired.c_str()) == 0) ::unlink(path.c_str());
-    else retired.clear();  // no previous file
-    if (std::rename(tmp.c_str(), path.c_str()) != 0) err = errno;
+    if (::renameat2(AT_FDCWD, tmp.c_str(), AT_FDCWD, path.c_str(), RENAME_EXCHANGE) == 0) {
+      // free the tmp name for the next store of this key (a rename onto a new
+      // name: no data writeback); the old data is unlinked in the background
+      retired = path + ".old." + std::to_string(reinterpret_cast<uintptr_t>(tk));
+      if (std::rename(tmp.c_str(), retired.c_str()) != 0) retired = tmp;
+    } else if (errno == ENOENT) {  // no previous file
+      if (std::rename(tmp.c_str(), path.c_str()) != 0) err = errno;
+    } else {
+      retired = path + ".old." + std::to_string(reinterpret_cast<uintptr_t>(tk));
+      if (std::rename(path.c_str(), retired.c_str()) != 0) retired.clear();
+      if (std::rename(tmp.c_str(), path.c_str()) != 0) {
+        err = errno;
+        if (!retired.empty() && std::rename(retired.c_str(), path.c_str()) == 0) retired.clear();
+      }
+    }
   }
   if (retired_out) *retired_out = retired;
   else if (!retired.empty()) std::thread([retired] { ::unlink(retired.c_str()); }).detach();
@@ -545,6 +598,16 @@ void io_stop(ackpt_tier* t) {
   if (t->fetch_thr.joinable()) t->fetch_thr.join();
 }
 
+bool capturing(void* after_stream) {
+  if (!after_stream) return false;
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(static_cast<cudaStream_t>(after_stream), &cs) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return cs != cudaStreamCaptureStatusNone;
+}
+
 // File-stage transfers go through the I/O threads unless the enqueue is being
 // captured into a CUDA graph (or a throttle needs the host-function hold).
 bool use_io_threads(ackpt_tier* t, void* after_stream) {
@@ -560,14 +623,30 @@ bool use_io_threads(ackpt_tier* t, void* after_stream) {
   return io_threads_on(t);
 }
 
-// Length of an existing CKPT file (header only), -1 when absent / unreadable.
-int64_t file_payload_len(const ackpt_tier* t, int64_t key) {
-  FILE* f = std::fopen(ckpt_path(t, key).c_str(), "rb");
-  if (!f) return -1;
+// Payload length of an existing CKPT file: -1 when absent, -2 when the header
+// is not a valid CKPT header for the file's size (bad magic / version, or
+// length + header + trailer != file size; `why` says which).  Allocations are
+// never sized from an unvalidated header; the fetch of such a file fails with
+// ChecksumMismatch at wait, like decode_checkpoint (storage.py:83-106).
+int64_t file_payload_len(const ackpt_tier* t, int64_t key, std::string* why = nullptr) {
+  const int fd = ::open(ckpt_path(t, key).c_str(), O_RDONLY | O_CLOEXEC);
+  if (fd < 0) return -1;
+  struct stat sb;
   unsigned char header[kHeader];
-  const bool ok = std::fread(header, 1, kHeader, f) == size_t(kHeader);
-  std::fclose(f);
-  return ok ? int64_t(get_le(header + 14, 8)) : 0;
+  const bool got = ::fstat(fd, &sb) == 0 && ::pread(fd, header, kHeader, 0) == kHeader;
+  ::close(fd);
+  auto bad = [&](const std::string& w) {
+    if (why) *why = ckpt_path(t, key) + ": " + w;
+    return int64_t(-2);
+  };
+  if (!got) return bad("checkpoint truncated");
+  if (std::memcmp(header, "CKPT", 4) != 0) return bad("bad magic bytes");
+  if (get_le(header + 4, 2) != 1) return bad("unsupported format version");
+  const uint64_t length = get_le(header + 14, 8);
+  if (length > uint64_t(sb.st_size) || uint64_t(sb.st_size) != length + kHeader + kTrailer)
+    return bad("length field says " + std::to_string(length) + ", file holds " +
+               std::to_string(int64_t(sb.st_size) - kHeader - kTrailer));
+  return int64_t(length);
 }
 
 void ensure_stage(ackpt_tier* t, int64_t bytes) {
@@ -643,40 +722,49 @@ void tier_reserve_keys(ackpt_tier* t, const std::vector<int64_t>& keys, int64_t 
 }
 cudaEvent_t tier_ticket_event(ackpt_tier* t, ackpt_ticket id) {
   std::lock_guard<std::mutex> lk(t->mu);
-  TierTicket& tk = get_ticket(t, id);
-  return tk.complete ? nullptr : tk.done;
+  TierTicket* tk = find_ticket(t, id);
+  return (!tk || tk->complete) ? nullptr : tk->done;
 }
 // Asynchronous (file-stage) status of a ticket whose event has completed.
 int tier_async_status(ackpt_tier* t, ackpt_ticket id, std::string* msg) {
   std::lock_guard<std::mutex> lk(t->mu);
-  TierTicket& tk = get_ticket(t, id);
-  if (!tk.async) return ACKPT_OK;
-  const int e = tk.async->err.load(std::memory_order_acquire);
-  if (e != ACKPT_OK && msg) *msg = tk.async->msg;
+  TierTicket* tk = find_ticket(t, id);
+  if (!tk) return recycled_status(t, id, msg);
+  if (!tk->async) return ACKPT_OK;
+  const int e = tk->async->err.load(std::memory_order_acquire);
+  if (e != ACKPT_OK && msg) *msg = tk->async->msg;
   return e;
 }
 int tier_ticket_status(ackpt_tier* t, ackpt_ticket id, std::string* msg) {
   std::lock_guard<std::mutex> lk(t->mu);
-  TierTicket& tk = get_ticket(t, id);
-  if (msg) *msg = tk.msg;
-  return tk.err;
+  TierTicket* tk = find_ticket(t, id);
+  if (!tk) return recycled_status(t, id, msg);
+  if (msg) *msg = tk->msg;
+  return tk->err;
 }
 // Clear a file-stage ticket's asynchronous status before a CUDA-graph replay
 // re-runs its host functions.
 void tier_reset_async(ackpt_tier* t, ackpt_ticket id) {
   std::lock_guard<std::mutex> lk(t->mu);
-  TierTicket& tk = get_ticket(t, id);
-  if (tk.async) tk.async->err.store(ACKPT_OK, std::memory_order_release);
+  TierTicket* tk = find_ticket(t, id);  // graph tickets are never recycled
+  if (tk && tk->async) tk->async->err.store(ACKPT_OK, std::memory_order_release);
 }
 // Drain the copy streams and forget the per-key copy-ordering events, so no
 // stream wait crosses a CUDA-graph capture boundary (before a capture, after
 // a graphed run): the events last recorded inside a capture are graph nodes.
+// The per-key events are then re-recorded on the idle copy streams (outside
+// any capture), so a later eager transfer or ensure_storage can wait on them.
 void tier_quiesce(ackpt_tier* t) {
   std::lock_guard<std::mutex> lk(t->mu);
   ACKPT_CUDA_CHECK(cudaStreamSynchronize(t->d2h));
   ACKPT_CUDA_CHECK(cudaStreamSynchronize(t->h2d));
   io_drain(t);
-  for (auto& kv : t->keys) kv.second.fetched = false;
+  for (auto& kv : t->keys) {
+    KeyEntry& ke = kv.second;
+    if (ke.last_store) ACKPT_CUDA_CHECK(cudaEventRecord(ke.last_store, t->d2h));
+    if (ke.last_fetch) ACKPT_CUDA_CHECK(cudaEventRecord(ke.last_fetch, t->h2d));
+    ke.fetched = false;
+  }
 }
 void tier_set_timing(ackpt_tier* t, bool on) {
   std::lock_guard<std::mutex> lk(t->mu);
@@ -684,15 +772,21 @@ void tier_set_timing(ackpt_tier* t, bool on) {
 }
 bool tier_ticket_times(ackpt_tier* t, ackpt_ticket id, cudaEvent_t* t0, cudaEvent_t* t1) {
   std::lock_guard<std::mutex> lk(t->mu);
-  TierTicket& tk = get_ticket(t, id);
-  *t0 = tk.t0;
-  *t1 = tk.t1;
-  return tk.t0 && tk.t1;
+  TierTicket* tk = find_ticket(t, id);
+  if (!tk) return false;
+  *t0 = tk->t0;
+  *t1 = tk->t1;
+  return tk->t0 && tk->t1;
 }
 
+// The engine's tickets once its run drained (every transfer of a pass has
+// completed by then): events back to the pool, the slot recyclable.
 void tier_retire(ackpt_tier* t, ackpt_ticket id) {
   std::lock_guard<std::mutex> lk(t->mu);
-  retire(t, get_ticket(t, id));
+  TierTicket* tk = find_ticket(t, id);
+  if (!tk) return;
+  retire(t, *tk);
+  tk->waited = true;
 }
 int64_t tier_slot_bytes(const ackpt_tier* t) { return t->slot_bytes; }
 cudaStream_t tier_d2h(const ackpt_tier* t) { return t->d2h; }
@@ -795,7 +889,8 @@ ACKPT_API int ackpt_tier_begin_store(ackpt_tier* t, int64_t key, int64_t step, c
       ke.step = step;
       ke.len = bytes;
       ackpt_ticket id = ackpt::add_ticket(t, std::move(tk));
-      ackpt::TierTicket& ref = t->tickets[size_t(id)];
+      ackpt::TierTicket& ref = *ackpt::find_ticket(t, id);
+      ref.captured = ackpt::capturing(after_stream);
       ref.tier = t;
       ref.len = bytes;
       ref.async = std::make_shared<ackpt::AsyncStatus>();
@@ -842,7 +937,8 @@ ACKPT_API int ackpt_tier_begin_store(ackpt_tier* t, int64_t key, int64_t step, c
     ke.step = step;
     ke.len = bytes;
     ackpt_ticket id = ackpt::add_ticket(t, std::move(tk));
-    ackpt::TierTicket& ref = t->tickets[size_t(id)];
+    ackpt::TierTicket& ref = *ackpt::find_ticket(t, id);
+      ref.captured = ackpt::capturing(after_stream);
     ackpt::hold(t, t->d2h, ref, bytes);
     ref.done = ackpt::new_event(t);
     ACKPT_CUDA_CHECK(cudaEventRecord(ref.done, t->d2h));
@@ -866,11 +962,12 @@ ACKPT_API int ackpt_tier_begin_fetch(ackpt_tier* t, int64_t key, void* dst, int6
     if (t->file_mode) {
       // Keys stored earlier in this tier, or CKPT files already on disk (resume).
       int64_t len = -1;
+      std::string why;
       if (it != t->keys.end() && it->second.stored) len = it->second.len;
-      else len = ackpt::file_payload_len(t, key);
+      else len = ackpt::file_payload_len(t, key, &why);
       if (len < 0) {
-        tk.err = ACKPT_MISSING_KEY;
-        tk.msg = ackpt::ckpt_path(t, key);
+        tk.err = len == -1 ? ACKPT_MISSING_KEY : ACKPT_CHECKSUM_MISMATCH;
+        tk.msg = len == -1 ? ackpt::ckpt_path(t, key) : why;
         tk.complete = true;
         *out = ackpt::add_ticket(t, std::move(tk));
         return;
@@ -895,7 +992,8 @@ ACKPT_API int ackpt_tier_begin_fetch(ackpt_tier* t, int64_t key, void* dst, int6
       if (ke.stored && !threads) ACKPT_CUDA_CHECK(cudaStreamWaitEvent(t->h2d, ke.last_store, 0));
       cudaEvent_t m0 = ackpt::mark(t, t->h2d);
       ackpt_ticket id = ackpt::add_ticket(t, std::move(tk));
-      ackpt::TierTicket& ref = t->tickets[size_t(id)];
+      ackpt::TierTicket& ref = *ackpt::find_ticket(t, id);
+      ref.captured = ackpt::capturing(after_stream);
       ref.tier = t;
       ref.len = len;
       ref.async = std::make_shared<ackpt::AsyncStatus>();
@@ -950,7 +1048,8 @@ ACKPT_API int ackpt_tier_begin_fetch(ackpt_tier* t, int64_t key, void* dst, int6
       ACKPT_CUDA_CHECK(cudaMemcpyAsync(dst, ackpt::key_ptr(t, ke), size_t(ke.len),
                                        cudaMemcpyHostToDevice, t->h2d));
     ackpt_ticket id = ackpt::add_ticket(t, std::move(tk));
-    ackpt::TierTicket& ref = t->tickets[size_t(id)];
+    ackpt::TierTicket& ref = *ackpt::find_ticket(t, id);
+      ref.captured = ackpt::capturing(after_stream);
     ackpt::hold(t, t->h2d, ref, ke.len);
     ref.done = ackpt::new_event(t);
     ACKPT_CUDA_CHECK(cudaEventRecord(ref.done, t->h2d));
@@ -965,20 +1064,32 @@ ACKPT_API int ackpt_tier_begin_fetch(ackpt_tier* t, int64_t key, void* dst, int6
 
 ACKPT_API int ackpt_tier_wait(ackpt_tier* t, ackpt_ticket ticket, int64_t* step_out) {
   cudaEvent_t ev = nullptr;
+  bool recycled = false;
   int rc = ackpt::guard([&] {
     std::lock_guard<std::mutex> lk(t->mu);
-    ackpt::TierTicket& tk = ackpt::get_ticket(t, ticket);
-    if (step_out) *step_out = tk.step;
-    if (tk.err != ACKPT_OK) ackpt::fail(tk.err, tk.msg);
-    ev = tk.complete ? nullptr : tk.done;
+    ackpt::TierTicket* tk = ackpt::find_ticket(t, ticket);
+    if (!tk) {  // waited before and recycled: idempotent, the first wait's status
+      recycled = true;
+      std::string msg;
+      const int e = ackpt::recycled_status(t, ticket, &msg);
+      if (e != ACKPT_OK) ackpt::fail(e, msg);
+      return;
+    }
+    if (step_out) *step_out = tk->step;
+    if (tk->err != ACKPT_OK) {
+      tk->waited = true;
+      ackpt::fail(tk->err, tk->msg);
+    }
+    ev = tk->complete ? nullptr : tk->done;
   });
-  if (rc != ACKPT_OK) return rc;
+  if (rc != ACKPT_OK || recycled) return rc;
   // Block without holding the lock (other threads may issue transfers).
   return ackpt::guard([&] {
     if (ev) ACKPT_CUDA_CHECK(cudaEventSynchronize(ev));
     std::lock_guard<std::mutex> lk(t->mu);
-    ackpt::TierTicket& tk = ackpt::get_ticket(t, ticket);
+    ackpt::TierTicket& tk = *ackpt::find_ticket(t, ticket);  // not recyclable before waited
     ackpt::retire(t, tk);
+    tk.waited = true;
     if (step_out) *step_out = tk.step;
     if (tk.async) {  // file-stage errors, raised by the worker side (storage.py:271-278)
       const int e = tk.async->err.load(std::memory_order_acquire);
@@ -990,10 +1101,16 @@ ACKPT_API int ackpt_tier_wait(ackpt_tier* t, ackpt_ticket ticket, int64_t* step_
 ACKPT_API int ackpt_tier_stream_wait(ackpt_tier* t, ackpt_ticket ticket, void* stream) {
   return ackpt::guard([&] {
     std::lock_guard<std::mutex> lk(t->mu);
-    ackpt::TierTicket& tk = ackpt::get_ticket(t, ticket);
-    if (tk.err != ACKPT_OK) ackpt::fail(tk.err, tk.msg);
-    if (!tk.complete && tk.done)
-      ACKPT_CUDA_CHECK(cudaStreamWaitEvent(static_cast<cudaStream_t>(stream), tk.done, 0));
+    ackpt::TierTicket* tk = ackpt::find_ticket(t, ticket);
+    if (!tk) {
+      std::string msg;
+      const int e = ackpt::recycled_status(t, ticket, &msg);
+      if (e != ACKPT_OK) ackpt::fail(e, msg);
+      return;
+    }
+    if (tk->err != ACKPT_OK) ackpt::fail(tk->err, tk->msg);
+    if (!tk->complete && tk->done)
+      ACKPT_CUDA_CHECK(cudaStreamWaitEvent(static_cast<cudaStream_t>(stream), tk->done, 0));
   });
 }
 
@@ -1001,15 +1118,15 @@ ACKPT_API int ackpt_tier_poll(ackpt_tier* t, ackpt_ticket ticket) {
   int ready = ACKPT_OK;
   int rc = ackpt::guard([&] {
     std::lock_guard<std::mutex> lk(t->mu);
-    ackpt::TierTicket& tk = ackpt::get_ticket(t, ticket);
-    if (tk.complete) return;
-    cudaError_t e = cudaEventQuery(tk.done);
+    ackpt::TierTicket* tk = ackpt::find_ticket(t, ticket);
+    if (!tk || tk->complete) return;
+    cudaError_t e = cudaEventQuery(tk->done);
     if (e == cudaErrorNotReady) {
       ready = ACKPT_NOT_READY;
       return;
     }
     ACKPT_CUDA_CHECK(e);
-    ackpt::retire(t, tk);
+    ackpt::retire(t, *tk);
   });
   return rc != ACKPT_OK ? rc : ready;
 }
@@ -1019,7 +1136,7 @@ ACKPT_API int ackpt_tier_contains(ackpt_tier* t, int64_t key, int32_t* out) {
     std::lock_guard<std::mutex> lk(t->mu);
     auto it = t->keys.find(key);
     *out = (it != t->keys.end() && it->second.stored) ? 1 : 0;
-    if (!*out && t->file_mode) *out = ackpt::file_payload_len(t, key) >= 0 ? 1 : 0;
+    if (!*out && t->file_mode) *out = ackpt::file_payload_len(t, key) != -1 ? 1 : 0;  // the file exists
   });
 }
 
@@ -1028,8 +1145,10 @@ ACKPT_API int ackpt_tier_key_bytes(ackpt_tier* t, int64_t key, int64_t* out) {
     std::lock_guard<std::mutex> lk(t->mu);
     auto it = t->keys.find(key);
     if (t->file_mode && (it == t->keys.end() || !it->second.stored)) {
-      const int64_t len = ackpt::file_payload_len(t, key);
-      if (len < 0) ackpt::fail(ACKPT_MISSING_KEY, ackpt::ckpt_path(t, key));
+      std::string why;
+      const int64_t len = ackpt::file_payload_len(t, key, &why);
+      if (len == -1) ackpt::fail(ACKPT_MISSING_KEY, ackpt::ckpt_path(t, key));
+      if (len < 0) ackpt::fail(ACKPT_CHECKSUM_MISMATCH, why);
       *out = len;
       return;
     }
@@ -1063,8 +1182,19 @@ ACKPT_API int ackpt_tier_clear(ackpt_tier* t) {
       if (kv.second.last_fetch) cudaEventDestroy(kv.second.last_fetch);
     }
     t->keys.clear();
-    for (auto& tk : t->tickets) ackpt::retire(t, tk);
+    for (auto& kv : t->tickets) {
+      ackpt::retire(t, kv.second);
+      kv.second.waited = true;
+    }
+    ackpt::compact_tickets(t);
   });
 }
 
 }  // extern "C"
+
+extern "C" ACKPT_API int ackpt_tier_streams(ackpt_tier* t, void** d2h, void** h2d) {
+  return ackpt::guard([&] {
+    if (d2h) *d2h = t->d2h;
+    if (h2d) *h2d = t->h2d;
+  });
+}

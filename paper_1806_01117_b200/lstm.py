@@ -99,6 +99,18 @@ def random_cell(d: int, n: int, seed: int) -> LstmCell:
     return LstmCell(*w, *b, xs=xs, target=draw(d))
 
 
+def long_memory_cell(d: int, n: int, seed: int, forget_bias: float = 6.0) -> LstmCell:
+    """random_cell(d, n, seed) with ``forget_bias`` added to b_f: the forget
+    gate sits near 1 (sigmoid(6) = 0.9975), so the state adjoint decays slowly
+    and stays far above fp32 underflow at n = 10^4 (d = 8: per-sequence norms
+    1e-14 .. 3e-7), where the reference cell's adjoint is exactly 0 past
+    n ~ 190.  Same timing as random_cell; the workload of the long-chain
+    parity checks (tests, bench.py's parity leg)."""
+    cell = random_cell(d, n, seed)
+    cell.b_f = cell.b_f + forget_bias
+    return cell
+
+
 def pack_state(h: np.ndarray, c: np.ndarray) -> bytes:
     """Reference byte image [h, c] as little-endian float64 (lstm.py:99-100)."""
     return np.ascontiguousarray(np.concatenate([h, c]), dtype=_F8).tobytes()
@@ -234,15 +246,14 @@ def _stream() -> int:
 
 
 def set_kernel_family(name: str) -> None:
-    """Kernel family of the fused d=8 fp32 launches: "ffma2" (packed fp32
-    FMA), "tcgen05" (default: tensor cores, 3xTF32), "mixed" (tcgen05
-    advance / forward_many, ffma2 backward_many) or "mma" (warp-level
-    mma.sync tensor cores with register fragments, 3xTF32).  All meet the fp32
-    tolerance; they round differently, so switch only between executions."""
+    """Kernel family of the fused d=8 fp32 launches: "tcgen05" (default:
+    tensor cores, 3xTF32 gate products) or "ffma2" (packed fp32 FMA, the
+    documented fallback).  Both meet the fp32 tolerance; they round
+    differently, so switch only between executions."""
     N.check(N.lib.ackpt_set_fused_family(KERNEL_FAMILIES.index(name)))
 
 
-KERNEL_FAMILIES = ("ffma2", "tcgen05", "mixed", "mma")
+KERNEL_FAMILIES = ("ffma2", "tcgen05")
 
 
 def kernel_family() -> str:

@@ -277,12 +277,27 @@ class Level2Backend:
             N.check(N.lib.ackpt_tier_set_throttle(self._handle, float(latency), float(bandwidth)))
 
     # -- public API (storage.py:233-263) --------------------------------------
+    def _copy_streams(self, h: int):
+        """torch handles of the tier's D2H / H2D copy streams (cached)."""
+        if getattr(self, "_streams", None) is None or self._streams[0] != h:
+            d2h, h2d = C.c_void_p(), C.c_void_p()
+            N.check(N.lib.ackpt_tier_streams(h, C.byref(d2h), C.byref(h2d)))
+            self._streams = (h, torch.cuda.ExternalStream(d2h.value, device=self._device),
+                             torch.cuda.ExternalStream(h2d.value, device=self._device))
+        return self._streams[1], self._streams[2]
+
     def begin_store(self, key: int, payload: CheckpointPayload) -> TransferTicket:
+        """Asynchronous store; the payload must not be modified until the
+        ticket completed (the reference stores immutable bytes, storage.py:233).
+        The source block is tied to the D2H stream (record_stream), so even a
+        dropped ticket cannot let the caching allocator reuse it mid-copy."""
         src = as_device_bytes(payload.data, self._device)
         h = self._ensure(src.numel())
         out = C.c_int64(-1)
         stream = torch.cuda.current_stream(self._device).cuda_stream
         N.check(N.lib.ackpt_tier_begin_store(h, key, payload.step, src.data_ptr(), src.numel(), stream, C.byref(out)))
+        if src.numel():
+            src.record_stream(self._copy_streams(h)[0])
         return TransferTicket(self, "store", key, out.value, keep=src)
 
     def begin_fetch(self, key: int) -> TransferTicket:
@@ -293,6 +308,8 @@ class Level2Backend:
         out = C.c_int64(-1)
         stream = torch.cuda.current_stream(self._device).cuda_stream
         N.check(N.lib.ackpt_tier_begin_fetch(h, key, dst.data_ptr(), dst.numel(), stream, C.byref(out)))
+        if dst.numel():
+            dst.record_stream(self._copy_streams(h)[1])
         return TransferTicket(self, "fetch", key, out.value, keep=dst)
 
     def wait(self, ticket: TransferTicket) -> Optional[CheckpointPayload]:

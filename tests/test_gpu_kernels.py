@@ -103,7 +103,7 @@ def test_seed_and_loss(P):
         assert L.rel_l2(losses, L.loss(ocell, x.astype(npdt).astype(np.float64))) <= tol
 
 
-@pytest.fixture(params=["ffma2", "tcgen05", "mixed", "mma"])
+@pytest.fixture(params=["ffma2", "tcgen05"])
 def family(request, P):
     before = P.kernel_family()
     P.set_kernel_family(request.param)
@@ -114,7 +114,7 @@ def family(request, P):
 def _tensor_core_family(P, d, batch, dtype):
     # fused d=8 fp32 forward launches (even batch above the CTA-per-sequence
     # crossover, B > 2048) run on tcgen05 / mma with the 3xTF32 split
-    return (P.kernel_family() in ("tcgen05", "mixed", "mma") and d == 8 and dtype == "f32" and batch % 2 == 0
+    return (P.kernel_family() == "tcgen05" and d == 8 and dtype == "f32" and batch % 2 == 0
             and batch > 2048)
 
 

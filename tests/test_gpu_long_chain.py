@@ -1,0 +1,113 @@
+"""Long-chain parity that can fail.
+
+With the reference's random_cell the fp32 state adjoint is exactly 0 (or
+denormal noise) past n ~ 190, so bit-identity between strategies at long n
+compares zeros.  long_memory_cell (random_cell + forget-gate bias 6) keeps
+per-sequence adjoint norms at 1e-14 .. 3e-7 over n = 10^4 (d = 8), so these
+tests compare real numbers:
+
+* the headline configuration itself -- BASELINE config 2: d = 8, B = 2^20
+  (64 MiB fp32 state), n = 10^4, Multistage(999, I = 75), pinned-host tier,
+  fused tcgen05 launches and the per-step contract -- on 64 sampled sequences
+  against the float64 oracle executor (oracle/runtime_oracle.py, following
+  runtime.py:339-381 and lstm.py:132-152);
+* bit-identity across strategies at n = 400 with a non-zero adjoint.
+
+Tolerance: aggregate rel-L2 over the sampled sequences <= 2e-4.  An fp32
+numpy restatement of the same chain (every operation in fp32, same inputs)
+sits at 5.2e-5 from float64 at n = 10^4: the forget gate near 1 makes c an
+integrator over ~400 steps, so fp32 rounding of the forward trajectory
+accumulates; per-step kernel parity stays at 1e-5 (test_gpu_kernels.py).
+"""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import lstm_oracle as L
+from oracle import runtime_oracle as RO
+
+pytestmark = pytest.mark.gpu
+
+LONG_TOL = 2e-4
+
+
+@pytest.fixture(scope="module")
+def P():
+    import paper_1806_01117_b200 as pkg
+    import paper_1806_01117_b200.lstm as lstm
+
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    return pkg, lstm
+
+
+def _rows(batch, k=64):
+    return np.unique(np.linspace(0, batch - 1, k).astype(np.int64))
+
+
+def _oracle_adjoint(d, n, s0_rows):
+    """float64 oracle on the sampled sequences (FullStorage: the strategies
+    are bit-identical in the oracle, runtime.py:23-27)."""
+    adj, _ = RO.execute("full", L.long_memory_cell(d, n, 0), s0_rows)
+    return adj
+
+
+@pytest.mark.parametrize("fuse", [True, False], ids=["fused-tcgen05", "per-step"])
+def test_headline_config_adjoint_vs_oracle(P, fuse):
+    pkg, lstm = P
+    d, n, batch, slots, interval = 8, 10_000, 1 << 20, 999, 75
+    cell = lstm.long_memory_cell(d, n, 0)
+    ops = lstm.operator_pair(cell, batch, "f32")
+    s0 = lstm.random_states(d, 1, batch, "f32")
+    with pkg.PinnedHostBackend(slot_bytes=ops.state_size) as backend:
+        adj, st = pkg.execute(pkg.Multistage(slots, interval), ops, s0, backend, fuse=fuse)
+    torch.cuda.synchronize()
+    assert st.forward_evals == 2 * n and st.backward_evals == n
+    assert st.stores_issued == -(-n // interval) == st.prefetches_issued
+    full_norm = adj.double().norm().item()
+    assert full_norm > 1e-30, "adjoint underflowed: the check would be vacuous"
+    rows = _rows(batch)
+    got = adj[:, :, rows].double().cpu().numpy()
+    ref = _oracle_adjoint(d, n, s0[:, :, rows].double().cpu().numpy())
+    assert np.linalg.norm(ref) > 1e-30
+    err = L.rel_l2(got, ref)
+    assert err <= LONG_TOL, err
+    # per sequence: most of the mass is checked tightly (tiny-norm rows are
+    # dominated by cancellation, see the module docstring)
+    per = np.array([L.rel_l2(got[:, :, i], ref[:, :, i]) for i in range(len(rows))])
+    assert np.median(per) <= LONG_TOL, np.median(per)
+
+
+def test_strategies_bit_identical_at_long_n_nonzero(P):
+    # SURVEY §8(c) protocol 3 on a cell whose adjoint does not underflow
+    pkg, lstm = P
+    d, n, batch = 8, 400, 1 << 14
+    cell = lstm.long_memory_cell(d, n, 0)
+    ops = lstm.operator_pair(cell, batch, "f32")
+    s0 = lstm.random_states(d, 1, batch, "f32")
+    with pkg.PinnedHostBackend() as backend:
+        g_full, _ = pkg.execute(pkg.FullStorage(), ops, s0)
+        g_rev, _ = pkg.execute(pkg.Revolve(20), ops, s0)
+        g_ms, st = pkg.execute(pkg.Multistage(19, interval=20), ops, s0, backend)
+        g_fused, st_f = pkg.execute(pkg.Multistage(19, interval=20), ops, s0, backend, fuse=True)
+        g_rev_fused, _ = pkg.execute(pkg.Revolve(20), ops, s0, fuse=True)
+        g_full_fused, _ = pkg.execute(pkg.FullStorage(), ops, s0, fuse=True)
+    for g in (g_full, g_fused):
+        assert g.double().norm().item() > 1e-20, "adjoint underflowed: bit-identity would be vacuous"
+    assert torch.equal(g_full, g_rev) and torch.equal(g_full, g_ms)
+    assert torch.equal(g_full_fused, g_fused) and torch.equal(g_full_fused, g_rev_fused)
+    assert st.forward_evals == st_f.forward_evals == 2 * n
+    rows = _rows(batch, 32)
+    ref = _oracle_adjoint(d, n, s0[:, :, rows].double().cpu().numpy())
+    for g in (g_full, g_full_fused):
+        assert L.rel_l2(g[:, :, rows].double().cpu().numpy(), ref) <= LONG_TOL
+
+
+def test_random_cell_adjoint_really_underflows(P):
+    # documents why the long-memory cell exists: the reference cell's fp32
+    # adjoint is exactly zero at the headline n
+    pkg, lstm = P
+    d, n, batch = 8, 400, 4096
+    ops = lstm.operator_pair(lstm.random_cell(d, n, 0), batch, "f32")
+    adj, _ = pkg.execute(pkg.FullStorage(), ops, lstm.random_states(d, 1, batch, "f32"), fuse=True)
+    assert adj.abs().max().item() < 1e-37

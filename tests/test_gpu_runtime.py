@@ -294,31 +294,8 @@ def test_fp32_batched_end_to_end_vs_reference(P, runtime_golden, fast_backend):
         assert st.peak_l1_bytes == cfg["stats"]["peak_l1_bytes"] // (2 * d * 8) * ops.state_size
 
 
-def test_fp32_strategies_bit_identical_at_long_n(P):
-    # SURVEY §8(c) protocol 3: at any n the GPU strategies agree bit for bit
-    pkg, lstm, _ = P
-    d, n, batch = 8, 400, 1 << 14
-    cell = lstm.random_cell(d, n, 0)
-    ops = lstm.operator_pair(cell, batch, "f32")
-    s0 = lstm.random_states(d, 1, batch, "f32")
-    backend = pkg.PinnedHostBackend()
-    try:
-        g_full, _ = pkg.execute(pkg.FullStorage(), ops, s0)
-        g_rev, _ = pkg.execute(pkg.Revolve(20), ops, s0)
-        g_ms, st = pkg.execute(pkg.Multistage(19, interval=20), ops, s0, backend)
-        g_fused, st_f = pkg.execute(pkg.Multistage(19, interval=20), ops, s0, backend, fuse=True)
-        g_rev_fused, _ = pkg.execute(pkg.Revolve(20), ops, s0, fuse=True)
-    finally:
-        backend.close()
-    assert torch.equal(g_full, g_rev) and torch.equal(g_full, g_ms)
-    # the fused mode (tensor-core family for d=8) is bit-identical across its strategies
-    g_full_fused, _ = pkg.execute(pkg.FullStorage(), ops, s0, fuse=True)
-    assert torch.equal(g_full_fused, g_fused) and torch.equal(g_full_fused, g_rev_fused)
-    assert st.forward_evals == st_f.forward_evals == 2 * n
-    # counters and ledger equal the CPU oracle executor's
-    _, ost = RO.execute("multistage", L.random_cell(d, n, 0), np.zeros((2, d, 1)), slots=19, interval=20)
-    assert st.forward_evals == ost["forward_evals"] and st.stores_issued == ost["stores_issued"]
-    assert st.peak_l1_bytes == ost["peak_l1_bytes"] // (2 * d * 8) * ops.state_size
+# (bit-identity across strategies at long n, with a non-vanishing adjoint:
+# tests/test_gpu_long_chain.py)
 
 
 def test_fused_and_per_step_modes_agree(P):

@@ -1,6 +1,6 @@
 """Per-step times of the fused launches (advance / tape / reverse, 64 steps)
 at the C2 shape for the active kernel family (ACKPT_TC=1 tensor cores,
-ACKPT_TC=0 packed FFMA2, ACKPT_TC=2 mixed; unset = tcgen05)."""
+ACKPT_TC=0 packed FFMA2; unset = tcgen05)."""
 import json
 import os
 import sys
