@@ -44,7 +44,7 @@ def random_cell(d: int, n: int, seed: int) -> Cell:
     return Cell(w, b, xs, target)
 
 
-def long_memory_cell(d: int, n: int, seed: int, forget_bias: float = 6.0) -> Cell:
+def long_memory_cell(d: int, n: int, seed: int, forget_bias: float = 5.0) -> Cell:
     """random_cell plus forget_bias on b_f (mirror of the product's
     lstm.long_memory_cell): non-vacuous adjoints at long n."""
     cell = random_cell(d, n, seed)

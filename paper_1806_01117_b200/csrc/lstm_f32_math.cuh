@@ -94,14 +94,20 @@ __device__ __forceinline__ float2 tanh2(float2 x) {
 // ---- Newton-Raphson variants (tensor-core family) ------------------------
 // With the matvec on the tensor cores the FMA pipe idles while MUFU (16/clk/SM)
 // saturates, so reciprocals move to the FMA pipe: a bit-trick seed (<= 12 %
-// error) and three Newton steps r <- r (2 - y r) reach ~1 ulp for any normal
-// y >= 1 (the only arguments here).
+// error) and Newton steps for any normal y >= 1 (the only arguments here).
+// Newton converges from below (r (1 - e) -> r (1 - e^2)), so the iterate
+// carries a one-signed error e^2: after three steps up to 4e-8 (0.7 ulp),
+// the same sign in every reciprocal of every step.  That bias reached the
+// forget gate and, compounded over a 10^4-step long-memory chain, put the
+// adjoint at 6e-4 rel-L2 from float64 against 1e-4 for MUFU reciprocals
+// (tools/long_chain_mix.py).  A fourth step in the form r + r (1 - y r)
+// leaves ~1e-15 of bias plus one rounding.
 __device__ __forceinline__ float2 rcp2_nr(float2 y) {
   float2 r = make_float2(__int_as_float(0x7EF311C3 - __float_as_int(y.x)),
                          __int_as_float(0x7EF311C3 - __float_as_int(y.y)));
 #pragma unroll
   for (int it = 0; it < 3; ++it) r = mul2(r, fma2(neg(y), r, bc(2.0f)));
-  return r;
+  return fma2(r, fma2(neg(y), r, bc(1.0f)), r);
 }
 
 __device__ __forceinline__ void activate_nr(float2 tf, float2 ti, float2 to, float2 tg, float2& f, float2& i,

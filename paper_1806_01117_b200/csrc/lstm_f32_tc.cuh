@@ -6,13 +6,14 @@
 //
 // Gate pre-activations of a step, for the 256 batch elements of a CTA, are one
 // MMA problem per M-tile: D[128 x 32] = A[128 x 16] . B[32 x 16]^T with
-//   A row r = [h_0..h_7, 1, 0 x 7]                    (element of the tile)
-//   B row n = [s_g W_g[j][0..7], s_g xb_k[g][j], 0 x 7]  n = 4 j + g (unit-major)
+//   A row r = [h_0..h_7, 1, 1, 1, 0 x 5]                         (element of the tile)
+//   B row n = [s_g W_g[j][0..7], split3(s_g xb_k[g][j]), 0 x 5]  n = 4 j + g (unit-major)
 // (s_g: the exponent scale folded into the weights, lstm_f32_math.cuh), so the
 // bias / input projection of step k rides in the MMA and D holds the ex2
 // arguments directly.  fp32 accuracy from TF32 tensor cores with the 3xTF32
-// split x = hi + lo (hi = x with the low 13 mantissa bits cleared):
-// A.B ~ Ahi.Bhi + Alo.Bhi + Ahi.Blo (rel. error ~5e-7, tools/umma_probe.cu).
+// split x = hi + lo (hi = x rounded to tf32, lo = x - hi exact):
+// A.B ~ Ahi.Bhi + Alo.Bhi + Ahi.Blo (rel. error <= ~2^-22), and the bias
+// split exactly into three tf32 parts (one MMA, no split error).
 // Operands are K-major, no swizzle, in shared memory; D (fp32) is in TMEM,
 // one column per gate, one lane per tile row, read back with tcgen05.ld.
 //
@@ -39,13 +40,19 @@ constexpr uint32_t kLBO = 128; // bytes between the two 16-byte K chunks (8 rows
 constexpr uint32_t kSBO = 256; // bytes between 8-row groups
 constexpr uint32_t kIdesc = (1u << 4) | (2u << 7) | (2u << 10) | (uint32_t(kN >> 3) << 17) | (uint32_t(128 >> 4) << 24);
 
-// 24 KB: h operands per tile (hi, lo), one constant bias operand A1 = [1, 0 x 7]
-// shared by both tiles, the weights (hi, lo) and the step's bias column (hi, lo).
+// ~23 KB: h operands per tile (hi, lo), one constant bias operand
+// A1 = [1, 1, 1, 0 x 5] shared by both tiles, the weights (hi, lo) and the
+// step's bias split exactly into three tf32 parts (columns 0..2): the bias
+// term enters the accumulator with no split error.  It is the same for every
+// element of a step and dominates the forget-gate pre-activation of
+// long-memory cells, so a split error there is systematic: over a 10^4-step
+// chain it accumulated to ~1e-3 rel-L2 in the adjoint (2-way truncated split,
+// tools/long_chain_err.py) against 1e-4 for exact fp32 FMAs.
 struct Smem {
   float a[2][2][128 * kK];  // [tile][hi, lo]
-  float a1[128 * kK];       // rows [1, 0, ..., 0]
+  float a1[128 * kK];       // rows [1, 1, 1, 0, ..., 0]
   float bw[2][kN * kK];     // [hi, lo] scaled W rows n = 4 j + g
-  float bb[2][kN * kK];     // [hi, lo] column 0 = scaled xb_k, rest 0
+  float bb[kN * kK];        // row n: [hi, mid, lo] of scaled xb_k, rest 0
   uint64_t mbar;
   uint32_t tmem;
 };
@@ -57,7 +64,12 @@ __device__ __forceinline__ uint64_t desc(uint32_t addr) {
 }
 // float offset of (row, k) in a K-major no-swizzle 16-wide operand
 __device__ __forceinline__ int kofs(int r, int k) { return (r >> 3) * (kSBO / 4) + (k >> 2) * (kLBO / 4) + (r & 7) * 4 + (k & 3); }
-__device__ __forceinline__ float hi_part(float x) { return __uint_as_float(__float_as_uint(x) & 0xFFFFE000u); }
+// tf32 head of x rounded to nearest (ties away from zero, = cvt.rna.tf32.f32):
+// x - hi_part(x) is exact in fp32 and at most half a tf32 ulp of x, so the
+// MMA's truncation of that residual to tf32 costs <= 2^-23 |x|.
+__device__ __forceinline__ float hi_part(float x) {
+  return __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xFFFFE000u);
+}
 
 __device__ __forceinline__ void mma(uint32_t d, uint64_t a, uint64_t b, uint32_t acc) {
   asm volatile(
@@ -93,10 +105,10 @@ __device__ __forceinline__ void setup(Smem& sm, const Weights& w, uint32_t tmem_
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(&sm.mbar)));
     asm volatile("fence.mbarrier_init.release.cluster;");
   }
-  // bias operand row of this thread: [1, 0, ..., 0]
-  *reinterpret_cast<float4*>(&sm.a1[kofs(tid, 0)]) = make_float4(1.f, 0.f, 0.f, 0.f);
+  // bias operand row of this thread: [1, 1, 1, 0, ..., 0]
+  *reinterpret_cast<float4*>(&sm.a1[kofs(tid, 0)]) = make_float4(1.f, 1.f, 1.f, 0.f);
   *reinterpret_cast<float4*>(&sm.a1[kofs(tid, 4)]) = make_float4(0.f, 0.f, 0.f, 0.f);
-  // weight rows n = 4 j + g (scaled, split), bias rows zero but for column 0 (per step)
+  // weight rows n = 4 j + g (scaled, split), bias rows zero but for columns 0..2 (per step)
   if (tid < kN) {
     const int j = tid >> 2, g = tid & 3;
 #pragma unroll
@@ -104,10 +116,15 @@ __device__ __forceinline__ void setup(Smem& sm, const Weights& w, uint32_t tmem_
       const float x = w.ws[g][j][k];
       sm.bw[0][kofs(tid, k)] = hi_part(x);
       sm.bw[1][kofs(tid, k)] = x - hi_part(x);
-      sm.bb[0][kofs(tid, k)] = 0.f;
-      sm.bb[1][kofs(tid, k)] = 0.f;
+      sm.bb[kofs(tid, k)] = 0.f;
     }
   }
+}
+
+// x = hi + mid + lo exactly, each part a tf32 value (11 + 11 + <= 2 bits).
+__device__ __forceinline__ float4 split3(float x) {
+  const float hi = hi_part(x), r = x - hi, mid = hi_part(r);
+  return make_float4(hi, mid, r - mid, 0.f);
 }
 
 // Scaled bias of step k for B row n = tid (threads < kN), loaded one step ahead.
@@ -140,10 +157,7 @@ __device__ __forceinline__ void stage_operands(Smem& sm, const float2 (&h)[kD], 
     *reinterpret_cast<float4*>(&sm.a[1][0][kofs(tid, 4 * c)]) = bh;
     *reinterpret_cast<float4*>(&sm.a[1][1][kofs(tid, 4 * c)]) = make_float4(b01.x, b01.y, b23.x, b23.y);
   }
-  if (tid < kN) {
-    sm.bb[0][kofs(tid, 0)] = hi_part(x);
-    sm.bb[1][kofs(tid, 0)] = x - hi_part(x);
-  }
+  if (tid < kN) *reinterpret_cast<float4*>(&sm.bb[kofs(tid, 0)]) = split3(x);
 }
 
 __device__ __forceinline__ void mbar_wait(const uint64_t* bar, uint32_t phase) {
@@ -157,7 +171,7 @@ __device__ __forceinline__ void mbar_wait(const uint64_t* bar, uint32_t phase) {
   } while (!done);
 }
 
-// Barrier, then thread 0 issues the 10 MMAs of a step and commits them to
+// Barrier, then thread 0 issues the 8 MMAs of a step and commits them to
 // sm.mbar.  Every thread's shared-memory reads and writes of the step so far
 // are complete (and visible to the async proxy) when this returns.
 __device__ __forceinline__ void gates_issue(Smem& sm) {
@@ -167,16 +181,15 @@ __device__ __forceinline__ void gates_issue(Smem& sm) {
   if (threadIdx.x == 0) {
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     const uint64_t wh = desc(su32(sm.bw[0])), wl = desc(su32(sm.bw[1]));
-    const uint64_t xh = desc(su32(sm.bb[0])), xl = desc(su32(sm.bb[1])), one = desc(su32(sm.a1));
+    const uint64_t xb = desc(su32(sm.bb)), one = desc(su32(sm.a1));
 #pragma unroll
     for (int t = 0; t < 2; ++t) {
       const uint32_t d = sm.tmem + uint32_t(t * kN);
       const uint64_t ah = desc(su32(sm.a[t][0])), al = desc(su32(sm.a[t][1]));
-      mma(d, ah, wh, 0u);   // h_hi . W_hi
+      mma(d, one, xb, 0u);  // 1 . (xb_hi + xb_mid + xb_lo), exact
+      mma(d, ah, wh, 1u);   // h_hi . W_hi
       mma(d, al, wh, 1u);   // h_lo . W_hi
       mma(d, ah, wl, 1u);   // h_hi . W_lo
-      mma(d, one, xh, 1u);  // 1 . xb_hi
-      mma(d, one, xl, 1u);  // 1 . xb_lo
     }
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(&sm.mbar))
                  : "memory");

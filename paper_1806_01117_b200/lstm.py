@@ -99,12 +99,14 @@ def random_cell(d: int, n: int, seed: int) -> LstmCell:
     return LstmCell(*w, *b, xs=xs, target=draw(d))
 
 
-def long_memory_cell(d: int, n: int, seed: int, forget_bias: float = 6.0) -> LstmCell:
+def long_memory_cell(d: int, n: int, seed: int, forget_bias: float = 5.0) -> LstmCell:
     """random_cell(d, n, seed) with ``forget_bias`` added to b_f: the forget
-    gate sits near 1 (sigmoid(6) = 0.9975), so the state adjoint decays slowly
-    and stays far above fp32 underflow at n = 10^4 (d = 8: per-sequence norms
-    1e-14 .. 3e-7), where the reference cell's adjoint is exactly 0 past
-    n ~ 190.  Same timing as random_cell; the workload of the long-chain
+    gate sits near 1 (sigmoid(5) = 0.993), so the state adjoint stays far above
+    fp32 underflow at n = 10^4 (d = 8, seed 0: per-sequence norms 8e-4 ..
+    1.8e-3), where the reference cell's adjoint is exactly 0 past n ~ 190.
+    The chain is well conditioned (a 1-ulp fp32 perturbation of the weights
+    moves the float64 adjoint by 2e-6 rel-L2; bias 6 has rows 30x more
+    sensitive).  Same timing as random_cell; the workload of the long-chain
     parity checks (tests, bench.py's parity leg)."""
     cell = random_cell(d, n, seed)
     cell.b_f = cell.b_f + forget_bias

@@ -2,8 +2,8 @@
 
 With the reference's random_cell the fp32 state adjoint is exactly 0 (or
 denormal noise) past n ~ 190, so bit-identity between strategies at long n
-compares zeros.  long_memory_cell (random_cell + forget-gate bias 6) keeps
-per-sequence adjoint norms at 1e-14 .. 3e-7 over n = 10^4 (d = 8), so these
+compares zeros.  long_memory_cell (random_cell + forget-gate bias 5) keeps
+per-sequence adjoint norms at 8e-4 .. 2e-3 over n = 10^4 (d = 8), so these
 tests compare real numbers:
 
 * the headline configuration itself -- BASELINE config 2: d = 8, B = 2^20
@@ -15,9 +15,11 @@ tests compare real numbers:
 
 Tolerance: aggregate rel-L2 over the sampled sequences <= 2e-4.  An fp32
 numpy restatement of the same chain (every operation in fp32, same inputs)
-sits at 5.2e-5 from float64 at n = 10^4: the forget gate near 1 makes c an
-integrator over ~400 steps, so fp32 rounding of the forward trajectory
-accumulates; per-step kernel parity stays at 1e-5 (test_gpu_kernels.py).
+sits at 9.6e-5 from float64 at n = 10^4: the adjoint is a product of ~10^4
+forget gates, so a relative error in f adds up over the whole chain (a
+one-signed 1-ulp error per step would give 6e-4); per-step kernel parity
+stays at 1e-5 (test_gpu_kernels.py).  Measured on B200: FFMA2 1.0e-4,
+tcgen05 8e-5 (tools/long_chain_err.py, tools/long_chain_mix.py).
 """
 
 import numpy as np
