@@ -6,9 +6,14 @@
 // directly the argument of ex2:
 //   sigmoid(a) = 1 / (1 + 2^(-log2e a)),   tanh(a) = 1 - 2 / (1 + 2^(2 log2e a)).
 // The four activations of a hidden unit share ONE reciprocal on the MUFU
-// pipe: 1/y_f = (y_i y_o y_g) / (y_f y_i y_o y_g).  If the product overflows
-// (pre-activations beyond ~22) a branch computes separate reciprocals, which
-// is exact there because rcp(inf) = 0.
+// pipe: 1/y_f = (y_i y_o y_g) / (y_f y_i y_o y_g).  If the product is large
+// (P > kShareMax: pre-activations summing past ~60) a branch computes separate
+// reciprocals, which is exact there because rcp(inf) = 0.  The bound keeps
+// 1/P a normal float: above 2^126 rcp.approx.ftz flushes 1/P to 0 (so f = i =
+// o = 0 where e.g. f = 1/y_f = 1), and the Newton seed 0x7EF311C3 - bits(P)
+// leaves the normal range -- both seen with pre-activations of +-100
+// (tests/test_gpu_saturation.py).
+constexpr float kShareMax = 1.0e37f;
 #pragma once
 
 #include <cuda_runtime.h>
@@ -71,7 +76,7 @@ __device__ __forceinline__ void activate(float2 tf, float2 ti, float2 to, float2
   const float2 yo = add2(ex2_2(to), one), yg = add2(ex2_2(tg), one);
   const float2 p12 = mul2(yf, yi), p34 = mul2(yo, yg);
   const float2 P = mul2(p12, p34);
-  if (__builtin_expect(P.x <= 3.0e38f && P.y <= 3.0e38f, 1)) {
+  if (__builtin_expect(P.x <= kShareMax && P.y <= kShareMax, 1)) {
     const float2 r = rcp2(P);
     const float2 q34 = mul2(r, p34), q12 = mul2(r, p12);
     f = mul2(q34, yi);
@@ -117,7 +122,7 @@ __device__ __forceinline__ void activate_nr(float2 tf, float2 ti, float2 to, flo
   const float2 yo = add2(ex2_2(to), one), yg = add2(ex2_2(tg), one);
   const float2 p12 = mul2(yf, yi), p34 = mul2(yo, yg);
   const float2 P = mul2(p12, p34);
-  if (__builtin_expect(P.x <= 3.0e38f && P.y <= 3.0e38f, 1)) {
+  if (__builtin_expect(P.x <= kShareMax && P.y <= kShareMax, 1)) {
     const float2 r = rcp2_nr(P);
     const float2 q34 = mul2(r, p34), q12 = mul2(r, p12);
     f = mul2(q34, yi);

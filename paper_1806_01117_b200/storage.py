@@ -277,27 +277,26 @@ class Level2Backend:
             N.check(N.lib.ackpt_tier_set_throttle(self._handle, float(latency), float(bandwidth)))
 
     # -- public API (storage.py:233-263) --------------------------------------
-    def _copy_streams(self, h: int):
-        """torch handles of the tier's D2H / H2D copy streams (cached)."""
-        if getattr(self, "_streams", None) is None or self._streams[0] != h:
-            d2h, h2d = C.c_void_p(), C.c_void_p()
-            N.check(N.lib.ackpt_tier_streams(h, C.byref(d2h), C.byref(h2d)))
-            self._streams = (h, torch.cuda.ExternalStream(d2h.value, device=self._device),
-                             torch.cuda.ExternalStream(h2d.value, device=self._device))
-        return self._streams[1], self._streams[2]
+    def _hold(self, ticket_id: int, buf: torch.Tensor) -> None:
+        """Keeps a transfer's device buffer alive until its ticket completed:
+        the copy engines read (store) or write (fetch) it asynchronously, so a
+        dropped ticket must not let the caching allocator hand the block to
+        someone else mid-copy.  Released at wait / a completed poll / close
+        (after the tier drained its streams)."""
+        if buf.numel():
+            if not hasattr(self, "_inflight"):
+                self._inflight = {}
+            self._inflight[ticket_id] = buf
 
     def begin_store(self, key: int, payload: CheckpointPayload) -> TransferTicket:
         """Asynchronous store; the payload must not be modified until the
-        ticket completed (the reference stores immutable bytes, storage.py:233).
-        The source block is tied to the D2H stream (record_stream), so even a
-        dropped ticket cannot let the caching allocator reuse it mid-copy."""
+        ticket completed (the reference stores immutable bytes, storage.py:233)."""
         src = as_device_bytes(payload.data, self._device)
         h = self._ensure(src.numel())
         out = C.c_int64(-1)
         stream = torch.cuda.current_stream(self._device).cuda_stream
         N.check(N.lib.ackpt_tier_begin_store(h, key, payload.step, src.data_ptr(), src.numel(), stream, C.byref(out)))
-        if src.numel():
-            src.record_stream(self._copy_streams(h)[0])
+        self._hold(out.value, src)
         return TransferTicket(self, "store", key, out.value, keep=src)
 
     def begin_fetch(self, key: int) -> TransferTicket:
@@ -308,13 +307,15 @@ class Level2Backend:
         out = C.c_int64(-1)
         stream = torch.cuda.current_stream(self._device).cuda_stream
         N.check(N.lib.ackpt_tier_begin_fetch(h, key, dst.data_ptr(), dst.numel(), stream, C.byref(out)))
-        if dst.numel():
-            dst.record_stream(self._copy_streams(h)[1])
+        self._hold(out.value, dst)
         return TransferTicket(self, "fetch", key, out.value, keep=dst)
 
     def wait(self, ticket: TransferTicket) -> Optional[CheckpointPayload]:
         step = C.c_int64(0)
-        N.check(N.lib.ackpt_tier_wait(self._handle, ticket.id, C.byref(step)))
+        try:
+            N.check(N.lib.ackpt_tier_wait(self._handle, ticket.id, C.byref(step)))
+        finally:
+            getattr(self, "_inflight", {}).pop(ticket.id, None)
         if ticket.kind == "fetch":
             if ticket._result is None:
                 ticket._result = CheckpointPayload(step.value, ticket._keep)
@@ -325,6 +326,7 @@ class Level2Backend:
         rc = N.lib.ackpt_tier_poll(self._handle, ticket.id)
         if rc == N.NOT_READY:
             return False
+        getattr(self, "_inflight", {}).pop(ticket.id, None)
         return True  # complete (an error surfaces at wait)
 
     def contains(self, key: int) -> bool:
@@ -344,9 +346,10 @@ class Level2Backend:
 
     def close(self) -> None:
         if self._handle is not None and not self._closed:
-            N.check(N.lib.ackpt_tier_destroy(self._handle))
+            N.check(N.lib.ackpt_tier_destroy(self._handle))  # drains the copy streams first
         self._handle = None
         self._closed = True
+        getattr(self, "_inflight", {}).clear()
 
     def __enter__(self) -> "Level2Backend":
         return self
