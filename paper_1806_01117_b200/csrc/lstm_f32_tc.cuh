@@ -48,9 +48,11 @@ constexpr uint32_t kIdesc = (1u << 4) | (2u << 7) | (2u << 10) | (uint32_t(kN >>
 // long-memory cells, so a split error there is systematic: over a 10^4-step
 // chain it accumulated to ~1e-3 rel-L2 in the adjoint (2-way truncated split,
 // tools/long_chain_err.py) against 1e-4 for exact fp32 FMAs.
+// A1 is one 8-row group read with stride-byte-offset 0: all 16 row groups of
+// the M = 128 operand alias it (256 B instead of 4 KB of shared memory).
 struct Smem {
   float a[2][2][128 * kK];  // [tile][hi, lo]
-  float a1[128 * kK];       // rows [1, 1, 1, 0, ..., 0]
+  float a1[8 * kK];         // rows [1, 1, 1, 0, ..., 0], broadcast over the 16 row groups
   float bw[2][kN * kK];     // [hi, lo] scaled W rows n = 4 j + g
   float bb[kN * kK];        // row n: [hi, mid, lo] of scaled xb_k, rest 0
   uint64_t mbar;
@@ -58,9 +60,9 @@ struct Smem {
 };
 
 __device__ __forceinline__ uint32_t su32(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
-__device__ __forceinline__ uint64_t desc(uint32_t addr) {
+__device__ __forceinline__ uint64_t desc(uint32_t addr, uint32_t sbo = kSBO) {
   return uint64_t((addr >> 4) & 0x3FFF) | (uint64_t((kLBO >> 4) & 0x3FFF) << 16) |
-         (uint64_t((kSBO >> 4) & 0x3FFF) << 32) | (uint64_t(1) << 46);
+         (uint64_t((sbo >> 4) & 0x3FFF) << 32) | (uint64_t(1) << 46);
 }
 // float offset of (row, k) in a K-major no-swizzle 16-wide operand
 __device__ __forceinline__ int kofs(int r, int k) { return (r >> 3) * (kSBO / 4) + (k >> 2) * (kLBO / 4) + (r & 7) * 4 + (k & 3); }
@@ -106,8 +108,10 @@ __device__ __forceinline__ void setup(Smem& sm, const Weights& w, uint32_t tmem_
     asm volatile("fence.mbarrier_init.release.cluster;");
   }
   // bias operand row of this thread: [1, 1, 1, 0, ..., 0]
-  *reinterpret_cast<float4*>(&sm.a1[kofs(tid, 0)]) = make_float4(1.f, 1.f, 1.f, 0.f);
-  *reinterpret_cast<float4*>(&sm.a1[kofs(tid, 4)]) = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (tid < 8) {
+    *reinterpret_cast<float4*>(&sm.a1[kofs(tid, 0)]) = make_float4(1.f, 1.f, 1.f, 0.f);
+    *reinterpret_cast<float4*>(&sm.a1[kofs(tid, 4)]) = make_float4(0.f, 0.f, 0.f, 0.f);
+  }
   // weight rows n = 4 j + g (scaled, split), bias rows zero but for columns 0..2 (per step)
   if (tid < kN) {
     const int j = tid >> 2, g = tid & 3;
@@ -181,7 +185,7 @@ __device__ __forceinline__ void gates_issue(Smem& sm) {
   if (threadIdx.x == 0) {
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     const uint64_t wh = desc(su32(sm.bw[0])), wl = desc(su32(sm.bw[1]));
-    const uint64_t xb = desc(su32(sm.bb)), one = desc(su32(sm.a1));
+    const uint64_t xb = desc(su32(sm.bb)), one = desc(su32(sm.a1), 0u);
 #pragma unroll
     for (int t = 0; t < 2; ++t) {
       const uint32_t d = sm.tmem + uint32_t(t * kN);
@@ -320,8 +324,30 @@ __device__ __forceinline__ void stage_state(RS& sm, const float* state, int64_t 
 // aligned states): the taped state of step i-1 streams into shared memory by
 // cp.async.bulk while step i computes, instead of a dependent load at the top
 // of every step.
+//
+// 6 CTAs/SM (80 registers, ~36 KB of shared memory with the broadcast bias
+// operand): 27.5 us/step at the C2 shape vs 27.9 at 5 CTAs (96 registers)
+// and 29.6 at 7 (72 registers, 148 B of spills).  Deferring the last units'
+// transposed-product FMAs past the next step's MMA issue (to cover the MMA
+// round trip) measured 28.1 / 30.3 us (2 / 4 units): the per-step wait is
+// the CTA barrier's warp skew, not the MMA latency (ncu source page:
+// barrier 17 %, mbarrier long-scoreboard 5 % of warp samples).
+#ifndef ACKPT_REV_MINB
+#define ACKPT_REV_MINB 6
+#endif
+
+__device__ __forceinline__ void tmatvec_unit(const Weights& w, int j, const float2 (&da)[4], float2 (&acc)[kD]) {
+#pragma unroll
+  for (int m = 0; m < kD; ++m) {
+    acc[m] = fma2(bc(w.wu[0][j][m]), da[0], acc[m]);
+    acc[m] = fma2(bc(w.wu[1][j][m]), da[1], acc[m]);
+    acc[m] = fma2(bc(w.wu[2][j][m]), da[2], acc[m]);
+    acc[m] = fma2(bc(w.wu[3][j][m]), da[3], acc[m]);
+  }
+}
+
 template <bool PF>
-__global__ void __launch_bounds__(kThreads, 5)  // 96 registers, 5 CTAs/SM: 28.3 vs 30.2 us/step at 4
+__global__ void __launch_bounds__(kThreads, ACKPT_REV_MINB)
     rev_tc(const float* __restrict__ adj_in, float* __restrict__ adj_out, int64_t B, const float* __restrict__ xbs_all,
            int64_t from, int count, const __grid_constant__ Weights w, const __grid_constant__ StatePtrs states) {
   __shared__ __align__(128) RevSmem rs;
@@ -379,15 +405,9 @@ __global__ void __launch_bounds__(kThreads, 5)  // 96 registers, 5 CTAs/SM: 28.3
 #pragma unroll
       for (int q = 0; q < 2; ++q) {
         const int j = u + q;
-        float2 daf, dai, dao, dag;
-        bwd_unit_u(pre[q][0], pre[q][1], pre[q][2], pre[q][3], c[j], dh[j], dc[j], daf, dai, dao, dag, dc[j]);
-#pragma unroll
-        for (int m = 0; m < kD; ++m) {
-          acc[m] = fma2(bc(w.wu[0][j][m]), daf, acc[m]);
-          acc[m] = fma2(bc(w.wu[1][j][m]), dai, acc[m]);
-          acc[m] = fma2(bc(w.wu[2][j][m]), dao, acc[m]);
-          acc[m] = fma2(bc(w.wu[3][j][m]), dag, acc[m]);
-        }
+        float2 da[4];
+        bwd_unit_u(pre[q][0], pre[q][1], pre[q][2], pre[q][3], c[j], dh[j], dc[j], da[0], da[1], da[2], da[3], dc[j]);
+        tmatvec_unit(w, j, da, acc);
       }
     }
 #pragma unroll
