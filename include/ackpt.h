@@ -202,6 +202,26 @@ ACKPT_API int ackpt_tier_create(int64_t capacity, int64_t slot_bytes, ackpt_tier
  * reported at wait (or at the end of an engine run).  Files already present
  * in the directory can be fetched (resume). */
 ACKPT_API int ackpt_tier_create_file(const char* directory, int64_t slot_bytes, ackpt_tier** out);
+/* Three-stage tier (BASELINE config 5): HBM -> pinned
+ * host DRAM (dram_slots slots of slot_bytes) -> CKPT files in `directory`
+ * (same byte format as ackpt_tier_create_file).  Recent boundaries stay in
+ * DRAM; older ones are spilled by an I/O thread (CRC32C, O_DIRECT, atomic
+ * publish) and read back (O_DIRECT, verified) ahead of their fetch.  No
+ * CUDA-graph capture.  Replaces FileBackend behind a pinned cache
+ * (storage.py:321-340) where the host RAM cannot hold every boundary. */
+ACKPT_API int ackpt_tier_create_cascade(const char* directory, int64_t slot_bytes, int32_t dram_slots,
+                                        ackpt_tier** out);
+typedef struct ackpt_cascade_stats {
+    int64_t dram_slots;
+    int64_t spills, spill_bytes;  /* completed DRAM -> file spills */
+    double spill_seconds;         /* host time in the spill thread (CRC + write + publish) */
+    int64_t reads, read_bytes;    /* completed file -> DRAM reads */
+    double read_seconds;
+    int64_t dram_hits;            /* fetches served from a DRAM slot */
+    int64_t ring_hits;            /* fetches of spilled keys already read ahead */
+    int64_t ring_misses;          /* fetches of spilled keys read on demand */
+} ackpt_cascade_stats;
+ACKPT_API int ackpt_tier_cascade_stats(ackpt_tier* tier, ackpt_cascade_stats* out);
 ACKPT_API int ackpt_tier_destroy(ackpt_tier* tier);
 /* Stall injection for contention tests: each transfer holds its copy stream
  * for at least latency_us + bytes / bandwidth (bandwidth <= 0: no limit),

@@ -84,6 +84,13 @@ class Stats(C.Structure):
     ]
 
 
+class CascadeStats(C.Structure):
+    _fields_ = [("dram_slots", C.c_int64), ("spills", C.c_int64), ("spill_bytes", C.c_int64),
+                ("spill_seconds", C.c_double), ("reads", C.c_int64), ("read_bytes", C.c_int64),
+                ("read_seconds", C.c_double), ("dram_hits", C.c_int64), ("ring_hits", C.c_int64),
+                ("ring_misses", C.c_int64)]
+
+
 class TimelineEvent(C.Structure):
     _fields_ = [("kind", C.c_int32), ("lane", C.c_int32), ("from_step", C.c_int64), ("to_step", C.c_int64),
                 ("start", C.c_double), ("end", C.c_double)]
@@ -158,6 +165,8 @@ _SIGS = {
     "ackpt_pad_operator_destroy": ([C.POINTER(Operator)], C.c_int),
     "ackpt_tier_create": ([C.c_int64, C.c_int64, C.POINTER(_vp)], C.c_int),
     "ackpt_tier_create_file": ([C.c_char_p, C.c_int64, C.POINTER(_vp)], C.c_int),
+    "ackpt_tier_create_cascade": ([C.c_char_p, C.c_int64, C.c_int32, C.POINTER(_vp)], C.c_int),
+    "ackpt_tier_cascade_stats": ([_vp, C.POINTER(CascadeStats)], C.c_int),
     "ackpt_tier_destroy": ([_vp], C.c_int),
     "ackpt_tier_set_throttle": ([_vp, C.c_double, C.c_double], C.c_int),
     "ackpt_tier_begin_store": ([_vp, C.c_int64, C.c_int64, _vp, C.c_int64, _vp, _i64p], C.c_int),

@@ -52,6 +52,8 @@ void tier_quiesce(ackpt_tier* t);
 bool tier_ticket_times(ackpt_tier* t, ackpt_ticket id, cudaEvent_t* t0, cudaEvent_t* t1);
 int64_t tier_slot_bytes(const ackpt_tier* t);
 cudaStream_t tier_d2h(const ackpt_tier* t);
+double tier_spill_seconds(ackpt_tier* t, int64_t bytes);
+int tier_dram_slots(ackpt_tier* t);
 }  // namespace ackpt
 
 namespace {
@@ -1079,6 +1081,14 @@ ACKPT_API int ackpt_engine_calibrate(ackpt_engine* E, ackpt_tier* tier, int64_t 
       *t_a = fused_step > 0 ? fused_step : std::min(chain(true), median(0));
       *t_b = std::min(chain(false), median(2 * trials));
       *t_t = median(4 * trials);
+      // Cascade tier: once a plan has more boundaries than DRAM slots, every
+      // store also costs one spill to the file stage (running beside the next
+      // D2H copy), so the sustained per-boundary time is the slower of the two.
+      const double spill = tier_spill_seconds(tier, E->S);
+      if (spill > 0) {
+        const int64_t I0 = interval_length_exact(*t_t, *t_a);
+        if ((E->n + I0 - 1) / I0 > int64_t(tier_dram_slots(tier)) - 2) *t_t = std::max(*t_t, spill);
+      }
     } catch (...) {
       cleanup();
       for (auto ev : evs) cudaEventDestroy(ev);

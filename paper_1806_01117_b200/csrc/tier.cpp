@@ -79,6 +79,8 @@ struct KeyEntry {
   uint32_t file_fetch_seq = 0;  // last I/O-thread fetch of this key
 };
 
+struct Cascade;
+
 }  // namespace ackpt
 
 struct ackpt_tier {
@@ -131,7 +133,26 @@ struct ackpt_tier {
   bool stop = false;
   std::atomic<bool> abort{false};  // destroy: stop waiting on flags a failed stream never bumps
   std::thread store_thr, fetch_thr;
+  // Three-stage cascade (cascade_impl.h): pinned DRAM slots backed by CKPT
+  // files; null for the pinned and file tiers.
+  ackpt::Cascade* cascade = nullptr;
+  int cascade_slots = 0;
 };
+
+namespace ackpt {
+// cascade_impl.h (same translation unit)
+void cascade_create(ackpt_tier* t, int dram_slots);
+void cascade_destroy(ackpt_tier* t);
+void cascade_quiesce(ackpt_tier* t);
+ackpt_ticket cascade_begin_store(ackpt_tier* t, int64_t key, int64_t step, const void* src, int64_t bytes,
+                                 void* after_stream);
+ackpt_ticket cascade_begin_fetch(ackpt_tier* t, int64_t key, void* dst, int64_t bytes, void* after_stream);
+bool cascade_contains(ackpt_tier* t, int64_t key);
+int64_t cascade_key_bytes(ackpt_tier* t, int64_t key);
+void* cascade_host_ptr(ackpt_tier* t, int64_t key);
+void cascade_clear(ackpt_tier* t);
+double cascade_spill_probe(ackpt_tier* t, int64_t bytes);
+}  // namespace ackpt
 
 namespace ackpt {
 enum Flag { kCopied = 0, kWritten = 16, kConsumed = 32, kStaged = 48 };
@@ -709,6 +730,7 @@ KeyEntry& ensure_storage(ackpt_tier* t, int64_t key, int64_t bytes) {
 // allocated at prepare time, outside the timed window.
 void tier_reserve_keys(ackpt_tier* t, const std::vector<int64_t>& keys, int64_t bytes) {
   std::lock_guard<std::mutex> lk(t->mu);
+  if (t->cascade) return;  // its DRAM slots and read buffers exist since creation
   if (bytes <= t->slot_bytes) {
     int64_t absent = 0;
     for (int64_t k : keys) {
@@ -755,6 +777,7 @@ void tier_reset_async(ackpt_tier* t, ackpt_ticket id) {
 // The per-key events are then re-recorded on the idle copy streams (outside
 // any capture), so a later eager transfer or ensure_storage can wait on them.
 void tier_quiesce(ackpt_tier* t) {
+  if (t->cascade) return cascade_quiesce(t);  // (its workers take t->mu: drain without it)
   std::lock_guard<std::mutex> lk(t->mu);
   ACKPT_CUDA_CHECK(cudaStreamSynchronize(t->d2h));
   ACKPT_CUDA_CHECK(cudaStreamSynchronize(t->h2d));
@@ -770,6 +793,15 @@ void tier_set_timing(ackpt_tier* t, bool on) {
   std::lock_guard<std::mutex> lk(t->mu);
   t->timing = on;
 }
+// Cascade tiers: seconds one boundary store takes on the spill stage (CRC +
+// O_DIRECT write of a `bytes` payload) and the number of DRAM slots; -1 / 0
+// for the other tiers (engine calibrate, runtime.py:420-466).
+double tier_spill_seconds(ackpt_tier* t, int64_t bytes) {
+  if (!t->cascade) return -1.0;
+  const double s = cascade_spill_probe(t, bytes);  // drains the workers: no t->mu here
+  return s;
+}
+int tier_dram_slots(ackpt_tier* t) { return t->cascade ? t->cascade_slots : 0; }
 bool tier_ticket_times(ackpt_tier* t, ackpt_ticket id, cudaEvent_t* t0, cudaEvent_t* t1) {
   std::lock_guard<std::mutex> lk(t->mu);
   TierTicket* tk = find_ticket(t, id);
@@ -832,6 +864,7 @@ ACKPT_API int ackpt_tier_destroy(ackpt_tier* t) {
     if (t->d2h) cudaStreamSynchronize(t->d2h);
     if (t->h2d) cudaStreamSynchronize(t->h2d);
     ackpt::io_stop(t);
+    ackpt::cascade_destroy(t);
     if (t->flags) cudaFreeHost(t->flags);
     for (auto e : t->all_events) cudaEventDestroy(e);
     for (auto& kv : t->keys) {
@@ -861,6 +894,12 @@ ACKPT_API int ackpt_tier_begin_store(ackpt_tier* t, int64_t key, int64_t step, c
                                      int64_t bytes, void* after_stream, ackpt_ticket* out) {
   return ackpt::guard([&] {
     std::lock_guard<std::mutex> lk(t->mu);
+    if (t->cascade) {
+      if (step < 0) ackpt::fail(ACKPT_VALUE_ERROR, "step must be >= 0");
+      if (bytes < 0) ackpt::fail(ACKPT_VALUE_ERROR, "bytes must be >= 0");
+      *out = ackpt::cascade_begin_store(t, key, step, src, bytes, after_stream);
+      return;
+    }
     if (step < 0) ackpt::fail(ACKPT_VALUE_ERROR, "step must be >= 0");
     ackpt::TierTicket tk;
     tk.kind = 0;
@@ -955,6 +994,10 @@ ACKPT_API int ackpt_tier_begin_fetch(ackpt_tier* t, int64_t key, void* dst, int6
                                      void* after_stream, ackpt_ticket* out) {
   return ackpt::guard([&] {
     std::lock_guard<std::mutex> lk(t->mu);
+    if (t->cascade) {
+      *out = ackpt::cascade_begin_fetch(t, key, dst, bytes, after_stream);
+      return;
+    }
     ackpt::TierTicket tk;
     tk.kind = 1;
     tk.key = key;
@@ -1134,6 +1177,10 @@ ACKPT_API int ackpt_tier_poll(ackpt_tier* t, ackpt_ticket ticket) {
 ACKPT_API int ackpt_tier_contains(ackpt_tier* t, int64_t key, int32_t* out) {
   return ackpt::guard([&] {
     std::lock_guard<std::mutex> lk(t->mu);
+    if (t->cascade) {
+      *out = ackpt::cascade_contains(t, key) ? 1 : 0;
+      return;
+    }
     auto it = t->keys.find(key);
     *out = (it != t->keys.end() && it->second.stored) ? 1 : 0;
     if (!*out && t->file_mode) *out = ackpt::file_payload_len(t, key) != -1 ? 1 : 0;  // the file exists
@@ -1143,6 +1190,10 @@ ACKPT_API int ackpt_tier_contains(ackpt_tier* t, int64_t key, int32_t* out) {
 ACKPT_API int ackpt_tier_key_bytes(ackpt_tier* t, int64_t key, int64_t* out) {
   return ackpt::guard([&] {
     std::lock_guard<std::mutex> lk(t->mu);
+    if (t->cascade) {
+      *out = ackpt::cascade_key_bytes(t, key);
+      return;
+    }
     auto it = t->keys.find(key);
     if (t->file_mode && (it == t->keys.end() || !it->second.stored)) {
       std::string why;
@@ -1161,6 +1212,10 @@ ACKPT_API int ackpt_tier_key_bytes(ackpt_tier* t, int64_t key, int64_t* out) {
 ACKPT_API int ackpt_tier_host_ptr(ackpt_tier* t, int64_t key, void** out) {
   return ackpt::guard([&] {
     std::lock_guard<std::mutex> lk(t->mu);
+    if (t->cascade) {
+      *out = ackpt::cascade_host_ptr(t, key);
+      return;
+    }
     if (t->file_mode) ackpt::fail(ACKPT_VALUE_ERROR, "file-stage keys live on disk, not in pinned memory");
     auto it = t->keys.find(key);
     if (it == t->keys.end() || !it->second.stored)
@@ -1174,7 +1229,9 @@ ACKPT_API int ackpt_tier_clear(ackpt_tier* t) {
     ACKPT_CUDA_CHECK(cudaStreamSynchronize(t->d2h));
     ACKPT_CUDA_CHECK(cudaStreamSynchronize(t->h2d));
     ackpt::io_drain(t);
+    if (t->cascade) ackpt::cascade_quiesce(t);
     std::lock_guard<std::mutex> lk(t->mu);
+    if (t->cascade) ackpt::cascade_clear(t);
     for (auto& kv : t->keys) {
       if (kv.second.slot >= 0) t->free_slots.push_back(kv.second.slot);
       if (kv.second.big) cudaFreeHost(kv.second.big);
@@ -1198,3 +1255,5 @@ extern "C" ACKPT_API int ackpt_tier_streams(ackpt_tier* t, void** d2h, void** h2
     if (h2d) *h2d = t->h2d;
   });
 }
+
+#include "cascade_impl.h"

@@ -398,6 +398,42 @@ class FileBackend(Level2Backend):
         raise ValueError("file-stage keys live on disk; read path_for(key)")
 
 
+class CascadeBackend(Level2Backend):
+    """Three stages, HBM -> pinned host DRAM -> CKPT files (SURVEY §8(f)
+    row 1, BASELINE config 5): ``dram_slots`` recent boundaries stay in pinned
+    DRAM; older ones are spilled by a native I/O thread to
+    ``<dir>/ckpt_<key>.bin`` in the reference's byte format (storage.py:9-18,
+    CRC32C, O_DIRECT, atomic publish) and read back ahead of their fetch
+    (two boundaries ahead, in the descending order of the multistage backward,
+    runtime.py:297-322).  Errors surface at wait like FileBackend's; existing
+    files can be fetched (resume).  Not capturable into a CUDA graph."""
+
+    def __init__(self, directory, slot_bytes=None, dram_slots: int = 8, device=None):
+        self.directory = Path(directory)
+        self.directory.mkdir(parents=True, exist_ok=True)
+        self.dram_slots = int(dram_slots)
+        super().__init__(slot_bytes=slot_bytes, device=device)
+
+    def _create_native(self, slot_bytes: int) -> int:
+        h = C.c_void_p()
+        N.check(N.lib.ackpt_tier_create_cascade(str(self.directory).encode(), slot_bytes, self.dram_slots,
+                                                C.byref(h)))
+        return h.value
+
+    def path_for(self, key: int) -> Path:
+        return self.directory / f"ckpt_{key}.bin"
+
+    def contains(self, key: int) -> bool:
+        self._ensure(1)
+        return super().contains(key)
+
+    def stats(self) -> dict:
+        """Spill / read counters and host I/O seconds of the file stage."""
+        out = N.CascadeStats()
+        N.check(N.lib.ackpt_tier_cascade_stats(self._ensure(1), C.byref(out)))
+        return {name: getattr(out, name) for name, _ in N.CascadeStats._fields_}
+
+
 class SimulatedBackend(Level2Backend):
     """Pinned-host tier whose transfers take at least latency + size /
     bandwidth (x time_scale) of real time, like the reference's test double
