@@ -2,7 +2,9 @@
 
 Two axes:
   * state size S = 16 MiB .. 4 GiB (B = S / (2 d 4), d = 8, fp32) over the
-    pinned-host tier and the file (CKPT, NVMe/page-cache) third stage;
+    pinned-host tier, the file (CKPT, page cache) tier and the three-stage
+    cascade (pinned DRAM for --dram-slots boundaries, the rest spilled to CKPT
+    files with O_DIRECT and read back ahead of the backward);
   * at S = 64 MiB, the host link throttled to 56 / 16 / 4 / 1 GB/s
     (SimulatedBackend), which sweeps t_t / t_a at a fixed step cost.
 For each point: calibrated t_a, t_b, t_t, the interval I = ceil(t_t / t_a),
@@ -14,7 +16,7 @@ run achieved.  Level-1 budget: slots = min(0.1 n - 1, 96 GiB / S - 2).
 One JSON line per point, then a summary line.
 
   python tools/sweep_c5.py [--sizes-mib 16,64,256,1024,4096] [--tiers pinned,file]
-                           [--sim-gbs 16,4,1] [--n 2000] [--file-dir /tmp/ackpt_c5]
+                           [--sim-gbs 16,4,1] [--n 2000] [--file-dir /tmp/ackpt_c5] [--dram-slots 8]
 """
 
 import argparse
@@ -102,6 +104,12 @@ def point(d, B, S, n, tier, backend, t_step, fuse, extra, n_max):
         "peak_l1_states": st.peak_l1_bytes / S,
         "adjoint_finite": bool(torch.isfinite(adj).all()),
     }
+    if hasattr(backend, "stats"):  # three-stage tier: what the file stage did in the timed pass and its warm-up
+        cs = backend.stats()
+        row["cascade"] = {**cs,
+                          "spill_gbs": cs["spill_bytes"] / cs["spill_seconds"] / 1e9 if cs["spill_seconds"] else None,
+                          "read_gbs": cs["read_bytes"] / cs["read_seconds"] / 1e9 if cs["read_seconds"] else None,
+                          "note": "O_DIRECT file I/O (no page cache); counters cover the warm-up pass too"}
     del ops, s0, adj
     torch.cuda.empty_cache()
     return row
@@ -117,6 +125,7 @@ def main():
     ap.add_argument("--n-large", type=int, default=1000, help="n for states >= 1 GiB")
     ap.add_argument("--n-max", type=int, default=20000, help="cap of n when scaling n to 8 intervals")
     ap.add_argument("--file-dir", default="/tmp/ackpt_c5")
+    ap.add_argument("--dram-slots", type=int, default=8, help="DRAM boundaries of the cascade tier")
     ap.add_argument("--per-step", dest="fuse", action="store_false")
     ap.add_argument("--d", type=int, default=8)
     args = ap.parse_args()
@@ -131,10 +140,13 @@ def main():
         n = args.n if S < GiB else args.n_large
         t_step, n_full = store_all_per_step(d, B, S, args.fuse)
         for tier in tiers:
-            if tier == "file" and mib not in file_sizes:
+            if tier in ("file", "cascade") and mib not in file_sizes:
                 continue
             if tier == "pinned":
                 backend = pkg.PinnedHostBackend(slot_bytes=S)
+            elif tier == "cascade":
+                shutil.rmtree(args.file_dir, ignore_errors=True)
+                backend = pkg.CascadeBackend(args.file_dir, slot_bytes=S, dram_slots=args.dram_slots)
             else:
                 shutil.rmtree(args.file_dir, ignore_errors=True)
                 backend = pkg.FileBackend(args.file_dir, slot_bytes=S)
@@ -142,7 +154,7 @@ def main():
                 row = point(d, B, S, n, tier, backend, t_step, args.fuse, {"store_all_n": n_full}, args.n_max)
             finally:
                 backend.close()
-                if tier == "file":
+                if tier in ("file", "cascade"):
                     shutil.rmtree(args.file_dir, ignore_errors=True)
             rows.append(row)
             print(json.dumps(row), flush=True)
