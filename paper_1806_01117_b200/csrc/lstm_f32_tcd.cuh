@@ -133,9 +133,11 @@ __host__ __device__ constexpr int tmem_cols(int c) { return c <= 32 ? 32 : c <= 
 // bias hi/lo.  Reverse adds B2 hi/lo (tf32).
 template <int D>
 struct Layout {
-  static constexpr int kA = 128 * D, kOne = 128 * 8, kW = 4 * D * D, kBias = 4 * D * 8, kW2 = 4 * D * D;
+  // ones: one 8-row group [1, 1, 1, 0 x 5] read with stride-byte-offset 0
+  // (broadcast to all 16 row groups); bias: row n = split3(scaled xb) exactly
+  static constexpr int kA = 128 * D, kOne = 8 * 8, kW = 4 * D * D, kBias = 4 * D * 8, kW2 = 4 * D * D;
   static constexpr int a_hi = 0, a_lo = a_hi + kA, one = a_lo + kA, w_hi = one + kOne, w_lo = w_hi + kW,
-                       b_hi = w_lo + kW, b_lo = b_hi + kBias, fwd_end = b_lo + kBias;
+                       b_hi = w_lo + kW, fwd_end = b_hi + kBias;
   static constexpr int w2_hi = fwd_end, w2_lo = w2_hi + kW2, rev_end = w2_lo + kW2;
   static constexpr size_t fwd_bytes = size_t(fwd_end) * 4 + 64, rev_bytes = size_t(rev_end) * 4 + 64;
 };
@@ -170,8 +172,10 @@ __device__ __forceinline__ void setup(float* sm, uint64_t* bars, uint32_t* tmem_
     for (int i = 0; i < nbars; ++i) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(bars + i)));
     asm volatile("fence.mbarrier_init.release.cluster;");
   }
-  *reinterpret_cast<float4*>(sm + L::one + kofs<8>(tid, 0)) = make_float4(1.f, 0.f, 0.f, 0.f);
-  *reinterpret_cast<float4*>(sm + L::one + kofs<8>(tid, 4)) = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (tid < 8) {
+    *reinterpret_cast<float4*>(sm + L::one + kofs<8>(tid, 0)) = make_float4(1.f, 1.f, 1.f, 0.f);
+    *reinterpret_cast<float4*>(sm + L::one + kofs<8>(tid, 4)) = make_float4(0.f, 0.f, 0.f, 0.f);
+  }
   // each warp writes one (8-row, 4-k) core-matrix block per iteration: the
   // 32 lanes hit 32 distinct banks (row-major order was an 8-way conflict)
   for (int idx = tid; idx < 4 * D * D; idx += kThreads) {
@@ -186,7 +190,6 @@ __device__ __forceinline__ void setup(float* sm, uint64_t* bars, uint32_t* tmem_
   for (int idx = tid; idx < 4 * D * 8; idx += kThreads) {
     const int n = idx / 8, k = idx % 8;
     sm[L::b_hi + kofs<8>(n, k)] = 0.f;
-    sm[L::b_lo + kofs<8>(n, k)] = 0.f;
   }
 }
 
@@ -208,8 +211,8 @@ __device__ __forceinline__ void stage(float* sm, const float2 (&h)[D / 2], const
     int gi, j;
     gate_of(n, gi, j);
     const float x = __ldg(xbs_k + gi * D + j);  // table is gate-major
-    sm[L::b_hi + kofs<8>(n, 0)] = hi_part(x);
-    sm[L::b_lo + kofs<8>(n, 0)] = x - hi_part(x);
+    const float hi = hi_part(x), r = x - hi, mid = hi_part(r);  // x = hi + mid + lo exactly (tf32 parts)
+    *reinterpret_cast<float4*>(sm + L::b_hi + kofs<8>(n, 0)) = make_float4(hi, mid, r - mid, 0.f);
   }
 }
 
@@ -228,9 +231,8 @@ __device__ __forceinline__ void issue_gates(float* sm, uint32_t tmem, uint64_t* 
     mma_ss(tmem, ah, wl, id, 1u);
     mma_ss(tmem, ah, wh, id, 1u);
   }
-  const uint64_t one = desc(su32(sm + L::one), 256);
-  mma_ss(tmem, one, desc(su32(sm + L::b_lo), 256), id, 1u);
-  mma_ss(tmem, one, desc(su32(sm + L::b_hi), 256), id, 1u);
+  const uint64_t one = desc(su32(sm + L::one), 0);  // broadcast row group
+  mma_ss(tmem, one, desc(su32(sm + L::b_hi), 256), id, 1u);  // exact bias (lstm_f32_tc.cuh)
   commit(bar);
 }
 
