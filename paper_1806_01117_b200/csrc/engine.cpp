@@ -220,7 +220,20 @@ struct Run {
     if (--refs[size_t(id)] == 0) {
       free_list.push_back(id);
       --in_use;
+      // ACKPT_POISON=1 (race check): a released buffer is filled
+      // with NaN bit patterns on the compute stream.  A copy engine still
+      // reading it (a store whose wait is missing) or a kernel reading a
+      // fetch destination before its H2D copy landed then sees NaN, which the
+      // bit-identity / oracle checks of the test suite turn into failures.
+      if (!dry && poison()) ACKPT_CUDA_CHECK(cudaMemsetAsync(E->bufs[size_t(id)], 0xFF, size_t(E->S), s));
     }
+  }
+  static bool poison() {
+    static const bool on = [] {
+      const char* v = std::getenv("ACKPT_POISON");
+      return v && v[0] == '1';
+    }();
+    return on;
   }
   const void* ptr(int id) const { return id == kExt ? ext : E->bufs[size_t(id)]; }
   void* wptr(int id) const { return E->bufs[size_t(id)]; }
@@ -587,6 +600,7 @@ void alloc_pool(ackpt_engine* E, int64_t need_bufs, size_t need_events) {
     E->slabs.push_back(slab);
     for (int64_t i = 0; i < add; ++i)
       E->bufs.push_back(static_cast<char*>(slab) + size_t(i) * size_t(E->S));
+    if (Run::poison()) ACKPT_CUDA_CHECK(cudaMemset(slab, 0xFF, size_t(add) * size_t(E->S)));  // never-written = NaN
   }
   if (!E->adj_internal) ACKPT_CUDA_CHECK(cudaMalloc(&E->adj_internal, size_t(E->S)));
   while (E->timing.size() < need_events) {
