@@ -22,7 +22,7 @@ struct ackpt_lstm {
   void* d_xb = nullptr;                             // n x 4 x d, dtype
   void* d_xbs = nullptr;  // n x 4 x d fp32, pre-scaled per gate (fp32 fast path, d <= 16)
   void* d_ws = nullptr;       // fp32 d in {16, 32, 64}: 4 x d x d pre-scaled W (lstm_f32_tcd.cu)
-  void* d_scratch = nullptr;  // fp32 d = 64 reverse: gate-adjoint table [4d][B] (allocated on first use)
+  void* d_scratch = nullptr;  // fp32 d = 64 reverse: chunk image of the scaled W^T (built on first use)
   size_t scratch_bytes = 0;
 };
 

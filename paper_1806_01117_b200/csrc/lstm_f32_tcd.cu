@@ -85,49 +85,37 @@ void rev_launch(const ackpt_lstm* c, int64_t from, int count, const float* const
       ai, ao, c->B, static_cast<const float*>(c->d_xbs), static_cast<const float*>(c->d_ws), from, count, sp);
 }
 
-// d = 64 reverse: per step rev_gates_tcd (tcgen05 gates + gate adjoints) then
-// rev_tmatvec (CUDA-core transposed product), the adjoint updated in place in
-// adj_out; da scratch [4D][B] fp32 cached on the cell.
+// d = 64 reverse: one kernel per launch (rev_tcd64: Wᵀ streamed through a
+// shared-memory ring from a chunk image built once per cell and cached in
+// cell->d_scratch).
 void rev64_launch(const ackpt_lstm* c, int64_t from, int count, const float* const* states, const float* ai,
                   float* ao, cudaStream_t s) {
-  constexpr int D = 64;
-  using L = tcd::Layout<D>;
+  static bool attr = [] {
+    cudaFuncSetAttribute(tcd::rev_tcd64, cudaFuncAttributeMaxDynamicSharedMemorySize, int(tcd::kRev64Smem));
+    cudaFuncSetAttribute(tcd::rev_tcd64, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    return true;
+  }();
+  (void)attr;
   static int sms = [] {
     int dev = 0, n = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
     return n;
   }();
-  static bool attr = [] {
-    cudaFuncSetAttribute(tcd::rev_gates_tcd<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(L::fwd_bytes));
-    cudaFuncSetAttribute(tcd::rev_gates_tcd<D>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-    cudaFuncSetAttribute(tcd::rev_tmatvec<D, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * D * D * 4);
-    return true;
-  }();
-  (void)attr;
   auto* cell = const_cast<ackpt_lstm*>(c);
-  const size_t da_bytes = size_t(4) * D * size_t(c->B) * sizeof(float);
-  if (cell->scratch_bytes < da_bytes) {
-    if (cell->d_scratch) cudaFree(cell->d_scratch);
-    cell->d_scratch = nullptr;
-    cell->scratch_bytes = 0;
-    ACKPT_CUDA_CHECK(cudaMalloc(&cell->d_scratch, da_bytes));
-    cell->scratch_bytes = da_bytes;
+  constexpr size_t img_bytes = size_t(tcd::kChunks64) * 2 * tcd::kChunkFloats64 * sizeof(float);
+  if (!cell->d_scratch) {
+    ACKPT_CUDA_CHECK(cudaMalloc(&cell->d_scratch, img_bytes));
+    cell->scratch_bytes = img_bytes;
+    tcd::w2_image64<<<64, 256, 0, s>>>(static_cast<const float*>(c->d_ws), static_cast<float*>(cell->d_scratch));
   }
-  float* da = static_cast<float*>(cell->d_scratch);
-  const auto xbs = static_cast<const float*>(c->d_xbs);
-  const auto ws = static_cast<const float*>(c->d_ws);
-  const unsigned g1 = tcd_grid(c->B, 1, tcd::rev_gates_tcd<D>, L::fwd_bytes, true, tcd::tmem_cols(4 * D));
-  int per_sm = 1;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tcd::rev_tmatvec<D, 1>, 256, 4 * D * D * 4);
-  const unsigned g2 = unsigned(std::min<int64_t>((c->B + 255) / 256, int64_t(std::max(1, per_sm)) * sms));
-  const float* in = ai;
-  for (int i = count - 1; i >= 0; --i) {
-    tcd::rev_gates_tcd<D><<<g1, tcd::kThreads, L::fwd_bytes, s>>>(states[i], in, ao, da, c->B,
-                                                                   xbs + (from + i) * 4 * D, ws);
-    tcd::rev_tmatvec<D, 1><<<g2, 256, 4 * D * D * 4, s>>>(da, ao, c->B, ws);
-    in = ao;  // in place from here on
-  }
+  tcd::StatePtrs sp{};
+  for (int i = 0; i < count; ++i) sp.p[i] = states[i];
+  const unsigned tiles = tcd_tiles(c->B);
+  const unsigned grid = count > 1 ? tiles : std::min<unsigned>(tiles, unsigned(sms));  // one CTA per SM
+  tcd::rev_tcd64<<<grid, tcd::kThreads64, tcd::kRev64Smem, s>>>(
+      ai, ao, c->B, static_cast<const float*>(c->d_xbs), static_cast<const float*>(c->d_ws),
+      static_cast<const float*>(cell->d_scratch), from, count, sp);
 }
 
 }  // namespace
@@ -150,8 +138,7 @@ bool tcd_common(const ackpt_lstm* c, std::initializer_list<const void*> ptrs) {
 bool tcd_ok(const ackpt_lstm* c, std::initializer_list<const void*> ptrs) {
   return (c->d == 16 || c->d == 32 || c->d == 64) && tcd_common(c, ptrs);
 }
-// Reverse kernels: d in {16, 32} (one fused kernel), d = 64 (two kernels per
-// step, rev64_launch).
+// Reverse kernels: d in {16, 32} (rev_tcd), d = 64 (rev_tcd64, Wᵀ streamed).
 bool tcd_rev_ok(const ackpt_lstm* c, std::initializer_list<const void*> ptrs) {
   return (c->d == 16 || c->d == 32 || c->d == 64) && tcd_common(c, ptrs);
 }

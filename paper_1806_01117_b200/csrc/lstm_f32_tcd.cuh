@@ -446,137 +446,241 @@ __global__ void __launch_bounds__(kThreads)
   if (threadIdx.x < 32) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kCols));
 }
 
-// ---- d = 64 reverse: two kernels per step ---------------------------------
-// W and Wᵀ do not both fit next to the A tiles at d = 64, so a reverse step
-// is split: rev_gates_tcd computes the gates on tcgen05 (as the forward), the
-// gate adjoints (bwd_unit) and the new dc, writing the adjoints da to a
-// scratch table [4D][B]; rev_tmatvec then forms dh = W_sᵀ da on the CUDA
-// cores (fp32, W_s from shared memory, float2-paired outputs).  The adjoint
-// is updated in place (each thread reads its own sequence's dh / dc before
-// writing them), so a Reverse run needs only the da table as scratch.
-__device__ __forceinline__ float2 ld_pair(const float* __restrict__ x, int64_t B, int64_t b, int row) {
-  return make_float2(ldg_nc(x + int64_t(row) * B + b), ldg_nc(x + int64_t(row + 1) * B + b));
+// ---- d = 64 reverse: one kernel, Wᵀ streamed ------------------------------
+// At d = 64 the gate operands (A = h hi/lo 64 KB, W hi/lo 128 KB, bias 8 KB)
+// fill the shared memory, so the B operand of the transposed product
+// dh = da · B2ᵀ (B2 = Wᵀ, another 128 KB as hi/lo, and kind::tf32 operands
+// cannot be read transposed: tools/umma_layout_probe.cu) streams every step
+// from a pre-split chunk image in global memory (128 KB per cell, L2
+// resident) through a ring of kRing64 shared-memory stages, one K = 8 chunk
+// (N = 64 rows x K = 8, hi and lo, 4 KB) per stage.  Warp roles: warps 0-3
+// compute (sequence = thread = TMEM lane, as rev_tcd), warp 4 issues every
+// MMA (one thread), warp 5 produces the ring (one thread, cp.async.bulk,
+// full / empty mbarriers; an empty barrier is released by tcgen05.commit when
+// the MMAs reading the stage complete).  The compute warps and the issuer
+// meet at named barrier 1 (160 threads); the producer runs ahead on the
+// mbarriers only.  Arithmetic as rev_tcd: 3xTF32 gates and transposed
+// product, da in TMEM as the A operand, two K halves sharing the residual.
+constexpr int kChunks64 = 4 * 64 / 8;    // K = 8 chunks of the transposed product per step
+constexpr int kChunkFloats64 = 64 * 8;   // one part (hi or lo) of a chunk: 2 KB
+#ifndef ACKPT_RING64
+#define ACKPT_RING64 6
+#endif
+constexpr int kRing64 = ACKPT_RING64;
+constexpr int kThreads64 = 192;
+constexpr size_t kRev64Smem = size_t(Layout<64>::fwd_end) * 4 + size_t(kRing64) * 2 * kChunkFloats64 * 4 + 256;
+
+// Chunk image of B2 = scaled Wᵀ for the d = 64 reverse: chunk c (gate rows
+// n in [8c, 8c + 8), the K index of the transposed product) is [hi | lo],
+// each N = 64 (m) x K = 8, K-major core matrices (LBO 128 B, SBO 256 B).
+__global__ void w2_image64(const float* __restrict__ ws, float* __restrict__ img) {
+  constexpr int D = 64;
+  for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < kChunks64 * 2 * kChunkFloats64;
+       idx += gridDim.x * blockDim.x) {
+    const int c = idx / (2 * kChunkFloats64), part = (idx / kChunkFloats64) & 1, e = idx % kChunkFloats64;
+    const int m = (e / 64) * 8 + ((e % 32) / 4), k = ((e % 64) / 32) * 4 + (e % 4);
+    int gi, j;
+    gate_of(8 * c + k, gi, j);
+    const float x = ws[(gi * D + j) * D + m];
+    img[idx] = part ? x - hi_part(x) : hi_part(x);
+  }
 }
 
-template <int D>
-__global__ void __launch_bounds__(kThreads)
-    rev_gates_tcd(const float* __restrict__ state, const float* adj_in, float* adj_out, float* __restrict__ da_out,
-                  int64_t B, const float* __restrict__ xbs_k, const float* __restrict__ ws) {
+__device__ __forceinline__ void bar_compute_issue() { asm volatile("bar.sync 1, 160;" ::: "memory"); }
+
+__global__ void __launch_bounds__(kThreads64, 1)
+    rev_tcd64(const float* __restrict__ adj_in, float* __restrict__ adj_out, int64_t B,
+              const float* __restrict__ xbs_all, const float* __restrict__ ws, const float* __restrict__ w2img,
+              int64_t from, int count, const __grid_constant__ StatePtrs states) {
+  constexpr int D = 64;
   using L = Layout<D>;
   extern __shared__ __align__(128) float sm[];
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sm + L::fwd_end);
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 2);
-  setup<D>(sm, bars, tslot, ws, tmem_cols(4 * D), 1);
-  const uint32_t tmem = tmem_base(tslot);
-  const uint32_t lane = uint32_t((threadIdx.x >> 5) * 32) << 16;
-  uint32_t ph = 0;
-  for (int64_t tile = blockIdx.x; tile * kThreads < B; tile += gridDim.x, ++ph) {
-    const int64_t b = tile * kThreads + threadIdx.x;
-    const bool live = b < B;
-    {
-      float2 h[D / 2];
+  float* ring = sm + L::fwd_end;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(ring + kRing64 * 2 * kChunkFloats64);
+  uint64_t* bar_g = bars;               // gate MMAs done
+  uint64_t* bar_t = bars + 1;           // transposed-product half done (completes twice per step)
+  uint64_t* full = bars + 2;            // [kRing64] chunk landed
+  uint64_t* empty = bars + 2 + kRing64; // [kRing64] chunk consumed by the MMAs
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 2 + 2 * kRing64);
+  constexpr int kCols = 512;
+  constexpr uint32_t kLo = 4 * D, kDh = 6 * D;
+  constexpr int kHalf = D / 4;  // unit pairs (= K chunks) per K half
+  const int tid = threadIdx.x, warp = tid >> 5;
+  const int64_t tiles = (B + kThreads - 1) / kThreads;
+  const int my_tiles = blockIdx.x < tiles ? int((tiles - 1 - blockIdx.x) / gridDim.x + 1) : 0;
+
+  // setup: TMEM (warp 0), barriers, ones, W, zero bias rows (compute threads)
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(tslot)), "r"(kCols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (tid == 0) {
+    for (int i = 0; i < 2 + 2 * kRing64; ++i) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(bars + i)));
+    asm volatile("fence.mbarrier_init.release.cluster;");
+  }
+  if (tid < kThreads) {
+    if (tid < 8) {
+      *reinterpret_cast<float4*>(sm + L::one + kofs<8>(tid, 0)) = make_float4(1.f, 1.f, 1.f, 0.f);
+      *reinterpret_cast<float4*>(sm + L::one + kofs<8>(tid, 4)) = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    for (int idx = tid; idx < 4 * D * D; idx += kThreads) {  // conflict-free order (setup)
+      const int q = idx & 31, blk = idx >> 5;
+      const int n = (blk / (D / 4)) * 8 + (q >> 2), k = (blk % (D / 4)) * 4 + (q & 3);
+      int gi, j;
+      gate_of(n, gi, j);
+      const float x = __ldg(ws + (gi * D + j) * D + k);
+      sm[L::w_hi + kofs<D>(n, k)] = hi_part(x);
+      sm[L::w_lo + kofs<D>(n, k)] = x - hi_part(x);
+    }
+    for (int idx = tid; idx < 4 * D * 8; idx += kThreads) sm[L::b_hi + kofs<8>(idx / 8, idx % 8)] = 0.f;
+  }
+  const uint32_t tmem = tmem_base(tslot);  // (all 192 threads: a full barrier)
+
+  if (warp == 5) {  // ---- producer: the chunk sequence, step after step
+    if (tid == 5 * 32) {
+      const int64_t total = int64_t(my_tiles) * count * kChunks64;
+      for (int64_t it = 0; it < total; ++it) {
+        const int st = int(it % kRing64);
+        if (it >= kRing64) wait_bar(empty + st, uint32_t((it / kRing64 - 1) & 1));
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(full + st)),
+                     "r"(uint32_t(2 * kChunkFloats64 * 4))
+                     : "memory");
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                         su32(ring + st * 2 * kChunkFloats64)),
+                     "l"(w2img + (it % kChunks64) * 2 * kChunkFloats64), "r"(uint32_t(2 * kChunkFloats64 * 4)),
+                     "r"(su32(full + st))
+                     : "memory");
+      }
+    }
+  } else if (warp == 4) {  // ---- MMA issuer
+    int64_t it = 0;
+    for (int t = 0; t < my_tiles; ++t)
+      for (int i = 0; i < count; ++i) {
+        bar_compute_issue();  // A operand and bias staged
+        if (tid == 4 * 32) issue_gates<D>(sm, tmem, bar_g);
+        __syncwarp();
+#pragma unroll 1
+        for (int half = 0; half < 2; ++half) {
+          bar_compute_issue();  // this half's da in TMEM
+          if (tid == 4 * 32) {
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            constexpr uint32_t id = idesc<D>(false);
+#pragma unroll 1
+            for (int q = 0; q < kHalf; ++q, ++it) {
+              const int ks = half * kHalf + q, st = int(it % kRing64);
+              wait_bar(full + st, uint32_t((it / kRing64) & 1));
+              const uint32_t base = su32(ring + st * 2 * kChunkFloats64);
+              const uint64_t bh = desc(base, 256), bl = desc(base + kChunkFloats64 * 4, 256);
+              mma_ts(tmem + kDh, tmem + kLo + uint32_t(8 * q), bh, id, (half == 0 && q == 0) ? 0u : 1u, false);
+              mma_ts(tmem + kDh, tmem + uint32_t(8 * ks), bl, id, 1u, false);
+              mma_ts(tmem + kDh, tmem + uint32_t(8 * ks), bh, id, 1u, false);
+              commit(empty + st);
+            }
+            commit(bar_t);
+          }
+          __syncwarp();
+        }
+      }
+  } else {  // ---- compute warps
+    const uint32_t lane = uint32_t(warp * 32) << 16;
+    uint32_t phase = 0, phase_t = 0;
+    for (int t = 0; t < my_tiles; ++t) {
+      const int64_t tile = blockIdx.x + int64_t(t) * gridDim.x;
+      const int64_t b = tile * kThreads + tid;
+      const bool live = b < B;
+      float2 dh[D / 2], dc[D / 2];
       if (live) {
-        load_rows<D>(state, B, b, 0, h);
+        load_rows<D>(adj_in, B, b, 0, dh);
+        load_rows<D>(adj_in, B, b, D, dc);
       } else {
 #pragma unroll
-        for (int p = 0; p < D / 2; ++p) h[p] = make_float2(0.f, 0.f);
+        for (int p = 0; p < D / 2; ++p) dh[p] = dc[p] = make_float2(0.f, 0.f);
       }
-      stage<D>(sm, h, xbs_k);
-    }
-    publish();
-    if (threadIdx.x == 0) issue_gates<D>(sm, tmem, bars);
-    // c, dh, dc of a group of 4 unit pairs are loaded one group ahead (the
-    // first group while the gate MMAs run)
-    float2 cq[4], dhq[4], dcq[4];
-    auto load_group = [&](int p0) {
+      for (int i = count - 1; i >= 0; --i, ++phase) {
+        {
+          float2 h[D / 2];
+          if (live) load_rows<D>(states.p[i], B, b, 0, h);
+          else
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const int p = p0 + q;
-        if (live) {
-          cq[q] = ld_pair(state, B, b, D + 2 * p);
-          dhq[q] = make_float2(adj_in[int64_t(2 * p) * B + b], adj_in[int64_t(2 * p + 1) * B + b]);
-          dcq[q] = make_float2(adj_in[int64_t(D + 2 * p) * B + b], adj_in[int64_t(D + 2 * p + 1) * B + b]);
+            for (int p = 0; p < D / 2; ++p) h[p] = make_float2(0.f, 0.f);
+          stage<D>(sm, h, xbs_all + (from + i) * 4 * D);
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+        bar_compute_issue();
+        const float* xs = states.p[i];
+        // c of a group of 4 unit pairs is loaded one group ahead (the first
+        // group while the gate MMAs run)
+        float2 cq[4];
+        auto load_c = [&](int p0) {
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            cq[q] = live ? make_float2(ldg_nc(xs + int64_t(D + 2 * (p0 + q)) * B + b),
+                                       ldg_nc(xs + int64_t(D + 2 * (p0 + q) + 1) * B + b))
+                         : make_float2(0.f, 0.f);
+        };
+        load_c(0);
+        wait_bar(bar_g, phase & 1u);
+#pragma unroll
+        for (int grp = 0; grp < D / 8; ++grp) {
+          const int p0 = 4 * grp, half = grp / (kHalf / 4);
+          float g[4][8];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) ld8(tmem + lane + uint32_t(8 * (p0 + q)), g[q]);
+          float2 c[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) c[q] = cq[q];
+          if (grp + 1 < D / 8) load_c(p0 + 4);
+          ld_wait();
+          if (p0 == kHalf) {  // the residual region is free once half 0's MMAs are done
+            wait_bar(bar_t, phase_t & 1u);
+            ++phase_t;
+          }
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const int p = p0 + q;
+            float2 da[4];
+            bwd_unit(make_float2(g[q][0], g[q][1]), make_float2(g[q][2], g[q][3]), make_float2(g[q][4], g[q][5]),
+                     make_float2(g[q][6], g[q][7]), c[q], dh[p], dc[p], da[0], da[1], da[2], da[3], dc[p]);
+            uint32_t hv[8], lv[8];
+#pragma unroll
+            for (int gi = 0; gi < 4; ++gi) {
+              const float2 hi = make_float2(hi_part(da[gi].x), hi_part(da[gi].y));
+              const float2 lo = sub2(da[gi], hi);
+              hv[2 * gi] = __float_as_uint(hi.x);
+              hv[2 * gi + 1] = __float_as_uint(hi.y);
+              lv[2 * gi] = __float_as_uint(lo.x);
+              lv[2 * gi + 1] = __float_as_uint(lo.y);
+            }
+            st8(tmem + lane + uint32_t(8 * p), hv);
+            st8(tmem + lane + kLo + uint32_t(8 * (p - half * kHalf)), lv);
+          }
+          if (p0 + 4 == (half + 1) * kHalf) {  // this half's da is in TMEM: the issuer may go
+            asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+            bar_compute_issue();
+          }
+        }
+        wait_bar(bar_t, phase_t & 1u);
+        ++phase_t;
+#pragma unroll
+        for (int m0 = 0; m0 < D; m0 += 8) {
+          float v[8];
+          ld8(tmem + lane + kDh + uint32_t(m0), v);
+          ld_wait();
+#pragma unroll
+          for (int q = 0; q < 4; ++q) dh[m0 / 2 + q] = make_float2(v[2 * q], v[2 * q + 1]);
         }
       }
-    };
-    load_group(0);
-    wait_bar(bars, ph & 1u);
-#pragma unroll 1
-    for (int p0 = 0; p0 < D / 2; p0 += 4) {
-      float g[4][8];
-#pragma unroll
-      for (int q = 0; q < 4; ++q) ld8(tmem + lane + uint32_t(8 * (p0 + q)), g[q]);
-      float2 cc[4], dhc[4], dcc[4];
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        cc[q] = cq[q];
-        dhc[q] = dhq[q];
-        dcc[q] = dcq[q];
-      }
-      if (p0 + 4 < D / 2) load_group(p0 + 4);
-      ld_wait();
-      if (!live) continue;
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const int p = p0 + q;
-        const float2 c = cc[q], dh = dhc[q], dc = dcc[q];
-        float2 da[4], dcn;
-        bwd_unit(make_float2(g[q][0], g[q][1]), make_float2(g[q][2], g[q][3]), make_float2(g[q][4], g[q][5]),
-                 make_float2(g[q][6], g[q][7]), c, dh, dc, da[0], da[1], da[2], da[3], dcn);
-#pragma unroll
-        for (int gi = 0; gi < 4; ++gi) {
-          da_out[int64_t(gi * D + 2 * p) * B + b] = da[gi].x;
-          da_out[int64_t(gi * D + 2 * p + 1) * B + b] = da[gi].y;
-        }
-        adj_out[int64_t(D + 2 * p) * B + b] = dcn.x;
-        adj_out[int64_t(D + 2 * p + 1) * B + b] = dcn.y;
+      if (live) {
+        store_rows<D>(adj_out, B, b, 0, dh);
+        store_rows<D>(adj_out, B, b, D, dc);
       }
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
-  if (threadIdx.x < 32)
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(tmem_cols(4 * D)));
-}
-
-// dh[m] = sum_n W_s[n][m] da[n] (n = gate * D + unit, lstm.py:149-150 with
-// the scaled weights / adjoints of bwd_unit).  kParts threads per sequence
-// (adjacent lanes, D / kParts outputs each), outputs paired for FFMA2, W_s
-// broadcast from shared memory.  Measured at d = 64, B = 65536: kParts = 1
-// is fastest (reverse step 147 us; 2: 212, 4: 351 -- the extra da loads and
-// shorter FFMA2 runs cost more than the added warps gain).
-template <int D, int kParts>
-__global__ void __launch_bounds__(256)
-    rev_tmatvec(const float* __restrict__ da, float* __restrict__ adj_out, int64_t B, const float* __restrict__ ws) {
-  constexpr int kM = D / kParts;
-  extern __shared__ __align__(16) float w[];  // [4D][D]
-  for (int i = threadIdx.x; i < 4 * D * D / 4; i += blockDim.x)
-    reinterpret_cast<float4*>(w)[i] = __ldg(reinterpret_cast<const float4*>(ws) + i);
-  __syncthreads();
-  const int part = threadIdx.x % kParts;
-  for (int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; t < B * kParts;
-       t += int64_t(gridDim.x) * blockDim.x) {
-    const int64_t b = t / kParts;
-    float2 acc[kM / 2];
-#pragma unroll
-    for (int m = 0; m < kM / 2; ++m) acc[m] = make_float2(0.f, 0.f);
-#pragma unroll 4
-    for (int n = 0; n < 4 * D; ++n) {
-      const float2 a = bc(ldg_nc(da + int64_t(n) * B + b));
-      const float4* row = reinterpret_cast<const float4*>(w + n * D + part * kM);
-#pragma unroll
-      for (int m4 = 0; m4 < kM / 4; ++m4) {
-        const float4 wv = row[m4];
-        acc[2 * m4] = fma2(make_float2(wv.x, wv.y), a, acc[2 * m4]);
-        acc[2 * m4 + 1] = fma2(make_float2(wv.z, wv.w), a, acc[2 * m4 + 1]);
-      }
-    }
-#pragma unroll
-    for (int m = 0; m < kM / 2; ++m) {
-      adj_out[int64_t(part * kM + 2 * m) * B + b] = acc[m].x;
-      adj_out[int64_t(part * kM + 2 * m + 1) * B + b] = acc[m].y;
-    }
-  }
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kCols));
 }
 
 }  // namespace tcd
