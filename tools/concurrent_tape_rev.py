@@ -59,3 +59,39 @@ t_seq = timed(lambda: (tape(), rev()))
 t_con = timed(concurrent)
 print(json.dumps({"tape_ms": t_tape, "rev_ms": t_rev, "sequential_ms": t_seq, "concurrent_ms": t_con,
                   "gain": t_seq / t_con}))
+
+# a backward-like chain: K intervals of (tape, reverse), sequential on one
+# stream vs the next interval's tape on a second stream under this
+# interval's reverse (the tape depends only on the prefetched boundary)
+K = 4
+
+
+def chain_seq():
+    for _ in range(K):
+        tape()
+        rev()
+
+
+def chain_pipe():
+    ev = torch.cuda.Event()
+    ev.record()
+    s1.wait_event(ev)
+    s2.wait_event(ev)
+    with torch.cuda.stream(s1):
+        tape()
+    for k in range(K):
+        done = torch.cuda.Event()
+        done.record(s1)
+        s2.wait_event(done)  # reverse k needs tape k
+        with torch.cuda.stream(s2):
+            rev()
+        if k + 1 < K:
+            with torch.cuda.stream(s1):
+                tape()
+    torch.cuda.current_stream().wait_stream(s1)
+    torch.cuda.current_stream().wait_stream(s2)
+
+
+chain_seq(); chain_pipe()
+t_cs, t_cp = timed(chain_seq), timed(chain_pipe)
+print(json.dumps({"intervals": K, "chain_sequential_ms": t_cs, "chain_pipelined_ms": t_cp, "gain": t_cs / t_cp}))
