@@ -160,6 +160,7 @@ ACKPT_API int ackpt_lstm_create(int32_t d, int64_t n_steps, int64_t batch, int32
               ws[(g * D + j) * D + k] = float(c->wh64[(g * D + j) * D + k] * double(scale[g]));
         ACKPT_CUDA_CHECK(cudaMalloc(&c->d_ws, ws.size() * sizeof(float)));
         ACKPT_CUDA_CHECK(cudaMemcpy(c->d_ws, ws.data(), ws.size() * sizeof(float), cudaMemcpyHostToDevice));
+        ackpt::tcd_build_images(c.get());  // shared-memory weight images, complete before any launch
       }
     }
     *out = c.release();
@@ -175,6 +176,7 @@ ACKPT_API int ackpt_lstm_destroy(ackpt_lstm* cell) {
     if (cell->d_xbs) cudaFree(cell->d_xbs);
     if (cell->d_ws) cudaFree(cell->d_ws);
     if (cell->d_scratch) cudaFree(cell->d_scratch);
+    if (cell->d_wimg) cudaFree(cell->d_wimg);
     delete cell;
   });
 }

@@ -22,7 +22,8 @@ struct ackpt_lstm {
   void* d_xb = nullptr;                             // n x 4 x d, dtype
   void* d_xbs = nullptr;  // n x 4 x d fp32, pre-scaled per gate (fp32 fast path, d <= 16)
   void* d_ws = nullptr;       // fp32 d in {16, 32, 64}: 4 x d x d pre-scaled W (lstm_f32_tcd.cu)
-  void* d_scratch = nullptr;  // fp32 d = 64 reverse: chunk image of the scaled W^T (built on first use)
+  void* d_scratch = nullptr;  // fp32 d = 64 reverse: chunk image of the scaled W^T (tcd_build_images)
+  void* d_wimg = nullptr;     // fp32 d in {16, 32, 64}: shared-memory image of W / W^T hi|lo (tcd_build_images)
   size_t scratch_bytes = 0;
 };
 
@@ -83,6 +84,10 @@ void tcd_forward(const ackpt_lstm* c, int64_t from, int count, const float* in, 
                  cudaStream_t s);
 void tcd_reverse(const ackpt_lstm* c, int64_t from, int count, const float* const* states, const float* adj_in,
                  float* adj_out, cudaStream_t s);
+// At cell creation (d in {16, 32, 64}): the split-weight images the kernels
+// copy into shared memory (d_wimg; d = 64 also the streamed W^T chunks,
+// d_scratch); synchronous.
+void tcd_build_images(ackpt_lstm* c);
 // Generic path, any d <= 128, f32 or f64 (lstm_generic.cu).
 template <typename T>
 void generic_forward(const ackpt_lstm* c, int64_t step, const T* in, T* out, cudaStream_t s);

@@ -13,6 +13,12 @@ namespace {
 
 unsigned tcd_tiles(int64_t B) { return unsigned((B + tcd::kThreads - 1) / tcd::kThreads); }
 
+// The cell's shared-memory weight image (tcd::w_image, tcd_build_images).
+template <int D>
+const float* tcd_wimg(const ackpt_lstm* c, cudaStream_t) {
+  return static_cast<const float*>(c->d_wimg);
+}
+
 // Grid: one CTA per tile for fused launches (long-running); per-step
 // launches run persistent CTAs, as many per SM as fit, each looping over
 // tiles so the weight setup is paid once per CTA.
@@ -44,28 +50,35 @@ unsigned tcd_grid(int64_t B, int count, K kernel, size_t smem, bool persistent, 
   return std::min(tiles, cap);
 }
 
+template <class K>
+void tcd_attrs(K k, size_t smem) {
+  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+  cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100);  // max shared memory
+}
+
 template <int D>
 void fwd_launch(const ackpt_lstm* c, int64_t from, int count, const float* in, float* out, float* const* outs,
                 cudaStream_t s) {
   using L = tcd::Layout<D>;
   static bool attr = [] {
-    for (auto k : {tcd::fwd_tcd<D, false>, tcd::fwd_tcd<D, true>}) {
-      cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(L::fwd_bytes));
-      cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100);  // max shared memory
-    }
+    tcd_attrs(tcd::fwd_tcd<D, false>, L::fwd_bytes);
+    tcd_attrs(tcd::fwd_tcd<D, true>, L::fwd_bytes);
     return true;
   }();
   (void)attr;
   tcd::OutPtrs o{};
   const auto xb = static_cast<const float*>(c->d_xbs);
-  const auto ws = static_cast<const float*>(c->d_ws);
+  const auto ws = tcd_wimg<D>(c, s);
+  const int cols = tcd::tmem_cols(4 * D);
   if (outs) {
     for (int i = 0; i < count; ++i) o.p[i] = outs[i];
-    tcd::fwd_tcd<D, true><<<tcd_grid(c->B, count, tcd::fwd_tcd<D, true>, L::fwd_bytes, true, tcd::tmem_cols(4 * D)), tcd::kThreads, L::fwd_bytes,
-                            s>>>(in, nullptr, c->B, xb, ws, from, count, o);
+    auto k = tcd::fwd_tcd<D, true>;
+    k<<<tcd_grid(c->B, count, k, L::fwd_bytes, true, cols), tcd::kThreads, L::fwd_bytes, s>>>(in, nullptr, c->B, xb,
+                                                                                                ws, from, count, o);
   } else {
-    tcd::fwd_tcd<D, false><<<tcd_grid(c->B, count, tcd::fwd_tcd<D, false>, L::fwd_bytes, true, tcd::tmem_cols(4 * D)), tcd::kThreads,
-                             L::fwd_bytes, s>>>(in, out, c->B, xb, ws, from, count, o);
+    auto k = tcd::fwd_tcd<D, false>;
+    k<<<tcd_grid(c->B, count, k, L::fwd_bytes, true, cols), tcd::kThreads, L::fwd_bytes, s>>>(in, out, c->B, xb, ws,
+                                                                                                from, count, o);
   }
 }
 
@@ -74,15 +87,15 @@ void rev_launch(const ackpt_lstm* c, int64_t from, int count, const float* const
                 cudaStream_t s) {
   using L = tcd::Layout<D>;
   static bool attr = [] {
-    cudaFuncSetAttribute(tcd::rev_tcd<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(L::rev_bytes));
-    cudaFuncSetAttribute(tcd::rev_tcd<D>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    tcd_attrs(tcd::rev_tcd<D>, L::rev_bytes);
     return true;
   }();
   (void)attr;
   tcd::StatePtrs sp{};
   for (int i = 0; i < count; ++i) sp.p[i] = states[i];
-  tcd::rev_tcd<D><<<tcd_grid(c->B, count, tcd::rev_tcd<D>, L::rev_bytes, true, tcd::tmem_cols(7 * D)), tcd::kThreads, L::rev_bytes, s>>>(
-      ai, ao, c->B, static_cast<const float*>(c->d_xbs), static_cast<const float*>(c->d_ws), from, count, sp);
+  auto k = tcd::rev_tcd<D>;
+  k<<<tcd_grid(c->B, count, k, L::rev_bytes, true, tcd::tmem_cols(7 * D)), tcd::kThreads, L::rev_bytes, s>>>(
+      ai, ao, c->B, static_cast<const float*>(c->d_xbs), tcd_wimg<D>(c, s), from, count, sp);
 }
 
 // d = 64 reverse: one kernel per launch (rev_tcd64: Wᵀ streamed through a
@@ -102,23 +115,33 @@ void rev64_launch(const ackpt_lstm* c, int64_t from, int count, const float* con
     cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
     return n;
   }();
-  auto* cell = const_cast<ackpt_lstm*>(c);
-  constexpr size_t img_bytes = size_t(tcd::kChunks64) * 2 * tcd::kChunkFloats64 * sizeof(float);
-  if (!cell->d_scratch) {
-    ACKPT_CUDA_CHECK(cudaMalloc(&cell->d_scratch, img_bytes));
-    cell->scratch_bytes = img_bytes;
-    tcd::w2_image64<<<64, 256, 0, s>>>(static_cast<const float*>(c->d_ws), static_cast<float*>(cell->d_scratch));
-  }
   tcd::StatePtrs sp{};
   for (int i = 0; i < count; ++i) sp.p[i] = states[i];
   const unsigned tiles = tcd_tiles(c->B);
   const unsigned grid = count > 1 ? tiles : std::min<unsigned>(tiles, unsigned(sms));  // one CTA per SM
   tcd::rev_tcd64<<<grid, tcd::kThreads64, tcd::kRev64Smem, s>>>(
-      ai, ao, c->B, static_cast<const float*>(c->d_xbs), static_cast<const float*>(c->d_ws),
-      static_cast<const float*>(cell->d_scratch), from, count, sp);
+      ai, ao, c->B, static_cast<const float*>(c->d_xbs), tcd_wimg<64>(c, s),
+      static_cast<const float*>(c->d_scratch), from, count, sp);
 }
 
 }  // namespace
+
+void tcd_build_images(ackpt_lstm* c) {
+  const auto ws = static_cast<const float*>(c->d_ws);
+  const size_t img = size_t(16) * c->d * c->d * sizeof(float);
+  ACKPT_CUDA_CHECK(cudaMalloc(&c->d_wimg, img));
+  if (c->d == 16) tcd::w_image<16><<<64, 256>>>(ws, static_cast<float*>(c->d_wimg));
+  else if (c->d == 32) tcd::w_image<32><<<64, 256>>>(ws, static_cast<float*>(c->d_wimg));
+  else tcd::w_image<64><<<64, 256>>>(ws, static_cast<float*>(c->d_wimg));
+  if (c->d == 64) {
+    const size_t chunks = size_t(tcd::kChunks64) * 2 * tcd::kChunkFloats64 * sizeof(float);
+    ACKPT_CUDA_CHECK(cudaMalloc(&c->d_scratch, chunks));
+    c->scratch_bytes = chunks;
+    tcd::w2_image64<<<64, 256>>>(ws, static_cast<float*>(c->d_scratch));
+  }
+  ACKPT_CUDA_CHECK(cudaGetLastError());
+  ACKPT_CUDA_CHECK(cudaDeviceSynchronize());
+}
 
 namespace {
 bool tcd_common(const ackpt_lstm* c, std::initializer_list<const void*> ptrs) {

@@ -157,39 +157,85 @@ __device__ __forceinline__ void gate_of(int n, int& gi, int& j) {
   j = 2 * (n >> 3) + (n & 1);
 }
 
-// One-time setup shared by both kernels: TMEM, barriers, ones, W, zero bias rows.
+// Shared-memory image of the split weights, built once per cell
+// (w_image<D>): [W hi | W lo] in the gate operand's layout (rows n = gate
+// rows, K-major, kofs<D>), then [B2 hi | B2 lo] (B2[m][n] = s_gate W_gate[j(n)][m],
+// the reverse's transposed-product operand, kofs<4D>).  The kernels copy it
+// in with cp.async.bulk instead of gathering and splitting W per CTA (the
+// per-step launches spent ~20 % of their stall samples there).
 template <int D>
-__device__ __forceinline__ void setup(float* sm, uint64_t* bars, uint32_t* tmem_slot, const float* __restrict__ ws,
-                                      int cols, int nbars) {
+__global__ void w_image(const float* __restrict__ ws, float* __restrict__ img) {
+  for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < 4 * D * D; idx += gridDim.x * blockDim.x) {
+    {
+      const int n = idx / D, k = idx % D;  // gate operand row n, column k
+      int gi, j;
+      gate_of(n, gi, j);
+      const float x = ws[(gi * D + j) * D + k];
+      img[kofs<D>(n, k)] = hi_part(x);
+      img[4 * D * D + kofs<D>(n, k)] = x - hi_part(x);
+    }
+    {
+      const int m = idx / (4 * D), n = idx % (4 * D);  // B2 row m, column n
+      int gi, j;
+      gate_of(n, gi, j);
+      const float x = ws[(gi * D + j) * D + m];
+      img[8 * D * D + kofs<4 * D>(m, n)] = hi_part(x);
+      img[12 * D * D + kofs<4 * D>(m, n)] = x - hi_part(x);
+    }
+  }
+}
+
+// Thread 0: `floats` floats of the image into shared memory by
+// cp.async.bulk (pieces of <= 32 KB), completing on `bar`, whose expected
+// transaction bytes were set beforehand (expect_bytes, once per phase).
+__device__ __forceinline__ void expect_bytes(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_in(float* dst, const float* src, int floats, uint64_t* bar) {
+  for (int off = 0; off < floats; off += 8192) {
+    const uint32_t bytes = uint32_t(min(8192, floats - off)) * 4u;
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     su32(dst + off)),
+                 "l"(src + off), "r"(bytes), "r"(su32(bar))
+                 : "memory");
+  }
+}
+
+// One-time setup shared by both kernels: TMEM, barriers, ones, zero bias
+// rows, and the weight image (W, plus B2 for the reverse) in flight on
+// bars[nbars] -- thread 0 waits for it before its first MMA (weights_ready).
+template <int D>
+__device__ __forceinline__ void setup(float* sm, uint64_t* bars, uint32_t* tslot, const float* __restrict__ wimg,
+                                      int cols, int nbars, bool rev) {
   using L = Layout<D>;
   const int tid = threadIdx.x;
   if (tid < 32) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(tmem_slot)),
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(tslot)),
                  "r"(cols));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   if (tid == 0) {
-    for (int i = 0; i < nbars; ++i) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(bars + i)));
+    for (int i = 0; i <= nbars; ++i) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(bars + i)));
     asm volatile("fence.mbarrier_init.release.cluster;");
+    expect_bytes(bars + nbars, uint32_t((rev ? 16 : 8) * D * D * 4));
+    bulk_in(sm + L::w_hi, wimg, 8 * D * D, bars + nbars);
+    if (rev) bulk_in(sm + L::w2_hi, wimg + 8 * D * D, 8 * D * D, bars + nbars);
   }
   if (tid < 8) {
     *reinterpret_cast<float4*>(sm + L::one + kofs<8>(tid, 0)) = make_float4(1.f, 1.f, 1.f, 0.f);
     *reinterpret_cast<float4*>(sm + L::one + kofs<8>(tid, 4)) = make_float4(0.f, 0.f, 0.f, 0.f);
   }
-  // each warp writes one (8-row, 4-k) core-matrix block per iteration: the
-  // 32 lanes hit 32 distinct banks (row-major order was an 8-way conflict)
-  for (int idx = tid; idx < 4 * D * D; idx += kThreads) {
-    const int q = idx & 31, blk = idx >> 5;
-    const int n = (blk / (D / 4)) * 8 + (q >> 2), k = (blk % (D / 4)) * 4 + (q & 3);
-    int gi, j;
-    gate_of(n, gi, j);
-    const float x = __ldg(ws + (gi * D + j) * D + k);
-    sm[L::w_hi + kofs<D>(n, k)] = hi_part(x);
-    sm[L::w_lo + kofs<D>(n, k)] = x - hi_part(x);
-  }
   for (int idx = tid; idx < 4 * D * 8; idx += kThreads) {
     const int n = idx / 8, k = idx % 8;
     sm[L::b_hi + kofs<8>(n, k)] = 0.f;
+  }
+}
+
+// Thread 0, before its first MMA: the weight image has landed.
+__device__ __forceinline__ void weights_ready(uint64_t* wbar, bool& ready) {
+  if (!ready) {
+    wait_bar(wbar, 0);
+    ready = true;
   }
 }
 
@@ -271,10 +317,11 @@ __global__ void __launch_bounds__(kThreads)
   extern __shared__ __align__(128) float sm[];
   uint64_t* bars = reinterpret_cast<uint64_t*>(sm + L::fwd_end);
   uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 2);
-  setup<D>(sm, bars, tslot, ws, tmem_cols(4 * D), 1);
+  setup<D>(sm, bars, tslot, ws, tmem_cols(4 * D), 1, false);
   const uint32_t tmem = tmem_base(tslot);
   const uint32_t lane = uint32_t((threadIdx.x >> 5) * 32) << 16;
   uint32_t ph = 0;
+  bool wready = false;
   // persistent over 128-sequence tiles (the weight setup is paid once per CTA)
   for (int64_t tile = blockIdx.x; tile * kThreads < B; tile += gridDim.x) {
   const int64_t b = tile * kThreads + threadIdx.x;
@@ -290,7 +337,10 @@ __global__ void __launch_bounds__(kThreads)
   for (int i = 0; i < count; ++i, ++ph) {
     stage<D>(sm, h, xbs_all + (from + i) * 4 * D);
     publish();
-    if (threadIdx.x == 0) issue_gates<D>(sm, tmem, bars);
+    if (threadIdx.x == 0) {
+      weights_ready(bars + 1, wready);
+      issue_gates<D>(sm, tmem, bars);
+    }
     wait_bar(bars, ph & 1u);
 #pragma unroll
     for (int p0 = 0; p0 < D / 2; p0 += 4) {  // 4 unit pairs per TMEM round trip
@@ -331,22 +381,13 @@ __global__ void __launch_bounds__(kThreads)
   using L = Layout<D>;
   extern __shared__ __align__(128) float sm[];
   uint64_t* bars = reinterpret_cast<uint64_t*>(sm + L::rev_end);
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 2);
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 3);
   constexpr int kCols = tmem_cols(7 * D);
   constexpr uint32_t kLo = 4 * D, kDh = 6 * D;
   constexpr int kHalf = D / 4;  // unit pairs per K half
-  setup<D>(sm, bars, tslot, ws, kCols, 2);
+  setup<D>(sm, bars, tslot, ws, kCols, 2, true);
   const uint32_t tmem = tmem_base(tslot);
-  // B2[m][n] = s_gate W_gate[j(n)][m], K = 4D (gate-row order), tf32 hi/lo
-  for (int idx = threadIdx.x; idx < 4 * D * D; idx += kThreads) {  // conflict-free order, as in setup
-    const int q = idx & 31, blk = idx >> 5;
-    const int m = (blk / D) * 8 + (q >> 2), n = (blk % D) * 4 + (q & 3);
-    int gi, j;
-    gate_of(n, gi, j);
-    const float x = __ldg(ws + (gi * D + j) * D + m);
-    sm[L::w2_hi + kofs<4 * D>(m, n)] = hi_part(x);
-    sm[L::w2_lo + kofs<4 * D>(m, n)] = x - hi_part(x);
-  }
+  bool wready = false;
   const uint32_t lane = uint32_t((threadIdx.x >> 5) * 32) << 16;
   // Thread 0: dh (+)= da . B2^T over unit pairs [p0, p0 + kHalf) (residual at kLo).
   auto issue_half = [&](int p0, bool first) {
@@ -387,7 +428,10 @@ __global__ void __launch_bounds__(kThreads)
     }
     stage<D>(sm, h, xbs_all + (from + i) * 4 * D);
     publish();
-    if (threadIdx.x == 0) issue_gates<D>(sm, tmem, bars);
+    if (threadIdx.x == 0) {
+      weights_ready(bars + 2, wready);
+      issue_gates<D>(sm, tmem, bars);
+    }
     wait_bar(bars, phase & 1u);
 #pragma unroll
     for (int half = 0; half < 2; ++half) {
@@ -490,7 +534,7 @@ __device__ __forceinline__ void bar_compute_issue() { asm volatile("bar.sync 1, 
 
 __global__ void __launch_bounds__(kThreads64, 1)
     rev_tcd64(const float* __restrict__ adj_in, float* __restrict__ adj_out, int64_t B,
-              const float* __restrict__ xbs_all, const float* __restrict__ ws, const float* __restrict__ w2img,
+              const float* __restrict__ xbs_all, const float* __restrict__ wimg, const float* __restrict__ w2img,
               int64_t from, int count, const __grid_constant__ StatePtrs states) {
   constexpr int D = 64;
   using L = Layout<D>;
@@ -501,7 +545,8 @@ __global__ void __launch_bounds__(kThreads64, 1)
   uint64_t* bar_t = bars + 1;           // transposed-product half done (completes twice per step)
   uint64_t* full = bars + 2;            // [kRing64] chunk landed
   uint64_t* empty = bars + 2 + kRing64; // [kRing64] chunk consumed by the MMAs
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 2 + 2 * kRing64);
+  uint64_t* wbar = bars + 2 + 2 * kRing64;  // weight image landed
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 3 + 2 * kRing64);
   constexpr int kCols = 512;
   constexpr uint32_t kLo = 4 * D, kDh = 6 * D;
   constexpr int kHalf = D / 4;  // unit pairs (= K chunks) per K half
@@ -515,22 +560,15 @@ __global__ void __launch_bounds__(kThreads64, 1)
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   if (tid == 0) {
-    for (int i = 0; i < 2 + 2 * kRing64; ++i) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(bars + i)));
+    for (int i = 0; i < 3 + 2 * kRing64; ++i) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(bars + i)));
     asm volatile("fence.mbarrier_init.release.cluster;");
+    expect_bytes(wbar, uint32_t(8 * D * D * 4));
+    bulk_in(sm + L::w_hi, wimg, 8 * D * D, wbar);  // W hi | lo (the issuer waits before its first MMA)
   }
   if (tid < kThreads) {
     if (tid < 8) {
       *reinterpret_cast<float4*>(sm + L::one + kofs<8>(tid, 0)) = make_float4(1.f, 1.f, 1.f, 0.f);
       *reinterpret_cast<float4*>(sm + L::one + kofs<8>(tid, 4)) = make_float4(0.f, 0.f, 0.f, 0.f);
-    }
-    for (int idx = tid; idx < 4 * D * D; idx += kThreads) {  // conflict-free order (setup)
-      const int q = idx & 31, blk = idx >> 5;
-      const int n = (blk / (D / 4)) * 8 + (q >> 2), k = (blk % (D / 4)) * 4 + (q & 3);
-      int gi, j;
-      gate_of(n, gi, j);
-      const float x = __ldg(ws + (gi * D + j) * D + k);
-      sm[L::w_hi + kofs<D>(n, k)] = hi_part(x);
-      sm[L::w_lo + kofs<D>(n, k)] = x - hi_part(x);
     }
     for (int idx = tid; idx < 4 * D * 8; idx += kThreads) sm[L::b_hi + kofs<8>(idx / 8, idx % 8)] = 0.f;
   }
@@ -554,10 +592,14 @@ __global__ void __launch_bounds__(kThreads64, 1)
     }
   } else if (warp == 4) {  // ---- MMA issuer
     int64_t it = 0;
+    bool wready = false;
     for (int t = 0; t < my_tiles; ++t)
       for (int i = 0; i < count; ++i) {
         bar_compute_issue();  // A operand and bias staged
-        if (tid == 4 * 32) issue_gates<D>(sm, tmem, bar_g);
+        if (tid == 4 * 32) {
+          weights_ready(wbar, wready);
+          issue_gates<D>(sm, tmem, bar_g);
+        }
         __syncwarp();
 #pragma unroll 1
         for (int half = 0; half < 2; ++half) {
