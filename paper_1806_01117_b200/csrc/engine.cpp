@@ -1010,9 +1010,13 @@ ACKPT_API int ackpt_engine_calibrate(ackpt_engine* E, ackpt_tier* tier, int64_t 
       }
       // With fused Advance launches the forward sweep runs at the fused
       // per-step cost; calibrate that instead so stores still hide (I grows).
+      // One launch of 64 steps, about the length of the sweep's own Advance
+      // launches (one per interval): a 16-step launch carried ~8 % of launch
+      // ramp and tail at the C2 shape (16.7 vs 15.5 us/step inside the pass),
+      // so I came out short and the sweep stalled on its stores.
       double fused_step = -1.0;
       if (E->fuse && E->op.advance && E->n >= 2) {
-        const int64_t len = std::min<int64_t>(E->n, std::max<int64_t>(trials, 16));
+        const int64_t len = std::min<int64_t>(E->n, std::max<int64_t>(trials, 64));
         cudaEvent_t f0, f1;
         ACKPT_CUDA_CHECK(cudaEventCreate(&f0));
         ACKPT_CUDA_CHECK(cudaEventCreate(&f1));
