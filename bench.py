@@ -36,9 +36,9 @@ if ROOT not in sys.path:
 
 METRIC = "reverse-pass steps/s at memory ratio 0.1, n=10^4 (overhead vs store-all reported beside)"
 # interval of the reference arm's bounded sample when --interval is not given
-# (the calibrated I of the ours arm at C2 is 74-85; the CPU cost per chain
-# step does not depend on it)
-REF_SAMPLE_INTERVAL = 75
+# (the calibrated I of the ours arm at C2 is 79-85 since the 64-step fused
+# calibration; the CPU cost per chain step does not depend on it)
+REF_SAMPLE_INTERVAL = 80
 
 
 def parse_args(argv=None):
