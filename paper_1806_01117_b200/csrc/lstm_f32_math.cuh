@@ -152,6 +152,34 @@ __device__ __forceinline__ float2 fwd_unit_nr(float2 af, float2 ai, float2 ao, f
   return mul2(o, tanh2_nr(c));
 }
 
+// tanh of two float2s sharing one Newton reciprocal: 1/y_a = y_b / (y_a y_b).
+// The exponent argument is clamped at 31, so the product stays below 2^63
+// and the Newton seed in the normal range; tanh = 1 - 2/(1 + 2^31) already
+// rounds to 1.0f, so the clamp changes no result.
+__device__ __forceinline__ void tanh2x2_nr(float2 xa, float2 xb, float2& ta, float2& tb) {
+  const float2 sa = mul2(xa, bc(2.0f * kL2e)), sb = mul2(xb, bc(2.0f * kL2e));
+  const float2 ya = add2(make_float2(ex2(fminf(sa.x, 31.0f)), ex2(fminf(sa.y, 31.0f))), bc(1.0f));
+  const float2 yb = add2(make_float2(ex2(fminf(sb.x, 31.0f)), ex2(fminf(sb.y, 31.0f))), bc(1.0f));
+  const float2 r = rcp2_nr(mul2(ya, yb));
+  ta = fma2(mul2(r, yb), bc(-2.0f), bc(1.0f));
+  tb = fma2(mul2(r, ya), bc(-2.0f), bc(1.0f));
+}
+
+// Forward of two hidden units (or two unit pairs) at once: as fwd_unit_nr,
+// with the two tanh(c') sharing one reciprocal (tanh2x2_nr).
+__device__ __forceinline__ void fwd_units2_nr(const float2 (&pa)[4], const float2 (&pb)[4], float2& ca, float2& cb,
+                                              float2& ha, float2& hb) {
+  float2 fa, ia, oa, ga, fb, ib, ob, gb;
+  activate_nr(pa[0], pa[1], pa[2], pa[3], fa, ia, oa, ga);
+  activate_nr(pb[0], pb[1], pb[2], pb[3], fb, ib, ob, gb);
+  ca = fma2(fa, ca, mul2(ia, ga));
+  cb = fma2(fb, cb, mul2(ib, gb));
+  float2 ta, tb;
+  tanh2x2_nr(ca, cb, ta, tb);
+  ha = mul2(oa, ta);
+  hb = mul2(ob, tb);
+}
+
 __device__ __forceinline__ void bwd_unit_nr(float2 af, float2 ai, float2 ao, float2 ag, float2 c, float2 dhn,
                                             float2 dcn, float2& daf, float2& dai, float2& dao, float2& dag,
                                             float2& dck) {

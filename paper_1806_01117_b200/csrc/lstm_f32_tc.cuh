@@ -272,8 +272,7 @@ __global__ void __launch_bounds__(kThreads, 8)
     for (int u = 0; u < kD; u += 2) {
       float2 pre[2][4];
       read_units(sm, u, pre);
-#pragma unroll
-      for (int q = 0; q < 2; ++q) h[u + q] = fwd_unit_nr(pre[q][0], pre[q][1], pre[q][2], pre[q][3], c[u + q]);
+      fwd_units2_nr(pre[0], pre[1], c[u], c[u + 1], h[u], h[u + 1]);
     }
     if (TAPE && live) {
       float* dst = outs.p[i] + b0;

@@ -349,9 +349,13 @@ __global__ void __launch_bounds__(kThreads)
       for (int q = 0; q < 4; ++q) ld8(tmem + lane + uint32_t(8 * (p0 + q)), g[q]);
       ld_wait();
 #pragma unroll
-      for (int q = 0; q < 4; ++q)
-        h[p0 + q] = fwd_unit_nr(make_float2(g[q][0], g[q][1]), make_float2(g[q][2], g[q][3]),
-                                make_float2(g[q][4], g[q][5]), make_float2(g[q][6], g[q][7]), c[p0 + q]);
+      for (int q = 0; q < 4; q += 2) {  // two unit pairs share the tanh reciprocal
+        const float2 pa[4] = {make_float2(g[q][0], g[q][1]), make_float2(g[q][2], g[q][3]),
+                              make_float2(g[q][4], g[q][5]), make_float2(g[q][6], g[q][7])};
+        const float2 pb[4] = {make_float2(g[q + 1][0], g[q + 1][1]), make_float2(g[q + 1][2], g[q + 1][3]),
+                              make_float2(g[q + 1][4], g[q + 1][5]), make_float2(g[q + 1][6], g[q + 1][7])};
+        fwd_units2_nr(pa, pb, c[p0 + q], c[p0 + q + 1], h[p0 + q], h[p0 + q + 1]);
+      }
     }
     if (TAPE && live) {
       store_rows<D>(outs.p[i], B, b, 0, h);
