@@ -137,21 +137,6 @@ __device__ __forceinline__ void activate_nr(float2 tf, float2 ti, float2 to, flo
   }
 }
 
-// tanh with the exponent argument clamped at 64 so 1 + 2^t stays finite for
-// the Newton reciprocal (tanh rounds to 1.0f long before).
-__device__ __forceinline__ float2 tanh2_nr(float2 x) {
-  const float2 t = mul2(x, bc(2.0f * kL2e));
-  const float2 y = add2(make_float2(ex2(fminf(t.x, 64.0f)), ex2(fminf(t.y, 64.0f))), bc(1.0f));
-  return fma2(rcp2_nr(y), bc(-2.0f), bc(1.0f));
-}
-
-__device__ __forceinline__ float2 fwd_unit_nr(float2 af, float2 ai, float2 ao, float2 ag, float2& c) {
-  float2 f, ig, o, g;
-  activate_nr(af, ai, ao, ag, f, ig, o, g);
-  c = fma2(f, c, mul2(ig, g));
-  return mul2(o, tanh2_nr(c));
-}
-
 // tanh of two float2s sharing one Newton reciprocal: 1/y_a = y_b / (y_a y_b).
 // The exponent argument is clamped at 31, so the product stays below 2^63
 // and the Newton seed in the normal range; tanh = 1 - 2/(1 + 2^31) already
@@ -165,8 +150,9 @@ __device__ __forceinline__ void tanh2x2_nr(float2 xa, float2 xb, float2& ta, flo
   tb = fma2(mul2(r, ya), bc(-2.0f), bc(1.0f));
 }
 
-// Forward of two hidden units (or two unit pairs) at once: as fwd_unit_nr,
-// with the two tanh(c') sharing one reciprocal (tanh2x2_nr).
+// Forward of two hidden units (or two unit pairs) at once (lstm.py:123-129):
+// c' = f c + i g, h' = o tanh(c'), the two tanh(c') sharing one reciprocal
+// (tanh2x2_nr).
 __device__ __forceinline__ void fwd_units2_nr(const float2 (&pa)[4], const float2 (&pb)[4], float2& ca, float2& cb,
                                               float2& ha, float2& hb) {
   float2 fa, ia, oa, ga, fb, ib, ob, gb;
@@ -180,21 +166,6 @@ __device__ __forceinline__ void fwd_units2_nr(const float2 (&pa)[4], const float
   hb = mul2(ob, tb);
 }
 
-__device__ __forceinline__ void bwd_unit_nr(float2 af, float2 ai, float2 ao, float2 ag, float2 c, float2 dhn,
-                                            float2 dcn, float2& daf, float2& dai, float2& dao, float2& dag,
-                                            float2& dck) {
-  float2 f, ig, o, g;
-  activate_nr(af, ai, ao, ag, f, ig, o, g);
-  const float2 cn = fma2(f, c, mul2(ig, g));
-  const float2 t = tanh2_nr(cn);
-  const float2 dco = fma2(mul2(dhn, o), fma2(neg(t), t, bc(1.0f)), dcn);
-  const float2 dcs = mul2(dco, bc(-kLn2));
-  daf = mul2(mul2(dcs, c), fma2(neg(f), f, f));
-  dai = mul2(mul2(dcs, g), fma2(neg(ig), ig, ig));
-  dao = mul2(mul2(dhn, mul2(t, bc(-kLn2))), fma2(neg(o), o, o));
-  dag = mul2(mul2(dco, mul2(ig, bc(0.5f * kLn2))), fma2(neg(g), g, bc(1.0f)));
-  dck = mul2(dco, f);
-}
 
 // Weights pre-scaled per gate (see file comment).
 template <int D>
