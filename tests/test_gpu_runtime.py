@@ -482,3 +482,28 @@ def test_graph_rejects_callback_operators(P):
     )
     with pytest.raises(ValueError):
         pkg.execute(pkg.Revolve(2), ops, lstm.random_state(4, 3), graph=True)
+
+
+def test_pinned_tier_usable_after_graphed_pass(P):
+    # The pinned tier's per-key ordering events are last recorded inside the
+    # capture of a graphed pass; a later backward sweep and a direct fetch on
+    # the same backend must still work (tier_quiesce re-records
+    # them on the idle copy streams), and return the stored bytes.
+    pkg, lstm, _ = P
+    n, d, batch = 24, 8, 4096
+    cell = lstm.random_cell(d, n, 0)
+    ops = lstm.operator_pair(cell, batch, "f32")
+    s0 = lstm.random_states(d, 1, batch, "f32")
+    plan = pkg.plan_multistage(n, 3, 8)
+    with pkg.PinnedHostBackend(slot_bytes=ops.state_size) as b:
+        for _ in range(3):  # eager, captured, replayed
+            adj, st = pkg.execute(pkg.Multistage(3, interval=8), ops, s0, b, fuse=False, graph=True)
+        assert st.stores_issued == 3
+        payload = b.wait(b.begin_fetch(8))
+        state = s0
+        for k in range(8):
+            state = ops.forward_step(k, state)
+        assert torch.equal(payload.data.view(torch.float32).view_as(state), state)
+        seed = lstm.loss_gradient_seed(cell, pkg.run_forward_sweep(plan, ops, b, s0)[1])
+        back = pkg.run_backward_sweep(plan, ops, b, seed)
+    assert torch.equal(back, adj)
