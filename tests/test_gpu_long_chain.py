@@ -113,3 +113,33 @@ def test_random_cell_adjoint_really_underflows(P):
     ops = lstm.operator_pair(lstm.random_cell(d, n, 0), batch, "f32")
     adj, _ = pkg.execute(pkg.FullStorage(), ops, lstm.random_states(d, 1, batch, "f32"), fuse=True)
     assert adj.abs().max().item() < 1e-37
+
+
+@pytest.mark.parametrize("d,n", [(16, 1000), (32, 1000), (64, 200)])
+@pytest.mark.parametrize("fuse", [True, False], ids=["fused", "per-step"])
+def test_tensor_core_large_d_long_chain(P, d, n, fuse):
+    # the d >= 16 tcgen05 kernels (exact bias split, rounded tf32 heads,
+    # unbiased Newton reciprocals, Wᵀ streamed at d = 64) over a long-memory
+    # chain through Multistage, against the float64 oracle.  fp32 rounding
+    # accumulates along the chain at a rate set by the cell (d = 16: 5e-5 at
+    # n = 500, 5e-4 at 2,000; d = 64's adjoint grows ~10^3x per 400 steps), so
+    # the bound is the larger of LONG_TOL and 3x the error of an fp32 numpy
+    # restatement of the same chain on the same rows (the same arithmetic
+    # precision, rounded differently).
+    pkg, lstm = P
+    batch, interval = 4096, 50
+    cell = lstm.long_memory_cell(d, n, 0)
+    ops = lstm.operator_pair(cell, batch, "f32")
+    s0 = lstm.random_states(d, 1, batch, "f32")
+    with pkg.PinnedHostBackend(slot_bytes=ops.state_size) as backend:
+        adj, st = pkg.execute(pkg.Multistage(interval - 1, interval), ops, s0, backend, fuse=fuse)
+    torch.cuda.synchronize()
+    assert st.forward_evals == 2 * n
+    rows = _rows(batch, 32)
+    x0 = s0[:, :, rows].double().cpu().numpy()
+    got = adj[:, :, rows].double().cpu().numpy()
+    ref = _oracle_adjoint(d, n, x0)
+    assert np.linalg.norm(ref) > 1e-30, "adjoint underflowed: the check would be vacuous"
+    f32, _ = RO.execute("full", L.long_memory_cell(d, n, 0), x0.astype(np.float32), dtype=np.float32)
+    bound = max(LONG_TOL, 3 * L.rel_l2(f32, ref))
+    assert L.rel_l2(got, ref) <= bound, (L.rel_l2(got, ref), bound)
