@@ -51,3 +51,30 @@ def test_bench_defaults():
     assert (a.gpus, a.n, a.d, a.batch, a.memory_ratio) == (1, 10_000, 8, 1 << 20, 0.1)
     assert a.warmup >= 3 and a.fuse
     assert not bench.parse_args(["--per-step"]).fuse
+
+
+def test_bench_config4_defaults():
+    import bench
+
+    a = bench.parse_args(["--config", "c4"])
+    assert (a.batch, a.memory_ratio) == (1 << 24, 0.05)
+    assert a.no_other_mode  # the per-step leg would need more pinned slots than the host holds
+    cfg = bench.workload_config(a, int(a.memory_ratio * a.n) - 1)
+    assert cfg["state_bytes_per_gpu"] == 1 << 30 and "config 4" in cfg["workload"]
+
+
+def test_fused_pass_bytes_matches_the_launch_split():
+    # sweep = one Advance launch (2S) per interval + a store (S
+    # read from HBM, S over the link); backward = tape (L+1)S + reverse (L+2)S
+    # per <= 64-step launch + a fetch (S) per interval.
+    import bench
+
+    class St:
+        prefetches_issued = 3
+
+    S, n = 1 << 20, 200
+    b = bench.fused_pass_bytes(n, [0, 80, 160], S, True, St())
+    launches = [64, 16, 64, 16, 40]  # intervals of 80, 80, 40 steps
+    assert b["sweep_link"] == 3 * S and b["sweep_hbm"] == 3 * 2 * S + 3 * S
+    assert b["backward_link"] == 3 * S
+    assert b["backward_hbm"] == sum((c + 1) * S + (c + 2) * S for c in launches) + 3 * S
