@@ -153,13 +153,32 @@ __device__ __forceinline__ void tanh2x2_nr(float2 xa, float2 xb, float2& ta, flo
 // Forward of two hidden units (or two unit pairs) at once (lstm.py:123-129):
 // c' = f c + i g, h' = o tanh(c'), the two tanh(c') sharing one reciprocal
 // (tanh2x2_nr).
+// The forward needs only c' and o, not f and i: with the shared reciprocal
+// r = 1/P, c' = f c + i g = r y_o y_g (y_i c + y_f g)  (lstm.py:127).
+__device__ __forceinline__ void fwd_cell_nr(float2 tf, float2 ti, float2 to, float2 tg, float2& c, float2& o) {
+  const float2 one = bc(1.0f);
+  const float2 yf = add2(ex2_2(tf), one), yi = add2(ex2_2(ti), one);
+  const float2 yo = add2(ex2_2(to), one), yg = add2(ex2_2(tg), one);
+  const float2 p12 = mul2(yf, yi), p34 = mul2(yo, yg);
+  const float2 P = mul2(p12, p34);
+  if (__builtin_expect(P.x <= kShareMax && P.y <= kShareMax, 1)) {
+    const float2 r = rcp2_nr(P);
+    const float2 q34 = mul2(r, p34), q12 = mul2(r, p12);
+    const float2 g = fma2(mul2(q12, yo), bc(-2.0f), one);
+    c = mul2(q34, fma2(yi, c, mul2(yf, g)));
+    o = mul2(q12, yg);
+  } else {
+    const float2 g = fma2(rcp2(yg), bc(-2.0f), one);
+    c = fma2(rcp2(yf), c, mul2(rcp2(yi), g));
+    o = rcp2(yo);
+  }
+}
+
 __device__ __forceinline__ void fwd_units2_nr(const float2 (&pa)[4], const float2 (&pb)[4], float2& ca, float2& cb,
                                               float2& ha, float2& hb) {
-  float2 fa, ia, oa, ga, fb, ib, ob, gb;
-  activate_nr(pa[0], pa[1], pa[2], pa[3], fa, ia, oa, ga);
-  activate_nr(pb[0], pb[1], pb[2], pb[3], fb, ib, ob, gb);
-  ca = fma2(fa, ca, mul2(ia, ga));
-  cb = fma2(fb, cb, mul2(ib, gb));
+  float2 oa, ob;
+  fwd_cell_nr(pa[0], pa[1], pa[2], pa[3], ca, oa);
+  fwd_cell_nr(pb[0], pb[1], pb[2], pb[3], cb, ob);
   float2 ta, tb;
   tanh2x2_nr(ca, cb, ta, tb);
   ha = mul2(oa, ta);
