@@ -309,7 +309,7 @@ __device__ __forceinline__ void stage_state(RS& sm, const float* state, int64_t 
                "r"(bytes * uint32_t(2 * kD))
                : "memory");
   const float* src = state + int64_t(blockIdx.x) * kTile;
-#pragma unroll 1
+#pragma unroll
   for (int j = 0; j < 2 * kD; ++j)
     asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
                      su32(sm.st[j])),
