@@ -317,6 +317,29 @@ __device__ __forceinline__ void stage_state(RS& sm, const float* state, int64_t 
                  : "memory");
 }
 
+// Lane 0 of every warp: 4 of the 16 row segments (warp w: rows 4w .. 4w+3),
+// thread 0 also the barrier's expected bytes -- the copies of a step are
+// issued by four threads at once instead of one (a complete_tx that lands
+// before the expect_tx only drives the transaction count negative; the
+// phase cannot complete before thread 0's arrival).
+template <class RS>
+__device__ __forceinline__ void stage_state_split(RS& sm, const float* state, int64_t B, uint32_t bytes) {
+  if (threadIdx.x == 0)
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(&sm.mbar_st)),
+                 "r"(bytes * uint32_t(2 * kD))
+                 : "memory");
+  const int w = threadIdx.x >> 5;
+  const float* src = state + int64_t(blockIdx.x) * kTile;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int j = 4 * w + q;
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     su32(sm.st[j])),
+                 "l"(src + int64_t(j) * B), "r"(bytes), "r"(su32(&sm.mbar_st))
+                 : "memory");
+  }
+}
+
 // Fused run of Reverse actions, steps from+count-1 .. from.  Gates on the
 // tensor cores; the transpose matvec dh = sum_g (s_g W_g)^T (da_g / s_g) on
 // the packed-fp32 pipe with uniform-register weights.  PF (B % 4 == 0, 16-byte
@@ -392,7 +415,7 @@ __global__ void __launch_bounds__(kThreads, ACKPT_REV_MINB)
     stage_operands(sm, h, xb);
     if (i > 0) xb = load_bias(xbs_all, from + i - 1);
     gates_issue(sm);  // after its barrier every thread has read rs.st
-    if (PF && i > 0 && threadIdx.x == 0) stage_state(rs, states.p[i - 1], B, seg);
+    if (PF && i > 0 && (threadIdx.x & 31) == 0) stage_state_split(rs, states.p[i - 1], B, seg);
     gates_wait(sm, uint32_t(phase & 1));
     float2 acc[kD];
 #pragma unroll
