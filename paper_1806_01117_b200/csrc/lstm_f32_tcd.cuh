@@ -44,12 +44,12 @@ __device__ __forceinline__ uint64_t desc(uint32_t addr, uint32_t sbo) {
   return uint64_t((addr >> 4) & 0x3FFF) | (uint64_t(128 >> 4) << 16) | (uint64_t((sbo >> 4) & 0x3FFF) << 32) |
          (uint64_t(1) << 46);
 }
-// tf32 head of x rounded to nearest (|x - hi| <= 2^-11 |x|; the tensor core
-// truncates the residual to tf32, so each split product carries ~2^-22).
+// tf32 head of x rounded to nearest, ties away from zero (|x - hi| <= 2^-11
+// |x|; the tensor core truncates the residual to tf32, so each split product
+// carries ~2^-22).  The same bits as cvt.rna.tf32.f32 for finite x, in two
+// integer instructions (cvt.rna.tf32 compiles to four: it also handles NaN).
 __device__ __forceinline__ float hi_part(float x) {
-  uint32_t r;
-  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
-  return __uint_as_float(r);
+  return __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xFFFFE000u);
 }
 
 // float index of (row, k) in a tf32 operand with K-extent K; bf16 index likewise
