@@ -165,14 +165,14 @@ __device__ __forceinline__ void stage_operands(Smem& sm, const float2 (&h)[kD], 
 }
 
 __device__ __forceinline__ void mbar_wait(const uint64_t* bar, uint32_t phase) {
-  uint32_t done = 0;
-  do {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
-        : "=r"(done)
-        : "r"(su32(bar)), "r"(phase)
-        : "memory");
-  } while (!done);
+  // the retry loop in one asm block: no register re-materialisation per spin
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(su32(bar)),
+      "r"(phase)
+      : "memory");
 }
 
 // Barrier, then thread 0 issues the 8 MMAs of a step and commits them to

@@ -86,14 +86,13 @@ __device__ __forceinline__ void commit(uint64_t* bar) {
                : "memory");
 }
 __device__ __forceinline__ void wait_bar(uint64_t* bar, uint32_t phase) {
-  uint32_t done = 0;
-  do {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
-        : "=r"(done)
-        : "r"(su32(bar)), "r"(phase)
-        : "memory");
-  } while (!done);
+  asm volatile(  // the retry loop in one asm block: no register re-materialisation per spin
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(su32(bar)),
+      "r"(phase)
+      : "memory");
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 }
 // Barrier that publishes this step's shared-memory / TMEM writes to the
