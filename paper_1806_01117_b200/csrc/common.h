@@ -19,6 +19,12 @@ struct Error : std::runtime_error {
 
 void set_last_error(const std::string& msg);
 
+// Set by the executor around a fused launch that directly follows another
+// fused launch of the same operator on the same stream, with nothing else
+// enqueued in between (engine.cpp); the operator may then chain the two
+// launches (lstm_f32_tc.cu).  0 everywhere else.
+extern thread_local int g_chain_hint;
+
 [[noreturn]] inline void fail(int code, const std::string& msg) { throw Error(code, msg); }
 
 // Runs fn and converts any exception into a status code + last-error string.

@@ -225,7 +225,10 @@ struct Run {
       // reading it (a store whose wait is missing) or a kernel reading a
       // fetch destination before its H2D copy landed then sees NaN, which the
       // bit-identity / oracle checks of the test suite turn into failures.
-      if (!dry && poison()) ACKPT_CUDA_CHECK(cudaMemsetAsync(E->bufs[size_t(id)], 0xFF, size_t(E->S), s));
+      if (!dry && poison()) {
+        ACKPT_CUDA_CHECK(cudaMemsetAsync(E->bufs[size_t(id)], 0xFF, size_t(E->S), s));
+        chainable = false;
+      }
     }
   }
   static bool poison() {
@@ -253,6 +256,7 @@ struct Run {
 
   // -- operator calls (runtime.py:174-190) ------------------------------------
   void do_seed(int state) {
+    chainable = false;
     // Seed the adjoint register so that after all n backward steps the result
     // lands in adj[0] (the caller's output buffer).
     a = (E->n % 2 == 0) ? 0 : 1;
@@ -308,7 +312,7 @@ struct Run {
     if (to - from >= 1 && E->fuse && E->op.advance) {
       int out = acquire();
       span(ACKPT_EV_FORWARD, from, to, [&] {
-        check_op(E->op.advance(E->op.ctx, from, to, ptr(cur), wptr(out), s));
+        fused_launch([&] { check_op(E->op.advance(E->op.ctx, from, to, ptr(cur), wptr(out), s)); });
         ++st.kernel_launches;
       });
       release(cur);
@@ -344,6 +348,7 @@ struct Run {
     std::string msg;
     int rc = tier_ticket_status(E->tier, t, &msg);
     if (rc != ACKPT_OK) fail(rc, msg);
+    chainable = false;
     cudaEvent_t done = tier_ticket_event(E->tier, t);
     cudaEvent_t before = timing_event(), after = timing_event();
     // under graph capture these are event-record nodes (re-recorded on replay)
@@ -357,8 +362,21 @@ struct Run {
 
   std::vector<ackpt_ticket> issued;  // checked for file-stage errors after the run
   bool capturing = false;            // enqueued under CUDA-graph stream capture
+  // The last operation enqueued on the compute stream was a fused launch of
+  // the operator (TapeForward chunk / Reverse run): the next fused launch may
+  // be chained to it (g_chain_hint, lstm_f32_tc.cu).  Cleared by every other
+  // enqueue (waits, transfers, seeds, other actions).
+  bool chainable = false;
+  template <class F>
+  void fused_launch(F&& launch) {
+    g_chain_hint = (chainable && !E->timeline && E->sample_every == 0) ? 1 : 0;
+    launch();
+    g_chain_hint = 0;
+    chainable = true;
+  }
 
   ackpt_ticket begin_store(int64_t key, int state) {
+    chainable = false;
     ackpt_ticket t = -1;
     if (!dry) {
       check_op(ackpt_tier_begin_store(E->tier, key, key, ptr(state), E->S, s, &t));
@@ -371,6 +389,7 @@ struct Run {
   }
 
   ackpt_ticket begin_fetch(int64_t key, int dst) {
+    chainable = false;
     ackpt_ticket t = -1;
     if (!dry) {
       int rc = ackpt_tier_begin_fetch(E->tier, key, wptr(dst), E->S, s, &t);
@@ -426,7 +445,7 @@ struct Run {
               ledger.add_tape(E->S);
             }
             span(ACKPT_EV_FORWARD, offset + rel, offset + rel + cnt, [&] {
-              check_op(E->op.forward_many(E->op.ctx, offset + rel, cnt, ptr(state), outs, s));
+              fused_launch([&] { check_op(E->op.forward_many(E->op.ctx, offset + rel, cnt, ptr(state), outs, s)); });
               ++st.kernel_launches;
             });
             release(state);
@@ -496,7 +515,7 @@ struct Run {
           ledger.drop_tape(E->S);
         }
         span(ACKPT_EV_BACKWARD, offset + lo, offset + lo + int64_t(run), [&] {
-          check_op(E->op.backward_many(E->op.ctx, offset + lo, int64_t(run), states, adj[a], adj[1 - a], s));
+          fused_launch([&] { check_op(E->op.backward_many(E->op.ctx, offset + lo, int64_t(run), states, adj[a], adj[1 - a], s)); });
           ++st.kernel_launches;
         });
         a = 1 - a;

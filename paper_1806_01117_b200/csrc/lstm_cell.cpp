@@ -177,6 +177,7 @@ ACKPT_API int ackpt_lstm_destroy(ackpt_lstm* cell) {
     if (cell->d_ws) cudaFree(cell->d_ws);
     if (cell->d_scratch) cudaFree(cell->d_scratch);
     if (cell->d_wimg) cudaFree(cell->d_wimg);
+    if (cell->d_chain) cudaFree(cell->d_chain);
     delete cell;
   });
 }
@@ -188,6 +189,7 @@ ACKPT_API int64_t ackpt_lstm_state_bytes(const ackpt_lstm* cell) {
 ACKPT_API int ackpt_lstm_forward(const ackpt_lstm* cell, int64_t step, const void* state_in,
                                  void* state_out, void* stream) {
   return ackpt::guard([&] {
+    ackpt::chain_touch(cell);
     ackpt::check_step(cell, step);
     auto s = static_cast<cudaStream_t>(stream);
     if (ackpt::sb_first(cell)) {
@@ -218,6 +220,7 @@ ACKPT_API int ackpt_lstm_forward(const ackpt_lstm* cell, int64_t step, const voi
 ACKPT_API int ackpt_lstm_advance(const ackpt_lstm* cell, int64_t from_step, int64_t to_step,
                                  const void* state_in, void* state_out, void* stream) {
   return ackpt::guard([&] {
+    ackpt::chain_touch(cell);
     if (from_step < 0 || to_step > cell->n || from_step >= to_step)
       ackpt::fail(ACKPT_VALUE_ERROR, "advance range out of bounds");
     auto s = static_cast<cudaStream_t>(stream);
@@ -253,6 +256,7 @@ ACKPT_API int ackpt_lstm_advance(const ackpt_lstm* cell, int64_t from_step, int6
 ACKPT_API int ackpt_lstm_backward(const ackpt_lstm* cell, int64_t step, const void* state,
                                   const void* adjoint_in, void* adjoint_out, void* stream) {
   return ackpt::guard([&] {
+    ackpt::chain_touch(cell);
     ackpt::check_step(cell, step);
     auto s = static_cast<cudaStream_t>(stream);
     if (ackpt::sb_first(cell)) {
@@ -287,6 +291,7 @@ ACKPT_API int ackpt_lstm_backward(const ackpt_lstm* cell, int64_t step, const vo
 ACKPT_API int ackpt_lstm_forward_many(const ackpt_lstm* cell, int64_t from_step, int64_t count,
                                       const void* state_in, void* const* states_out, void* stream) {
   return ackpt::guard([&] {
+    ackpt::chain_touch(cell);
     if (count < 1 || count > ACKPT_MAX_FUSED) ackpt::fail(ACKPT_VALUE_ERROR, "count must be in [1, 64]");
     if (from_step < 0 || from_step + count > cell->n) ackpt::fail(ACKPT_VALUE_ERROR, "steps out of range");
     auto s = static_cast<cudaStream_t>(stream);
@@ -330,6 +335,7 @@ ACKPT_API int ackpt_lstm_backward_many(const ackpt_lstm* cell, int64_t from_step
                                        const void* const* states, const void* adjoint_in,
                                        void* adjoint_out, void* stream) {
   return ackpt::guard([&] {
+    ackpt::chain_touch(cell);
     if (count < 1 || count > ACKPT_MAX_FUSED) ackpt::fail(ACKPT_VALUE_ERROR, "count must be in [1, 64]");
     if (from_step < 0 || from_step + count > cell->n) ackpt::fail(ACKPT_VALUE_ERROR, "steps out of range");
     auto s = static_cast<cudaStream_t>(stream);
@@ -365,6 +371,7 @@ ACKPT_API int ackpt_lstm_backward_many(const ackpt_lstm* cell, int64_t from_step
 ACKPT_API int ackpt_lstm_seed(const ackpt_lstm* cell, const void* final_state, void* adjoint_out,
                               void* stream) {
   return ackpt::guard([&] {
+    ackpt::chain_touch(cell);
     auto s = static_cast<cudaStream_t>(stream);
     if (cell->dtype == ACKPT_F32)
       ackpt::launch_seed<float>(cell, static_cast<const float*>(final_state),
@@ -379,6 +386,7 @@ ACKPT_API int ackpt_lstm_seed(const ackpt_lstm* cell, const void* final_state, v
 ACKPT_API int ackpt_lstm_loss(const ackpt_lstm* cell, const void* final_state, void* loss_out,
                               void* stream) {
   return ackpt::guard([&] {
+    ackpt::chain_touch(cell);
     auto s = static_cast<cudaStream_t>(stream);
     if (cell->dtype == ACKPT_F32)
       ackpt::launch_loss<float>(cell, static_cast<const float*>(final_state),

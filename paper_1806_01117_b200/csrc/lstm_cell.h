@@ -24,6 +24,13 @@ struct ackpt_lstm {
   void* d_ws = nullptr;       // fp32 d in {16, 32, 64}: 4 x d x d pre-scaled W (lstm_f32_tcd.cu)
   void* d_scratch = nullptr;  // fp32 d = 64 reverse: chunk image of the scaled W^T (tcd_build_images)
   void* d_wimg = nullptr;     // fp32 d in {16, 32, 64}: shared-memory image of W / W^T hi|lo (tcd_build_images)
+  // launch chain of the fused d = 8 tcgen05 kernels (lstm_f32_tc.cu)
+  uint32_t* d_chain = nullptr;  // per-tile completion epochs
+  int64_t chain_tiles = 0;
+  uint32_t chain_epoch = 0;     // the last epoch handed out
+  bool chain_open = false;      // the cell's last launch was a fused tc launch ...
+  bool chain_prev = false;      // ... as seen at the entry of the current API call
+  void* chain_stream = nullptr; // ... on this stream
   size_t scratch_bytes = 0;
 };
 
@@ -61,6 +68,13 @@ void f32_forward_many(const ackpt_lstm* c, int64_t from, int count, const float*
 template <int D>
 void f32_backward_many(const ackpt_lstm* c, int64_t from, int count, const float* const* states,
                        const float* adj_in, float* adj_out, cudaStream_t s);
+// Launch chain bookkeeping: every API entry point calls chain_touch first
+// (a non-tc launch of the cell then leaves the chain closed).
+inline void chain_touch(const ackpt_lstm* c) {
+  auto* m = const_cast<ackpt_lstm*>(c);
+  m->chain_prev = m->chain_open;
+  m->chain_open = false;
+}
 // Tensor-core (tcgen05, 3xTF32) fused kernels, d = 8 (lstm_f32_tc.cu).
 void tc_advance(const ackpt_lstm* c, int64_t from, int count, const float* in, float* out, cudaStream_t s);
 void tc_forward_many(const ackpt_lstm* c, int64_t from, int count, const float* in, float* const* outs,

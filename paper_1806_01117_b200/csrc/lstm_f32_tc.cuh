@@ -247,21 +247,71 @@ struct StatePtrs {
   const float* p[ACKPT_MAX_FUSED];
 };
 
+// Per-tile launch chain (lstm_f32_tc.cu): consecutive fused launches of one
+// cell on one stream, the later one launched as a programmatic dependent
+// launch.  CTA b of a chained launch waits until flags[b] >= wait -- tile b of
+// the previous launch (the only producer of tile b's inputs: every access is
+// per tile) has finished and published its stores -- and publishes flags[b] =
+// set at its end.  So the launch fills the previous one's tail with the tiles
+// that are already done, instead of waiting for its last CTA.  Dependents are
+// allowed only after the CTA holds its TMEM, so a waiting CTA never keeps an
+// earlier one from allocating; with wait = 0 it is a plain launch.
+struct Chain {
+  uint32_t* flags;
+  uint32_t wait, set;
+};
+
+__device__ __forceinline__ void chain_begin(const Chain& ch) {
+  if (!ch.flags) return;
+  __syncthreads();  // TMEM allocated (setup): dependents may be scheduled now
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  if (ch.wait) {
+    if (threadIdx.x == 0) {
+      uint32_t v;
+      for (;;) {
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(ch.flags + blockIdx.x) : "memory");
+        if (int32_t(v - ch.wait) >= 0) break;
+        __nanosleep(128);
+      }
+    }
+    __syncthreads();
+    // the producer's generic-proxy stores, now acquired, before this CTA's
+    // bulk-copy (async-proxy) reads of the same data
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+  }
+}
+__device__ __forceinline__ void chain_end(const Chain& ch) {
+  if (!ch.flags) return;
+  __threadfence();  // this thread's stores, device-wide, before the flag
+  __syncthreads();
+  if (threadIdx.x == 0)
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(ch.flags + blockIdx.x), "r"(ch.set) : "memory");
+}
+// Coherent (L2) load for inputs a chained predecessor may have written while
+// this kernel was already resident.
+__device__ __forceinline__ float2 ldcg2(const float* p) {
+  float2 v;
+  asm volatile("ld.global.cg.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "l"(p));
+  return v;
+}
+
 // Fused forward over `count` steps from `from`; TAPE stores every step's
 // output to outs.p[i], otherwise only the final state goes to `out`.
 template <bool TAPE>
 __global__ void __launch_bounds__(kThreads, 8)
     fwd_tc(const float* __restrict__ in, float* __restrict__ out, int64_t B, const float* __restrict__ xbs_all,
-           int64_t from, int count, const __grid_constant__ Weights w, const __grid_constant__ OutPtrs outs) {
+           int64_t from, int count, const __grid_constant__ Weights w, const __grid_constant__ OutPtrs outs,
+           Chain chain) {
   __shared__ __align__(128) Smem sm;
   const int64_t b0 = int64_t(blockIdx.x) * kTile + 2 * threadIdx.x;
   const bool live = b0 < B;  // every thread takes part in the MMA protocol
   setup(sm, w);
+  chain_begin(chain);
   float2 h[kD], c[kD];
 #pragma unroll
   for (int j = 0; j < kD; ++j) {
-    h[j] = live ? ldg2(in + b0 + int64_t(j) * B) : make_float2(0.f, 0.f);
-    c[j] = live ? ldg2(in + b0 + int64_t(kD + j) * B) : make_float2(0.f, 0.f);
+    h[j] = live ? ldcg2(in + b0 + int64_t(j) * B) : make_float2(0.f, 0.f);
+    c[j] = live ? ldcg2(in + b0 + int64_t(kD + j) * B) : make_float2(0.f, 0.f);
   }
   float xb = load_bias(xbs_all, from);
   for (int i = 0; i < count; ++i) {
@@ -290,6 +340,7 @@ __global__ void __launch_bounds__(kThreads, 8)
       stg2(out + b0 + int64_t(kD + j) * B, c[j]);
     }
   }
+  chain_end(chain);
   teardown(sm);
 }
 
@@ -371,7 +422,8 @@ __device__ __forceinline__ void tmatvec_unit(const Weights& w, int j, const floa
 template <bool PF>
 __global__ void __launch_bounds__(kThreads, ACKPT_REV_MINB)
     rev_tc(const float* __restrict__ adj_in, float* __restrict__ adj_out, int64_t B, const float* __restrict__ xbs_all,
-           int64_t from, int count, const __grid_constant__ Weights w, const __grid_constant__ StatePtrs states) {
+           int64_t from, int count, const __grid_constant__ Weights w, const __grid_constant__ StatePtrs states,
+           Chain chain) {
   __shared__ __align__(128) RevSmem rs;
   Smem& sm = rs.g;
   const int64_t b0 = int64_t(blockIdx.x) * kTile + 2 * threadIdx.x;
@@ -379,6 +431,7 @@ __global__ void __launch_bounds__(kThreads, ACKPT_REV_MINB)
   const int64_t rem = B - int64_t(blockIdx.x) * kTile;
   const uint32_t seg = uint32_t(rem < kTile ? rem : kTile) * 4u;
   setup(sm, w);
+  chain_begin(chain);
   if (PF) {
     if (threadIdx.x == 0) {
       asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(&rs.mbar_st)));
@@ -390,8 +443,8 @@ __global__ void __launch_bounds__(kThreads, ACKPT_REV_MINB)
   float2 dh[kD], dc[kD];
 #pragma unroll
   for (int j = 0; j < kD; ++j) {
-    dh[j] = live ? ldg2(adj_in + b0 + int64_t(j) * B) : make_float2(0.f, 0.f);
-    dc[j] = live ? ldg2(adj_in + b0 + int64_t(kD + j) * B) : make_float2(0.f, 0.f);
+    dh[j] = live ? ldcg2(adj_in + b0 + int64_t(j) * B) : make_float2(0.f, 0.f);
+    dc[j] = live ? ldcg2(adj_in + b0 + int64_t(kD + j) * B) : make_float2(0.f, 0.f);
   }
   int phase = 0;
   float xb = load_bias(xbs_all, from + count - 1);
@@ -408,8 +461,8 @@ __global__ void __launch_bounds__(kThreads, ACKPT_REV_MINB)
       const float* xs = states.p[i] + b0;
 #pragma unroll
       for (int j = 0; j < kD; ++j) {
-        h[j] = live ? ldg2(xs + int64_t(j) * B) : make_float2(0.f, 0.f);
-        c[j] = live ? ldg2(xs + int64_t(kD + j) * B) : make_float2(0.f, 0.f);
+        h[j] = live ? ldcg2(xs + int64_t(j) * B) : make_float2(0.f, 0.f);
+        c[j] = live ? ldcg2(xs + int64_t(kD + j) * B) : make_float2(0.f, 0.f);
       }
     }
     stage_operands(sm, h, xb);
@@ -442,6 +495,7 @@ __global__ void __launch_bounds__(kThreads, ACKPT_REV_MINB)
       stg2(adj_out + b0 + int64_t(kD + j) * B, dc[j]);
     }
   }
+  chain_end(chain);
   teardown(sm);
 }
 

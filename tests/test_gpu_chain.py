@@ -1,0 +1,31 @@
+"""Chained fused launches (programmatic dependent launch + per-tile
+completion flags, csrc/lstm_f32_tc.cu) produce bit-identical results to
+plain launches: tools/chain_probe.py with ACKPT_TC_CHAIN=0 (never chain),
+default (the executor's fused launches chain) and force (every back-to-back
+launch of the cell chains)."""
+import os
+import subprocess
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _run(mode):
+    env = dict(os.environ)
+    env.pop("ACKPT_TC_CHAIN", None)
+    if mode is not None:
+        env["ACKPT_TC_CHAIN"] = mode
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "chain_probe.py")], env=env,
+                         capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stderr[-3000:]
+    line = [x for x in out.stdout.splitlines() if x.startswith("chain_probe ok")][-1]
+    return line.split("digest")[-1].strip()
+
+
+@pytest.mark.gpu
+def test_chained_launches_bit_identical():
+    plain = _run("0")
+    assert _run(None) == plain
+    assert _run("force") == plain
