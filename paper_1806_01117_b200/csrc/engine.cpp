@@ -295,7 +295,7 @@ struct Run {
     int out = acquire();
     span(ACKPT_EV_FORWARD, step, step + 1, [&] {
       timed(fwd_calls, fwd_pairs, [&] {
-        check_op(E->op.forward(E->op.ctx, step, ptr(cur), wptr(out), s));
+        fused_launch([&] { check_op(E->op.forward(E->op.ctx, step, ptr(cur), wptr(out), s)); });
         ++st.kernel_launches;
       });
     });
@@ -330,7 +330,7 @@ struct Run {
       fail(ACKPT_EXECUTION_ERROR, "Reverse " + std::to_string(step) + " before the adjoint was seeded");
     span(ACKPT_EV_BACKWARD, step, step + 1, [&] {
       timed(bwd_calls, bwd_pairs, [&] {
-        check_op(E->op.backward(E->op.ctx, step, ptr(state), adj[a], adj[1 - a], s));
+        fused_launch([&] { check_op(E->op.backward(E->op.ctx, step, ptr(state), adj[a], adj[1 - a], s)); });
         ++st.kernel_launches;
       });
     });
@@ -362,10 +362,10 @@ struct Run {
 
   std::vector<ackpt_ticket> issued;  // checked for file-stage errors after the run
   bool capturing = false;            // enqueued under CUDA-graph stream capture
-  // The last operation enqueued on the compute stream was a fused launch of
-  // the operator (TapeForward chunk / Reverse run): the next fused launch may
-  // be chained to it (g_chain_hint, lstm_f32_tc.cu).  Cleared by every other
-  // enqueue (waits, transfers, seeds, other actions).
+  // The last operation enqueued on the compute stream was a step launch of
+  // the operator (per-step, fused Advance / TapeForward / Reverse run): the
+  // next one may be chained to it (g_chain_hint, chain.cuh).  Cleared by
+  // every other enqueue (waits, transfers, seeds, poison fills).
   bool chainable = false;
   template <class F>
   void fused_launch(F&& launch) {

@@ -24,6 +24,7 @@
 
 #include <cuda_runtime.h>
 
+#include "chain.cuh"
 #include "lstm_f32_math.cuh"
 
 namespace ackpt {
@@ -247,53 +248,17 @@ struct StatePtrs {
   const float* p[ACKPT_MAX_FUSED];
 };
 
-// Per-tile launch chain (lstm_f32_tc.cu): consecutive fused launches of one
-// cell on one stream, the later one launched as a programmatic dependent
-// launch.  CTA b of a chained launch waits until flags[b] >= wait -- tile b of
-// the previous launch (the only producer of tile b's inputs: every access is
-// per tile) has finished and published its stores -- and publishes flags[b] =
-// set at its end.  So the launch fills the previous one's tail with the tiles
-// that are already done, instead of waiting for its last CTA.  Dependents are
-// allowed only after the CTA holds its TMEM, so a waiting CTA never keeps an
-// earlier one from allocating; with wait = 0 it is a plain launch.
-struct Chain {
-  uint32_t* flags;
-  uint32_t wait, set;
-};
-
+// Launch chain (chain.cuh): one tile per CTA, so CTA b waits for and
+// publishes tile b.
+using Chain = chain::Chain;
+using chain::ldcg2;
 __device__ __forceinline__ void chain_begin(const Chain& ch) {
   if (!ch.flags) return;
   __syncthreads();  // TMEM allocated (setup): dependents may be scheduled now
-  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-  if (ch.wait) {
-    if (threadIdx.x == 0) {
-      uint32_t v;
-      for (;;) {
-        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(ch.flags + blockIdx.x) : "memory");
-        if (int32_t(v - ch.wait) >= 0) break;
-        __nanosleep(128);
-      }
-    }
-    __syncthreads();
-    // the producer's generic-proxy stores, now acquired, before this CTA's
-    // bulk-copy (async-proxy) reads of the same data
-    asm volatile("fence.proxy.async.global;" ::: "memory");
-  }
+  chain::allow_dependents(ch);
+  chain::wait_tile(ch, blockIdx.x, 0);
 }
-__device__ __forceinline__ void chain_end(const Chain& ch) {
-  if (!ch.flags) return;
-  __threadfence();  // this thread's stores, device-wide, before the flag
-  __syncthreads();
-  if (threadIdx.x == 0)
-    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(ch.flags + blockIdx.x), "r"(ch.set) : "memory");
-}
-// Coherent (L2) load for inputs a chained predecessor may have written while
-// this kernel was already resident.
-__device__ __forceinline__ float2 ldcg2(const float* p) {
-  float2 v;
-  asm volatile("ld.global.cg.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "l"(p));
-  return v;
-}
+__device__ __forceinline__ void chain_end(const Chain& ch) { chain::set_tile(ch, blockIdx.x, 0); }
 
 // Fused forward over `count` steps from `from`; TAPE stores every step's
 // output to outs.p[i], otherwise only the final state goes to `out`.

@@ -70,15 +70,17 @@ void fwd_launch(const ackpt_lstm* c, int64_t from, int count, const float* in, f
   const auto xb = static_cast<const float*>(c->d_xbs);
   const auto ws = tcd_wimg<D>(c, s);
   const int cols = tcd::tmem_cols(4 * D);
+  bool pdl = false;
+  const chain::Chain ch = chain::next(c, s, tcd_tiles(c->B), pdl);
   if (outs) {
     for (int i = 0; i < count; ++i) o.p[i] = outs[i];
     auto k = tcd::fwd_tcd<D, true>;
-    k<<<tcd_grid(c->B, count, k, L::fwd_bytes, true, cols), tcd::kThreads, L::fwd_bytes, s>>>(in, nullptr, c->B, xb,
-                                                                                                ws, from, count, o);
+    chain::launch(k, tcd_grid(c->B, count, k, L::fwd_bytes, true, cols), tcd::kThreads, L::fwd_bytes, pdl, s, in,
+                  static_cast<float*>(nullptr), c->B, xb, ws, from, count, o, ch);
   } else {
     auto k = tcd::fwd_tcd<D, false>;
-    k<<<tcd_grid(c->B, count, k, L::fwd_bytes, true, cols), tcd::kThreads, L::fwd_bytes, s>>>(in, out, c->B, xb, ws,
-                                                                                                from, count, o);
+    chain::launch(k, tcd_grid(c->B, count, k, L::fwd_bytes, true, cols), tcd::kThreads, L::fwd_bytes, pdl, s, in,
+                  out, c->B, xb, ws, from, count, o, ch);
   }
 }
 
@@ -94,8 +96,10 @@ void rev_launch(const ackpt_lstm* c, int64_t from, int count, const float* const
   tcd::StatePtrs sp{};
   for (int i = 0; i < count; ++i) sp.p[i] = states[i];
   auto k = tcd::rev_tcd<D>;
-  k<<<tcd_grid(c->B, count, k, L::rev_bytes, true, tcd::tmem_cols(7 * D)), tcd::kThreads, L::rev_bytes, s>>>(
-      ai, ao, c->B, static_cast<const float*>(c->d_xbs), tcd_wimg<D>(c, s), from, count, sp);
+  bool pdl = false;
+  const chain::Chain ch = chain::next(c, s, tcd_tiles(c->B), pdl);
+  chain::launch(k, tcd_grid(c->B, count, k, L::rev_bytes, true, tcd::tmem_cols(7 * D)), tcd::kThreads, L::rev_bytes,
+                pdl, s, ai, ao, c->B, static_cast<const float*>(c->d_xbs), tcd_wimg<D>(c, s), from, count, sp, ch);
 }
 
 // d = 64 reverse: one kernel per launch (rev_tcd64: Wᵀ streamed through a
@@ -119,9 +123,11 @@ void rev64_launch(const ackpt_lstm* c, int64_t from, int count, const float* con
   for (int i = 0; i < count; ++i) sp.p[i] = states[i];
   const unsigned tiles = tcd_tiles(c->B);
   const unsigned grid = count > 1 ? tiles : std::min<unsigned>(tiles, unsigned(sms));  // one CTA per SM
-  tcd::rev_tcd64<<<grid, tcd::kThreads64, tcd::kRev64Smem, s>>>(
-      ai, ao, c->B, static_cast<const float*>(c->d_xbs), tcd_wimg<64>(c, s),
-      static_cast<const float*>(c->d_scratch), from, count, sp);
+  bool pdl = false;
+  const chain::Chain ch = chain::next(c, s, tiles, pdl);
+  chain::launch(tcd::rev_tcd64, grid, tcd::kThreads64, tcd::kRev64Smem, pdl, s, ai, ao, c->B,
+                static_cast<const float*>(c->d_xbs), tcd_wimg<64>(c, s), static_cast<const float*>(c->d_scratch), from,
+                count, sp, ch);
 }
 
 }  // namespace

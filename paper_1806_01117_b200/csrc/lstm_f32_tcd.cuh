@@ -23,6 +23,7 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
+#include "chain.cuh"
 #include "lstm_f32_math.cuh"
 
 namespace ackpt {
@@ -281,19 +282,16 @@ __device__ __forceinline__ void issue_gates(float* sm, uint32_t tmem, uint64_t* 
   commit(bar);
 }
 
-__device__ __forceinline__ float ldg_nc(const float* p) {
-  float v;
-  asm volatile("ld.global.nc.L1::no_allocate.f32 %0, [%1];" : "=f"(v) : "l"(p));
-  return v;
-}
-
 // Unit pairs of this thread's sequence, block `base` (0: h, D: c) of a state.
+// Through L2 (ld.global.cg): a chained predecessor may have written the rows
+// while this kernel was resident (chain.cuh).
 template <int D>
 __device__ __forceinline__ void load_rows(const float* __restrict__ x, int64_t B, int64_t b, int base,
                                           float2 (&v)[D / 2]) {
 #pragma unroll
   for (int p = 0; p < D / 2; ++p)
-    v[p] = make_float2(ldg_nc(x + int64_t(base + 2 * p) * B + b), ldg_nc(x + int64_t(base + 2 * p + 1) * B + b));
+    v[p] = make_float2(chain::ldcg(x + int64_t(base + 2 * p) * B + b),
+                       chain::ldcg(x + int64_t(base + 2 * p + 1) * B + b));
 }
 template <int D>
 __device__ __forceinline__ void store_rows(float* __restrict__ x, int64_t B, int64_t b, int base,
@@ -309,20 +307,23 @@ __device__ __forceinline__ void store_rows(float* __restrict__ x, int64_t B, int
 // TAPE stores every step's output state to outs.p[i]; otherwise the final
 // state goes to `out`.
 template <int D, bool TAPE>
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(kThreads, D == 16 ? 6 : D == 32 ? 4 : 1)  // register caps: d = 16 85, d = 32 128
     fwd_tcd(const float* __restrict__ in, float* __restrict__ out, int64_t B, const float* __restrict__ xbs_all,
-            const float* __restrict__ ws, int64_t from, int count, const __grid_constant__ OutPtrs outs) {
+            const float* __restrict__ ws, int64_t from, int count, const __grid_constant__ OutPtrs outs,
+            chain::Chain ch) {
   using L = Layout<D>;
   extern __shared__ __align__(128) float sm[];
   uint64_t* bars = reinterpret_cast<uint64_t*>(sm + L::fwd_end);
   uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 2);
   setup<D>(sm, bars, tslot, ws, tmem_cols(4 * D), 1, false);
   const uint32_t tmem = tmem_base(tslot);
+  chain::allow_dependents(ch);
   const uint32_t lane = uint32_t((threadIdx.x >> 5) * 32) << 16;
   uint32_t ph = 0;
   bool wready = false;
   // persistent over 128-sequence tiles (the weight setup is paid once per CTA)
   for (int64_t tile = blockIdx.x; tile * kThreads < B; tile += gridDim.x) {
+  chain::wait_tile(ch, tile, 0);
   const int64_t b = tile * kThreads + threadIdx.x;
   const bool live = b < B;
   float2 h[D / 2], c[D / 2];
@@ -365,6 +366,7 @@ __global__ void __launch_bounds__(kThreads)
     store_rows<D>(out, B, b, 0, h);
     store_rows<D>(out, B, b, D, c);
   }
+  chain::set_tile(ch, tile, 0);
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
@@ -380,7 +382,8 @@ __global__ void __launch_bounds__(kThreads)
 template <int D>
 __global__ void __launch_bounds__(kThreads)
     rev_tcd(const float* __restrict__ adj_in, float* __restrict__ adj_out, int64_t B, const float* __restrict__ xbs_all,
-            const float* __restrict__ ws, int64_t from, int count, const __grid_constant__ StatePtrs states) {
+            const float* __restrict__ ws, int64_t from, int count, const __grid_constant__ StatePtrs states,
+            chain::Chain ch) {
   using L = Layout<D>;
   extern __shared__ __align__(128) float sm[];
   uint64_t* bars = reinterpret_cast<uint64_t*>(sm + L::rev_end);
@@ -390,6 +393,7 @@ __global__ void __launch_bounds__(kThreads)
   constexpr int kHalf = D / 4;  // unit pairs per K half
   setup<D>(sm, bars, tslot, ws, kCols, 2, true);
   const uint32_t tmem = tmem_base(tslot);
+  chain::allow_dependents(ch);
   bool wready = false;
   const uint32_t lane = uint32_t((threadIdx.x >> 5) * 32) << 16;
   // Thread 0: dh (+)= da . B2^T over unit pairs [p0, p0 + kHalf) (residual at kLo).
@@ -410,6 +414,7 @@ __global__ void __launch_bounds__(kThreads)
   uint32_t phase = 0, phase2 = 0;
   // persistent over 128-sequence tiles (the weight setup is paid once per CTA)
   for (int64_t tile = blockIdx.x; tile * kThreads < B; tile += gridDim.x) {
+  chain::wait_tile(ch, tile, 0);
   const int64_t b = tile * kThreads + threadIdx.x;
   const bool live = b < B;
   float2 dh[D / 2], dc[D / 2];
@@ -487,6 +492,7 @@ __global__ void __launch_bounds__(kThreads)
     store_rows<D>(adj_out, B, b, 0, dh);
     store_rows<D>(adj_out, B, b, D, dc);
   }
+  chain::set_tile(ch, tile, 0);
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
@@ -538,7 +544,7 @@ __device__ __forceinline__ void bar_compute_issue() { asm volatile("bar.sync 1, 
 __global__ void __launch_bounds__(kThreads64, 1)
     rev_tcd64(const float* __restrict__ adj_in, float* __restrict__ adj_out, int64_t B,
               const float* __restrict__ xbs_all, const float* __restrict__ wimg, const float* __restrict__ w2img,
-              int64_t from, int count, const __grid_constant__ StatePtrs states) {
+              int64_t from, int count, const __grid_constant__ StatePtrs states, chain::Chain ch) {
   constexpr int D = 64;
   using L = Layout<D>;
   extern __shared__ __align__(128) float sm[];
@@ -576,6 +582,7 @@ __global__ void __launch_bounds__(kThreads64, 1)
     for (int idx = tid; idx < 4 * D * 8; idx += kThreads) sm[L::b_hi + kofs<8>(idx / 8, idx % 8)] = 0.f;
   }
   const uint32_t tmem = tmem_base(tslot);  // (all 192 threads: a full barrier)
+  chain::allow_dependents(ch);
 
   if (warp == 5) {  // ---- producer: the chunk sequence, step after step
     if (tid == 5 * 32) {
@@ -631,6 +638,7 @@ __global__ void __launch_bounds__(kThreads64, 1)
     uint32_t phase = 0, phase_t = 0;
     for (int t = 0; t < my_tiles; ++t) {
       const int64_t tile = blockIdx.x + int64_t(t) * gridDim.x;
+      chain::wait_tile(ch, tile, 0, 2, kThreads);  // the compute warps (named barrier 2)
       const int64_t b = tile * kThreads + tid;
       const bool live = b < B;
       float2 dh[D / 2], dc[D / 2];
@@ -660,8 +668,8 @@ __global__ void __launch_bounds__(kThreads64, 1)
         auto load_c = [&](int p0) {
 #pragma unroll
           for (int q = 0; q < 4; ++q)
-            cq[q] = live ? make_float2(ldg_nc(xs + int64_t(D + 2 * (p0 + q)) * B + b),
-                                       ldg_nc(xs + int64_t(D + 2 * (p0 + q) + 1) * B + b))
+            cq[q] = live ? make_float2(chain::ldcg(xs + int64_t(D + 2 * (p0 + q)) * B + b),
+                                       chain::ldcg(xs + int64_t(D + 2 * (p0 + q) + 1) * B + b))
                          : make_float2(0.f, 0.f);
         };
         load_c(0);
@@ -721,6 +729,7 @@ __global__ void __launch_bounds__(kThreads64, 1)
         store_rows<D>(adj_out, B, b, 0, dh);
         store_rows<D>(adj_out, B, b, D, dc);
       }
+      chain::set_tile(ch, tile, 0, 2, kThreads);
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");

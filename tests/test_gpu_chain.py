@@ -1,7 +1,8 @@
-"""Chained fused launches (programmatic dependent launch + per-tile
-completion flags, csrc/lstm_f32_tc.cu) produce bit-identical results to
+"""Chained tensor-core launches (programmatic dependent launch + per-tile
+completion flags, csrc/chain.cuh; d = 8 fused and d = 16 / 32 / 64 fused and
+per-step) produce bit-identical results to
 plain launches: tools/chain_probe.py with ACKPT_TC_CHAIN=0 (never chain),
-default (the executor's fused launches chain) and force (every back-to-back
+default (the launches the executor marks chain) and force (every back-to-back
 launch of the cell chains)."""
 import os
 import subprocess
