@@ -89,7 +89,8 @@ __device__ __forceinline__ float2 ldcg2(const float* p) {
 
 // ACKPT_TC_CHAIN=0 off, =force chains every back-to-back launch of a cell on
 // one stream (probes that enqueue nothing else in between); default: chain
-// when the executor marks the launch (g_chain_hint, engine.cpp).
+// when the executor marks the launch of its native operator (g_chain_hint /
+// g_chain_native, common.h).
 inline int mode() {
   static const int m = [] {
     const char* e = std::getenv("ACKPT_TC_CHAIN");
@@ -101,8 +102,10 @@ inline int mode() {
 }
 
 // The chain parameters of the next launch of cell c on stream s over `tiles`
-// tiles; pdl = launch it as a programmatic dependent launch.  Never chains
-// under stream capture (the graph keeps full dependencies).
+// tiles; pdl = launch it as a programmatic dependent launch.  Chained only
+// when marked (the executor's hint through the native operator, or =force), when the process's last cell launch
+// was a chain-publishing launch of this cell on this stream (chain_touch),
+// and never under stream capture (the graph keeps full dependencies).
 inline Chain next(const ackpt_lstm* c, cudaStream_t s, int64_t tiles, bool& pdl) {
   auto* cell = const_cast<ackpt_lstm*>(c);
   pdl = false;
@@ -110,23 +113,33 @@ inline Chain next(const ackpt_lstm* c, cudaStream_t s, int64_t tiles, bool& pdl)
   ACKPT_CUDA_CHECK(cudaStreamIsCapturing(s, &cs));
   const int m = mode();
   if (m == 0 || cs != cudaStreamCaptureStatusNone) return Chain{nullptr, 0u, 0u};  // the chain stays closed
-  if (!cell->d_chain || cell->chain_tiles < tiles) {
-    if (cell->d_chain) {
-      ACKPT_CUDA_CHECK(cudaStreamSynchronize(s));
-      cudaFree(cell->d_chain);
-      cell->d_chain = nullptr;
+  ackpt_lstm::ChainSlot* slot = nullptr;
+  for (auto& sl : cell->chain_slots)
+    if (sl.flags && sl.stream == static_cast<void*>(s)) slot = &sl;
+  bool fresh = false;
+  if (!slot || slot->tiles < tiles) {
+    if (!slot) {
+      for (auto& sl : cell->chain_slots)
+        if (!sl.flags && !slot) slot = &sl;
+      if (!slot) slot = &cell->chain_slots[cell->chain_victim++ % 4];
     }
-    ACKPT_CUDA_CHECK(cudaMalloc(&cell->d_chain, size_t(tiles) * sizeof(uint32_t)));
-    ACKPT_CUDA_CHECK(cudaMemset(cell->d_chain, 0, size_t(tiles) * sizeof(uint32_t)));
-    cell->chain_tiles = tiles;
-    cell->chain_epoch = 0;
-    cell->chain_prev = false;
+    if (slot->flags) {  // evicted or too small: no kernel may still use it
+      ACKPT_CUDA_CHECK(cudaDeviceSynchronize());
+      cudaFree(slot->flags);
+      slot->flags = nullptr;
+    }
+    ACKPT_CUDA_CHECK(cudaMalloc(&slot->flags, size_t(tiles) * sizeof(uint32_t)));
+    ACKPT_CUDA_CHECK(cudaMemset(slot->flags, 0, size_t(tiles) * sizeof(uint32_t)));
+    slot->stream = s;
+    slot->tiles = tiles;
+    slot->epoch = 0;
+    fresh = true;
   }
-  const bool chained = (m == 2 || g_chain_hint) && cell->chain_prev && cell->chain_stream == s;
-  Chain ch{cell->d_chain, chained ? cell->chain_epoch : 0u, cell->chain_epoch + 1};
-  if (++cell->chain_epoch == 0) cell->chain_epoch = 1;  // (flags compare by signed distance)
-  cell->chain_open = true;
-  cell->chain_stream = s;
+  const bool chained =
+      !fresh && (m == 2 || g_chain_native) && cell->chain_prev && cell->chain_prev_stream == static_cast<void*>(s);
+  Chain ch{slot->flags, chained ? slot->epoch : 0u, slot->epoch + 1};
+  if (++slot->epoch == 0) slot->epoch = 1;  // (flags compare by signed distance)
+  chain_publish(c, s);
   pdl = chained;
   return ch;
 }

@@ -19,11 +19,16 @@ struct Error : std::runtime_error {
 
 void set_last_error(const std::string& msg);
 
-// Set by the executor around a fused launch that directly follows another
-// fused launch of the same operator on the same stream, with nothing else
-// enqueued in between (engine.cpp); the operator may then chain the two
-// launches (lstm_f32_tc.cu).  0 everywhere else.
+// Set by the executor around a step launch that directly follows another
+// step launch of the same operator on the same stream, with nothing else
+// enqueued in between (engine.cpp).  The native LSTM operator's callbacks
+// pass it on as g_chain_native for the duration of the call, and only then
+// may the cell chain the two launches (chain.cuh) -- an operator written in
+// Python that calls the cell's public API never chains (its temporaries come
+// from an allocator that may hand a buffer a running launch still reads to
+// the next one).  0 everywhere else.
 extern thread_local int g_chain_hint;
+extern thread_local int g_chain_native;
 
 [[noreturn]] inline void fail(int code, const std::string& msg) { throw Error(code, msg); }
 

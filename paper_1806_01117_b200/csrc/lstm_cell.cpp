@@ -57,28 +57,55 @@ bool tc_on() { return family() == 1; }
 
 }  // namespace
 
+// The executor's chain mark applies to the cell calls made here (and only
+// here): see g_chain_native in common.h.
+struct NativeCall {
+  NativeCall() { g_chain_native = g_chain_hint; }
+  ~NativeCall() { g_chain_native = 0; }
+};
+
 int lstm_op_forward(void* ctx, int64_t step, const void* in, void* out, void* stream) {
+  NativeCall nc;
   return ackpt_lstm_forward(static_cast<ackpt_lstm*>(ctx), step, in, out, stream);
 }
 int lstm_op_backward(void* ctx, int64_t step, const void* st, const void* ai, void* ao,
                      void* stream) {
+  NativeCall nc;
   return ackpt_lstm_backward(static_cast<ackpt_lstm*>(ctx), step, st, ai, ao, stream);
 }
 int lstm_op_seed(void* ctx, const void* fin, void* adj, void* stream) {
   return ackpt_lstm_seed(static_cast<ackpt_lstm*>(ctx), fin, adj, stream);
 }
 int lstm_op_advance(void* ctx, int64_t from, int64_t to, const void* in, void* out, void* stream) {
+  NativeCall nc;
   return ackpt_lstm_advance(static_cast<ackpt_lstm*>(ctx), from, to, in, out, stream);
 }
 int lstm_op_forward_many(void* ctx, int64_t from, int64_t count, const void* in, void* const* outs,
                          void* stream) {
+  NativeCall nc;
   return ackpt_lstm_forward_many(static_cast<ackpt_lstm*>(ctx), from, count, in, outs, stream);
 }
 int lstm_op_backward_many(void* ctx, int64_t from, int64_t count, const void* const* states,
                           const void* ai, void* ao, void* stream) {
+  NativeCall nc;
   return ackpt_lstm_backward_many(static_cast<ackpt_lstm*>(ctx), from, count, states, ai, ao, stream);
 }
 
+}  // namespace ackpt
+
+namespace ackpt {
+void chain_release(ackpt_lstm* c) {
+  bool any = false;
+  for (auto& sl : c->chain_slots) any = any || sl.flags;
+  if (any) cudaDeviceSynchronize();  // no kernel may still publish into the flags
+  for (auto& sl : c->chain_slots) {
+    if (sl.flags) cudaFree(sl.flags);
+    sl = ackpt_lstm::ChainSlot{};
+  }
+  auto& t = chain_token();
+  std::lock_guard<std::mutex> lk(t.mu);
+  if (t.cell == c) t.cell = nullptr, t.stream = nullptr;
+}
 }  // namespace ackpt
 
 extern "C" {
@@ -177,7 +204,7 @@ ACKPT_API int ackpt_lstm_destroy(ackpt_lstm* cell) {
     if (cell->d_ws) cudaFree(cell->d_ws);
     if (cell->d_scratch) cudaFree(cell->d_scratch);
     if (cell->d_wimg) cudaFree(cell->d_wimg);
-    if (cell->d_chain) cudaFree(cell->d_chain);
+    ackpt::chain_release(cell);
     delete cell;
   });
 }

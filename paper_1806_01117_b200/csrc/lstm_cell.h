@@ -6,6 +6,7 @@
 
 #include <cstdint>
 #include <initializer_list>
+#include <mutex>
 #include <vector>
 
 #include "common.h"
@@ -24,14 +25,21 @@ struct ackpt_lstm {
   void* d_ws = nullptr;       // fp32 d in {16, 32, 64}: 4 x d x d pre-scaled W (lstm_f32_tcd.cu)
   void* d_scratch = nullptr;  // fp32 d = 64 reverse: chunk image of the scaled W^T (tcd_build_images)
   void* d_wimg = nullptr;     // fp32 d in {16, 32, 64}: shared-memory image of W / W^T hi|lo (tcd_build_images)
-  // launch chain of the fused d = 8 tcgen05 kernels (lstm_f32_tc.cu)
-  uint32_t* d_chain = nullptr;  // per-tile completion epochs
-  int64_t chain_tiles = 0;
-  uint32_t chain_epoch = 0;     // the last epoch handed out
-  bool chain_open = false;      // the cell's last launch was a fused tc launch ...
-  bool chain_prev = false;      // ... as seen at the entry of the current API call
-  void* chain_stream = nullptr; // ... on this stream
   size_t scratch_bytes = 0;
+  // launch chain of the tensor-core kernels (chain.cuh): per-tile completion
+  // epochs, one flag array per stream the cell launches on (launches on
+  // different streams never share flags)
+  struct ChainSlot {
+    void* stream = nullptr;
+    uint32_t* flags = nullptr;
+    int64_t tiles = 0;
+    uint32_t epoch = 0;  // the last epoch handed out on this stream
+  };
+  ChainSlot chain_slots[4];
+  int chain_victim = 0;
+  bool chain_prev = false;            // the process's last cell launch was a chain-publishing
+  void* chain_prev_stream = nullptr;  // launch of this cell, on this stream (chain_touch;
+                                      // 0 is a valid stream handle: the legacy default stream)
 };
 
 namespace ackpt {
@@ -68,13 +76,38 @@ void f32_forward_many(const ackpt_lstm* c, int64_t from, int count, const float*
 template <int D>
 void f32_backward_many(const ackpt_lstm* c, int64_t from, int count, const float* const* states,
                        const float* adj_in, float* adj_out, cudaStream_t s);
-// Launch chain bookkeeping: every API entry point calls chain_touch first
-// (a non-tc launch of the cell then leaves the chain closed).
-inline void chain_touch(const ackpt_lstm* c) {
-  auto* m = const_cast<ackpt_lstm*>(c);
-  m->chain_prev = m->chain_open;
-  m->chain_open = false;
+// Launch chain bookkeeping.  The process-wide token names the (cell, stream)
+// of the last cell launch if it was a tensor-core launch that publishes tile
+// flags; every cell API entry point calls chain_touch first, which hands the
+// token to the cell if it is its own and clears it -- so a launch can only be
+// chained to the immediately preceding launch of ANY cell, on the same
+// stream (another cell's or a non-chain kernel in between breaks the chain).
+struct ChainToken {
+  std::mutex mu;
+  const ackpt_lstm* cell = nullptr;
+  void* stream = nullptr;
+};
+inline ChainToken& chain_token() {
+  static ChainToken t;
+  return t;
 }
+inline void chain_touch(const ackpt_lstm* c) {
+  auto& t = chain_token();
+  std::lock_guard<std::mutex> lk(t.mu);
+  auto* m = const_cast<ackpt_lstm*>(c);
+  m->chain_prev = t.cell == c;
+  m->chain_prev_stream = t.stream;
+  t.cell = nullptr;
+  t.stream = nullptr;
+}
+inline void chain_publish(const ackpt_lstm* c, void* stream) {
+  auto& t = chain_token();
+  std::lock_guard<std::mutex> lk(t.mu);
+  t.cell = c;
+  t.stream = stream;
+}
+// Frees the cell's flag arrays (after a device synchronization).
+void chain_release(ackpt_lstm* c);
 // Tensor-core (tcgen05, 3xTF32) fused kernels, d = 8 (lstm_f32_tc.cu).
 void tc_advance(const ackpt_lstm* c, int64_t from, int count, const float* in, float* out, cudaStream_t s);
 void tc_forward_many(const ackpt_lstm* c, int64_t from, int count, const float* in, float* const* outs,

@@ -24,6 +24,7 @@ unsigned tc_grid(int64_t B) { return unsigned((B + tc::kTile - 1) / tc::kTile); 
 }  // namespace
 
 thread_local int g_chain_hint = 0;
+thread_local int g_chain_native = 0;
 
 void tc_advance(const ackpt_lstm* c, int64_t from, int count, const float* in, float* out, cudaStream_t s) {
   tc::OutPtrs none{};

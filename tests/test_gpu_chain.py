@@ -21,12 +21,14 @@ def _run(mode):
     out = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "chain_probe.py")], env=env,
                          capture_output=True, text=True, timeout=600)
     assert out.returncode == 0, out.stderr[-3000:]
-    line = [x for x in out.stdout.splitlines() if x.startswith("chain_probe ok")][-1]
-    return line.split("digest")[-1].strip()
+    line = [x for x in out.stdout.splitlines() if x.startswith("chain_probe ok")][-1].split()
+    return line[line.index("direct") + 1], line[line.index("engine") + 1]
 
 
 @pytest.mark.gpu
 def test_chained_launches_bit_identical():
-    plain = _run("0")
-    assert _run(None) == plain
-    assert _run("force") == plain
+    plain_direct, plain_engine = _run("0")
+    direct, engine = _run(None)
+    assert (direct, engine) == (plain_direct, plain_engine)
+    forced_direct, _ = _run("force")
+    assert forced_direct == plain_direct
