@@ -38,6 +38,7 @@
 #include <vector>
 
 #include "common.h"
+#include "nvtx.h"
 
 namespace ackpt {
 // tier.cpp
@@ -341,6 +342,7 @@ struct Run {
   // -- transfers ------------------------------------------------------------
   void wait_transfer(ackpt_ticket t, int64_t at_step) {
     // runtime.py:192-199.  Errors captured by the transfer surface here.
+    NvtxRange range("wait");
     if (dry) {
       next_ev += 2;
       return;
@@ -376,6 +378,7 @@ struct Run {
   }
 
   ackpt_ticket begin_store(int64_t key, int state) {
+    NvtxRange range("store");
     chainable = false;
     ackpt_ticket t = -1;
     if (!dry) {
@@ -389,6 +392,7 @@ struct Run {
   }
 
   ackpt_ticket begin_fetch(int64_t key, int dst) {
+    NvtxRange range("fetch");
     chainable = false;
     ackpt_ticket t = -1;
     if (!dry) {
@@ -544,6 +548,7 @@ struct Run {
 
   // -- multistage (runtime.py:269-322) ----------------------------------------
   int multistage_forward(int state) {
+    NvtxRange range("sweep");
     const auto& bs = E->boundaries;
     ackpt_ticket ticket = -1;
     int store_src = -2;
@@ -572,6 +577,7 @@ struct Run {
   }
 
   void multistage_backward() {
+    NvtxRange range("backward");
     const bool pf = E->prefetch < 0 ? env_prefetch() : E->prefetch != 0;
     const auto& bs = E->boundaries;
     const size_t nseg = bs.size();
@@ -593,6 +599,7 @@ struct Run {
       if (pf && jj > 0) issue(bs[jj - 1]);
       ledger.drop_transfer(E->S);  // fetched bytes go live
       const SegPlan& plan = E->seg_by_len.at(end - start);
+      NvtxRange seg(dry ? std::string() : "segment " + std::to_string(start) + "-" + std::to_string(end));
       int last = run_schedule(plan, start, tk.second);
       release(last);
     }
@@ -704,6 +711,7 @@ void run_impl(ackpt_engine* E, Mode mode, const void* initial_state, const void*
   ACKPT_CUDA_CHECK(cudaEventRecord(E->ev_sync, caller));
   ACKPT_CUDA_CHECK(cudaStreamWaitEvent(E->compute, E->ev_sync, 0));
 
+  NvtxRange range(mode == Mode::kFull ? "pass" : mode == Mode::kForwardSweep ? "forward_sweep" : "backward_sweep");
   Run r(E, false, E->compute);
   r.ext = initial_state;
   r.seed_bytes = seed;
@@ -715,11 +723,13 @@ void run_impl(ackpt_engine* E, Mode mode, const void* initial_state, const void*
   }
   auto t0 = std::chrono::steady_clock::now();
   if (replay) {
+    NvtxRange gr("graph replay");
     for (ackpt_ticket tk : G.issued) tier_reset_async(E->tier, tk);
     ACKPT_CUDA_CHECK(cudaEventRecord(E->ev_start, E->compute));
     ACKPT_CUDA_CHECK(cudaGraphLaunch(G.exec, E->compute));
     ACKPT_CUDA_CHECK(cudaEventRecord(E->ev_end, E->compute));
   } else if (capture) {
+    NvtxRange gc("graph capture");
     r.capturing = true;
     if (E->tier) tier_quiesce(E->tier);
     cudaGraph_t graph = nullptr;
@@ -864,6 +874,7 @@ ACKPT_API int ackpt_engine_prepare(ackpt_engine* E, int32_t strategy, int64_t sl
                                    int64_t interval, ackpt_tier* tier) {
   return ackpt::guard([&] {
     using namespace ackpt;
+    NvtxRange range("prepare");
     E->prepared = false;
     E->drop_graph();
     E->strategy = strategy;
@@ -998,6 +1009,7 @@ ACKPT_API int ackpt_engine_calibrate(ackpt_engine* E, ackpt_tier* tier, int64_t 
                                      double* t_t) {
   return ackpt::guard([&] {
     using namespace ackpt;
+    NvtxRange range("calibrate");
     if (trials < 3) fail(ACKPT_VALUE_ERROR, "trial_steps must be >= 3, got " + std::to_string(trials));
     if (!tier) fail(ACKPT_VALUE_ERROR, "calibrate requires a Level-2 backend");
     cudaStream_t s = E->compute;

@@ -31,6 +31,7 @@
 #include <vector>
 
 #include "common.h"
+#include "nvtx.h"
 
 namespace ackpt {
 
@@ -342,6 +343,7 @@ uint32_t payload_io(int fd, unsigned char* buf, int64_t len, uint32_t reg, bool 
 // replaced file's second name is returned in `*retired` for the caller to
 // unlink off the critical path (null: a detached thread unlinks it).
 void write_ckpt(TierTicket* tk, std::string* retired_out = nullptr) {
+  NvtxRange range("ckpt write");
   ackpt_tier* t = tk->tier;
   unsigned char header[kHeader];
   std::memcpy(header, "CKPT", 4);
@@ -413,6 +415,7 @@ void CUDART_CB file_store_cb(void* arg) { write_ckpt(static_cast<TierTicket*>(ar
 // Read + verify the ticket's CKPT file into stage_in (decode_checkpoint /
 // read_checkpoint_file, storage.py:83-127).  Errors go to tk->async.
 void read_ckpt(TierTicket* tk) {
+  NvtxRange range("ckpt read");
   ackpt_tier* t = tk->tier;
   static const bool trace = std::getenv("ACKPT_FILE_TRACE") != nullptr;
   const auto c0 = std::chrono::steady_clock::now();
