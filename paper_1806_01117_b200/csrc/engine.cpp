@@ -152,6 +152,36 @@ struct Run {
   // buffer pool
   std::vector<int> refs;
   std::vector<int> free_list;
+  // Stream-ordering check (SURVEY §5 race detection, always on, host side):
+  // a buffer a store reads or a fetch writes is in flight from begin_store /
+  // begin_fetch until its wait_transfer.  Returning it to the pool, handing
+  // it out, or enqueueing a kernel that reads a fetch destination or writes
+  // an in-flight buffer before that wait is a protocol error (ExecutionError)
+  // -- the host-side counterpart of ACKPT_POISON's device-side NaN check.
+  enum : int8_t { kIdle = 0, kStoreSrc = 1, kFetchDst = 2 };
+  std::vector<int8_t> flight;
+  std::map<ackpt_ticket, int> flight_of;
+  ackpt_ticket dry_ticket = -2;  // distinct tickets in the dry run too
+  void flight_mark(ackpt_ticket t, int id, int8_t kind) {
+    if (id < 0) return;  // the caller's input: read-only, never pooled
+    if (size_t(id) >= flight.size()) flight.resize(size_t(id) + 1, kIdle);
+    if (flight[size_t(id)] != kIdle) order_error(id, "second transfer on a buffer already in flight");
+    flight[size_t(id)] = kind;
+    flight_of[t] = id;
+  }
+  void flight_clear(ackpt_ticket t) {
+    auto it = flight_of.find(t);
+    if (it == flight_of.end()) return;
+    flight[size_t(it->second)] = kIdle;
+    flight_of.erase(it);
+  }
+  int8_t flight_state(int id) const {
+    return id >= 0 && size_t(id) < flight.size() ? flight[size_t(id)] : int8_t(kIdle);
+  }
+  [[noreturn]] void order_error(int id, const char* what) const {
+    fail(ACKPT_EXECUTION_ERROR, std::string("stream-ordering check: ") + what + " (pool buffer " +
+                                    std::to_string(id) + ")");
+  }
   int in_use = 0, peak_in_use = 0;
   const void* ext = nullptr;
   // adjoint
@@ -209,6 +239,7 @@ struct Run {
     }
     int id = free_list.back();
     free_list.pop_back();
+    if (flight_state(id) != kIdle) order_error(id, "buffer handed out while a transfer uses it");
     refs[size_t(id)] = 1;
     peak_in_use = std::max(peak_in_use, ++in_use);
     return id;
@@ -219,6 +250,7 @@ struct Run {
   void release(int id) {
     if (id < 0) return;
     if (--refs[size_t(id)] == 0) {
+      if (flight_state(id) != kIdle) order_error(id, "buffer released before its transfer was waited");
       free_list.push_back(id);
       --in_use;
       // ACKPT_POISON=1 (race check): a released buffer is filled
@@ -232,6 +264,15 @@ struct Run {
       }
     }
   }
+  // ACKPT_FAULT_ORDER=1 (test only, tests/test_gpu_poison.py): the forward
+  // sweep does not hold a boundary state while its store is in flight.
+  static bool fault_skip_hold() {
+    static const bool on = [] {
+      const char* v = std::getenv("ACKPT_FAULT_ORDER");
+      return v && v[0] == '1';
+    }();
+    return on;
+  }
   static bool poison() {
     static const bool on = [] {
       const char* v = std::getenv("ACKPT_POISON");
@@ -239,8 +280,16 @@ struct Run {
     }();
     return on;
   }
-  const void* ptr(int id) const { return id == kExt ? ext : E->bufs[size_t(id)]; }
-  void* wptr(int id) const { return E->bufs[size_t(id)]; }
+  // Buffer addresses for enqueued work: kernels may not read a fetch
+  // destination, nor write any in-flight buffer, before its wait.
+  const void* ptr(int id) const {
+    if (flight_state(id) == kFetchDst) order_error(id, "read of a fetch destination before its wait");
+    return id == kExt ? ext : E->bufs[size_t(id)];
+  }
+  void* wptr(int id) const {
+    if (flight_state(id) != kIdle) order_error(id, "write to a buffer while a transfer uses it");
+    return E->bufs[size_t(id)];
+  }
 
   cudaEvent_t timing_event() {
     if (dry) {
@@ -343,6 +392,7 @@ struct Run {
   void wait_transfer(ackpt_ticket t, int64_t at_step) {
     // runtime.py:192-199.  Errors captured by the transfer surface here.
     NvtxRange range("wait");
+    flight_clear(t);
     if (dry) {
       next_ev += 2;
       return;
@@ -380,12 +430,13 @@ struct Run {
   ackpt_ticket begin_store(int64_t key, int state) {
     NvtxRange range("store");
     chainable = false;
-    ackpt_ticket t = -1;
+    ackpt_ticket t = dry_ticket--;
     if (!dry) {
       check_op(ackpt_tier_begin_store(E->tier, key, key, ptr(state), E->S, s, &t));
       issued.push_back(t);
       if (E->timeline) xfers.push_back({ACKPT_EV_STORE, key, t});
     }
+    flight_mark(t, state, kStoreSrc);
     ++st.stores_issued;
     st.link_bytes += E->S;
     return t;
@@ -394,13 +445,14 @@ struct Run {
   ackpt_ticket begin_fetch(int64_t key, int dst) {
     NvtxRange range("fetch");
     chainable = false;
-    ackpt_ticket t = -1;
+    ackpt_ticket t = dry_ticket--;
     if (!dry) {
       int rc = ackpt_tier_begin_fetch(E->tier, key, wptr(dst), E->S, s, &t);
       if (rc != ACKPT_OK) fail(rc, ackpt_last_error());
       issued.push_back(t);
       if (E->timeline) xfers.push_back({ACKPT_EV_FETCH, key, t});
     }
+    flight_mark(t, dst, kFetchDst);
     ++st.prefetches_issued;
     st.link_bytes += E->S;
     return t;
@@ -561,7 +613,7 @@ struct Run {
         release(store_src);
       }
       ticket = begin_store(b, state);
-      retain(state);
+      if (!fault_skip_hold()) retain(state);  // (test switch: drop the hold, the ordering check must fire)
       store_src = state;
       have = true;
       ledger.add_transfer(E->S);

@@ -37,3 +37,27 @@ def test_poisoned_pool_is_bit_identical():
     plain = _run(False)
     poisoned = _run(True)
     assert plain == poisoned
+
+
+@pytest.mark.gpu
+def test_ordering_check_fires_on_a_missing_hold():
+    """The executor's host-side stream-ordering check (engine.cpp, always on):
+    with ACKPT_FAULT_ORDER=1 the forward sweep drops its hold on a boundary
+    state whose store is still in flight, and the pass must fail with the
+    check's ExecutionError instead of racing the copy engine."""
+    code = (
+        "import paper_1806_01117_b200 as pkg, paper_1806_01117_b200.lstm as lstm\n"
+        "ops = lstm.operator_pair(lstm.long_memory_cell(8, 60, 0), 4096, 'f32')\n"
+        "s0 = lstm.random_states(8, 1, 4096, 'f32')\n"
+        "try:\n"
+        "    with pkg.PinnedHostBackend(slot_bytes=ops.state_size) as b:\n"
+        "        pkg.execute(pkg.Multistage(8, 10), ops, s0, b, fuse=True)\n"
+        "    print('NO ERROR')\n"
+        "except pkg.ExecutionError as e:\n"
+        "    print('RAISED', e)\n"
+    )
+    env = dict(os.environ, ACKPT_FAULT_ORDER="1")
+    out = subprocess.run([sys.executable, "-c", code], env=env, cwd=ROOT, capture_output=True, text=True,
+                         timeout=300)
+    assert out.returncode == 0, out.stderr[-3000:]
+    assert "RAISED" in out.stdout and "stream-ordering check" in out.stdout, out.stdout
