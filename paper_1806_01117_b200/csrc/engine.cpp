@@ -421,9 +421,12 @@ struct Run {
   bool chainable = false;
   template <class F>
   void fused_launch(F&& launch) {
-    g_chain_hint = (chainable && !E->timeline && E->sample_every == 0) ? 1 : 0;
+    struct Hint {  // reset on every exit, exceptions included
+      explicit Hint(int on) { g_chain_hint = on; }
+      ~Hint() { g_chain_hint = 0; }
+    } hint((chainable && !E->timeline && E->sample_every == 0) ? 1 : 0);
+    chainable = false;
     launch();
-    g_chain_hint = 0;
     chainable = true;
   }
 
