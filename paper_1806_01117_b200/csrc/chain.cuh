@@ -63,13 +63,17 @@ __device__ __forceinline__ void wait_tile(const Chain& ch, int64_t t, int leader
   // bulk-copy (async-proxy) reads of the same data
   asm volatile("fence.proxy.async.global;" ::: "memory");
 }
-// CTA-wide publish of tile t (after this launch's last access of it).
+// CTA-wide publish of tile t (after this launch's last access of it): the
+// barrier orders every thread's accesses before the leader's gpu-scope
+// release fence (cumulative), so only the leader fences -- a per-thread
+// __threadfence() made every warp wait for its stores to drain, once per
+// tile of a persistent kernel.
 __device__ __forceinline__ void set_tile(const Chain& ch, int64_t t, int leader, int id = 0, int nthreads = 0) {
   if (!ch.flags) return;
-  __threadfence();  // this thread's stores, device-wide, before the flag
   sync_group(id, nthreads);
   if (int(threadIdx.x) == leader)
-    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(ch.flags + t), "r"(ch.set) : "memory");
+    asm volatile("fence.acq_rel.gpu;\n\tst.relaxed.gpu.global.u32 [%0], %1;" ::"l"(ch.flags + t), "r"(ch.set)
+                 : "memory");
 }
 
 // Coherent (L2) loads for inputs a chained predecessor may have written
