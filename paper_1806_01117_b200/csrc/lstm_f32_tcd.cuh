@@ -326,10 +326,14 @@ __global__ void __launch_bounds__(kThreads, D == 16 ? 6 : D == 32 ? 4 : 1)  // r
   chain::wait_tile(ch, tile, 0);
   const int64_t b = tile * kThreads + threadIdx.x;
   const bool live = b < B;
+  // d = 64 (one CTA per SM, latency-bound): c is loaded after the first gate
+  // MMAs are issued, overlapping them (36.1 vs 37.4 us per step); at d = 16 /
+  // 32 the later loads cost more than they hide (measured, not kept)
+  constexpr bool kLateC = D == 64;
   float2 h[D / 2], c[D / 2];
   if (live) {
     load_rows<D>(in, B, b, 0, h);
-    load_rows<D>(in, B, b, D, c);
+    if (!kLateC) load_rows<D>(in, B, b, D, c);
   } else {
 #pragma unroll
     for (int p = 0; p < D / 2; ++p) h[p] = c[p] = make_float2(0.f, 0.f);
@@ -341,6 +345,7 @@ __global__ void __launch_bounds__(kThreads, D == 16 ? 6 : D == 32 ? 4 : 1)  // r
       weights_ready(bars + 1, wready);
       issue_gates<D>(sm, tmem, bars);
     }
+    if (kLateC && i == 0 && live) load_rows<D>(in, B, b, D, c);
     wait_bar(bars, ph & 1u);
 #pragma unroll
     for (int p0 = 0; p0 < D / 2; p0 += 4) {  // 4 unit pairs per TMEM round trip
