@@ -649,6 +649,19 @@ def main(argv=None) -> None:
         if S != 64 << 20 or (args.fuse and fk_steps != 64):
             traffic = None  # the ncu captures are of the config-2 launch shape
         pipes = tj.get("pipes", {}).get(f"{base}@{kfam}", tj.get("pipes", {}).get(base))
+    # issue-bound roofline of the dominant fused launch: its ncu instruction
+    # count (scaled to this batch and launch length) at one warp instruction
+    # per SMSP per cycle at the maximum SM clock, against the measured time
+    issue = None
+    if args.fuse and pipes and pipes.get("inst_per_launch"):
+        inst = pipes["inst_per_launch"] * (args.batch / pipes["inst_batch"]) * (fk_steps / pipes["inst_steps"])
+        smsps = 4 * torch.cuda.get_device_properties(0).multi_processor_count
+        clk = float(peaks.get("sm_max_mhz", 1965.0)) * 1e6
+        floor = inst / (smsps * clk)
+        issue = {"instructions_per_launch": inst, "floor_us": floor * 1e6, "measured_us": t_dom * 1e6,
+                 "frac": floor / t_dom,
+                 "how": "ncu smsp__inst_executed.sum of the launch (profiles/ncu_traffic.json pipes) / "
+                        "(4 x SMs x sm_max_mhz): the time at 100 % issue; frac = floor / measured"}
     link_gbs = S / t_t / 1e9
     # phase-wise pass roofline: sum over phases of max(HBM, link)
     pb = fused_pass_bytes(args.n, pkg.plan_multistage(args.n, slots, interval).boundaries, S, args.fuse, last)
@@ -801,6 +814,7 @@ def main(argv=None) -> None:
                          "timing": "CUDA events around back-to-back launches of the same kernel",
                          "peak_source": peak_src,
                          "binding_pipes": pipes,
+                         "issue_bound": issue,
                          "note": ("the fused launches are compute bound (FMA / MUFU issue, see binding_pipes "
                                   "from ncu); frac is their HBM fraction, not a pipe fraction")
                          if args.fuse else "per-step kernels: HBM bound"},
