@@ -33,7 +33,8 @@ struct ackpt_lstm {
     void* stream = nullptr;
     uint32_t* flags = nullptr;
     int64_t tiles = 0;
-    uint32_t epoch = 0;  // the last epoch handed out on this stream
+    int64_t last_tiles = 0;  // tile count of the last launch (chains only between equal tilings)
+    uint32_t epoch = 0;      // the last epoch handed out on this stream
   };
   ChainSlot chain_slots[4];
   int chain_victim = 0;
