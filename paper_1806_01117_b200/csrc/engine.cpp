@@ -345,7 +345,7 @@ struct Run {
     int out = acquire();
     span(ACKPT_EV_FORWARD, step, step + 1, [&] {
       timed(fwd_calls, fwd_pairs, [&] {
-        fused_launch([&] { check_op(E->op.forward(E->op.ctx, step, ptr(cur), wptr(out), s)); });
+        step_launch([&] { check_op(E->op.forward(E->op.ctx, step, ptr(cur), wptr(out), s)); });
         ++st.kernel_launches;
       });
     });
@@ -362,7 +362,7 @@ struct Run {
     if (to - from >= 1 && E->fuse && E->op.advance) {
       int out = acquire();
       span(ACKPT_EV_FORWARD, from, to, [&] {
-        fused_launch([&] { check_op(E->op.advance(E->op.ctx, from, to, ptr(cur), wptr(out), s)); });
+        step_launch([&] { check_op(E->op.advance(E->op.ctx, from, to, ptr(cur), wptr(out), s)); });
         ++st.kernel_launches;
       });
       release(cur);
@@ -380,7 +380,7 @@ struct Run {
       fail(ACKPT_EXECUTION_ERROR, "Reverse " + std::to_string(step) + " before the adjoint was seeded");
     span(ACKPT_EV_BACKWARD, step, step + 1, [&] {
       timed(bwd_calls, bwd_pairs, [&] {
-        fused_launch([&] { check_op(E->op.backward(E->op.ctx, step, ptr(state), adj[a], adj[1 - a], s)); });
+        step_launch([&] { check_op(E->op.backward(E->op.ctx, step, ptr(state), adj[a], adj[1 - a], s)); });
         ++st.kernel_launches;
       });
     });
@@ -420,7 +420,7 @@ struct Run {
   // every other enqueue (waits, transfers, seeds, poison fills).
   bool chainable = false;
   template <class F>
-  void fused_launch(F&& launch) {
+  void step_launch(F&& launch) {
     struct Hint {  // reset on every exit, exceptions included
       explicit Hint(int on) { g_chain_hint = on; }
       ~Hint() { g_chain_hint = 0; }
@@ -504,7 +504,7 @@ struct Run {
               ledger.add_tape(E->S);
             }
             span(ACKPT_EV_FORWARD, offset + rel, offset + rel + cnt, [&] {
-              fused_launch([&] { check_op(E->op.forward_many(E->op.ctx, offset + rel, cnt, ptr(state), outs, s)); });
+              step_launch([&] { check_op(E->op.forward_many(E->op.ctx, offset + rel, cnt, ptr(state), outs, s)); });
               ++st.kernel_launches;
             });
             release(state);
@@ -574,7 +574,7 @@ struct Run {
           ledger.drop_tape(E->S);
         }
         span(ACKPT_EV_BACKWARD, offset + lo, offset + lo + int64_t(run), [&] {
-          fused_launch([&] { check_op(E->op.backward_many(E->op.ctx, offset + lo, int64_t(run), states, adj[a], adj[1 - a], s)); });
+          step_launch([&] { check_op(E->op.backward_many(E->op.ctx, offset + lo, int64_t(run), states, adj[a], adj[1 - a], s)); });
           ++st.kernel_launches;
         });
         a = 1 - a;
