@@ -430,9 +430,25 @@ __global__ void __launch_bounds__(kThreads)
 #pragma unroll
     for (int p = 0; p < D / 2; ++p) dh[p] = dc[p] = make_float2(0.f, 0.f);
   }
+  // d = 32 (two CTAs per SM, set by TMEM, so registers are free): the taped
+  // state of the next step is loaded into registers while this step computes
+  constexpr bool kAhead = D == 32;
+  float2 hn[D / 2], cn[D / 2];
+  if (kAhead) {
+    if (live) {
+      load_rows<D>(states.p[count - 1], B, b, 0, hn);
+      load_rows<D>(states.p[count - 1], B, b, D, cn);
+    } else {
+#pragma unroll
+      for (int p = 0; p < D / 2; ++p) hn[p] = cn[p] = make_float2(0.f, 0.f);
+    }
+  }
   for (int i = count - 1; i >= 0; --i, ++phase) {
     float2 h[D / 2], c[D / 2];
-    if (live) {
+    if (kAhead) {
+#pragma unroll
+      for (int p = 0; p < D / 2; ++p) h[p] = hn[p], c[p] = cn[p];
+    } else if (live) {
       load_rows<D>(states.p[i], B, b, 0, h);
       load_rows<D>(states.p[i], B, b, D, c);
     } else {
@@ -444,6 +460,10 @@ __global__ void __launch_bounds__(kThreads)
     if (threadIdx.x == 0) {
       weights_ready(bars + 2, wready);
       issue_gates<D>(sm, tmem, bars);
+    }
+    if (kAhead && live && i > 0) {
+      load_rows<D>(states.p[i - 1], B, b, 0, hn);
+      load_rows<D>(states.p[i - 1], B, b, D, cn);
     }
     wait_bar(bars, phase & 1u);
 #pragma unroll
