@@ -116,6 +116,7 @@ inline int mode() {
 inline Chain next(const ackpt_lstm* c, cudaStream_t s, int64_t tiles, bool& pdl) {
   auto* cell = const_cast<ackpt_lstm*>(c);
   pdl = false;
+  std::lock_guard<std::mutex> lk(chain_token().mu);  // the cell's slots and the token
   cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
   ACKPT_CUDA_CHECK(cudaStreamIsCapturing(s, &cs));
   const int m = mode();
@@ -136,7 +137,9 @@ inline Chain next(const ackpt_lstm* c, cudaStream_t s, int64_t tiles, bool& pdl)
       slot->flags = nullptr;
     }
     ACKPT_CUDA_CHECK(cudaMalloc(&slot->flags, size_t(tiles) * sizeof(uint32_t)));
-    ACKPT_CUDA_CHECK(cudaMemset(slot->flags, 0, size_t(tiles) * sizeof(uint32_t)));
+    // on the launch stream: a legacy-stream memset is not ordered before work
+    // on a non-blocking stream and could land after the first flag publish
+    ACKPT_CUDA_CHECK(cudaMemsetAsync(slot->flags, 0, size_t(tiles) * sizeof(uint32_t), s));
     slot->stream = s;
     slot->tiles = tiles;
     slot->epoch = 0;
@@ -148,7 +151,8 @@ inline Chain next(const ackpt_lstm* c, cudaStream_t s, int64_t tiles, bool& pdl)
   slot->last_tiles = tiles;
   Chain ch{slot->flags, chained ? slot->epoch : 0u, slot->epoch + 1};
   if (++slot->epoch == 0) slot->epoch = 1;  // (flags compare by signed distance)
-  chain_publish(c, s);
+  chain_token().cell = c;  // this launch is now the last cell launch
+  chain_token().stream = s;
   pdl = chained;
   return ch;
 }

@@ -101,12 +101,6 @@ inline void chain_touch(const ackpt_lstm* c) {
   t.cell = nullptr;
   t.stream = nullptr;
 }
-inline void chain_publish(const ackpt_lstm* c, void* stream) {
-  auto& t = chain_token();
-  std::lock_guard<std::mutex> lk(t.mu);
-  t.cell = c;
-  t.stream = stream;
-}
 // Frees the cell's flag arrays (after a device synchronization).
 void chain_release(ackpt_lstm* c);
 // Tensor-core (tcgen05, 3xTF32) fused kernels, d = 8 (lstm_f32_tc.cu).
