@@ -681,7 +681,10 @@ void alloc_pool(ackpt_engine* E, int64_t need_bufs, size_t need_events) {
     E->slabs.push_back(slab);
     for (int64_t i = 0; i < add; ++i)
       E->bufs.push_back(static_cast<char*>(slab) + size_t(i) * size_t(E->S));
-    if (Run::poison()) ACKPT_CUDA_CHECK(cudaMemset(slab, 0xFF, size_t(add) * size_t(E->S)));  // never-written = NaN
+    if (Run::poison()) {  // never-written = NaN; complete before the (non-blocking) compute stream uses it
+      ACKPT_CUDA_CHECK(cudaMemset(slab, 0xFF, size_t(add) * size_t(E->S)));
+      ACKPT_CUDA_CHECK(cudaDeviceSynchronize());
+    }
   }
   if (!E->adj_internal) ACKPT_CUDA_CHECK(cudaMalloc(&E->adj_internal, size_t(E->S)));
   while (E->timing.size() < need_events) {

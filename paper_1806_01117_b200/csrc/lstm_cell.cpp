@@ -190,6 +190,9 @@ ACKPT_API int ackpt_lstm_create(int32_t d, int64_t n_steps, int64_t batch, int32
         ackpt::tcd_build_images(c.get());  // shared-memory weight images, complete before any launch
       }
     }
+    // pageable-host uploads may still be in flight on the legacy stream when
+    // cudaMemcpy returns; the step kernels run on other (non-blocking) streams
+    ACKPT_CUDA_CHECK(cudaDeviceSynchronize());
     *out = c.release();
   });
 }
