@@ -360,6 +360,12 @@ ACKPT_API int ackpt_engine_set_timeline(ackpt_engine* engine, int32_t on);
 ACKPT_API int ackpt_engine_timeline(const ackpt_engine* engine, ackpt_timeline_event* out, int64_t cap,
                                     int64_t* len);
 
+/* ---- launch chain of the tensor-core kernels (no reference counterpart) ----
+ * Host-only self-test of the chain bookkeeping (which launch may chain to
+ * which: same cell, same stream, adjacent, equal tilings, marked); 0 = pass,
+ * else ACKPT_EXECUTION_ERROR with the failing case in ackpt_last_error(). */
+ACKPT_API int ackpt_chain_selftest(void);
+
 /* ---- CRC32C (storage.py:49-68), hardware crc32 instruction when present ---- */
 ACKPT_API uint32_t ackpt_crc32c(const void* data, int64_t len, uint32_t crc);
 

@@ -194,6 +194,7 @@ _SIGS = {
     "ackpt_engine_set_graph": ([_vp, C.c_int32], C.c_int),
     "ackpt_engine_timeline": ([_vp, C.POINTER(TimelineEvent), C.c_int64, _i64p], C.c_int),
     "ackpt_crc32c": ([_vp, C.c_int64, C.c_uint32], C.c_uint32),
+    "ackpt_chain_selftest": ([], C.c_int),
 }
 
 for _name, (_args, _res) in _SIGS.items():

@@ -121,40 +121,20 @@ inline Chain next(const ackpt_lstm* c, cudaStream_t s, int64_t tiles, bool& pdl)
   ACKPT_CUDA_CHECK(cudaStreamIsCapturing(s, &cs));
   const int m = mode();
   if (m == 0 || cs != cudaStreamCaptureStatusNone) return Chain{nullptr, 0u, 0u};  // the chain stays closed
-  ackpt_lstm::ChainSlot* slot = nullptr;
-  for (auto& sl : cell->chain_slots)
-    if (sl.flags && sl.stream == static_cast<void*>(s)) slot = &sl;
-  bool fresh = false;
-  if (!slot || slot->tiles < tiles) {
-    if (!slot) {
-      for (auto& sl : cell->chain_slots)
-        if (!sl.flags && !slot) slot = &sl;
-      if (!slot) slot = &cell->chain_slots[cell->chain_victim++ % 4];
-    }
-    if (slot->flags) {  // evicted or too small: no kernel may still use it
+  const ChainStep st = chain_step(cell, s, tiles, m == 2 || g_chain_native, [&](uint32_t* old, int64_t n) {
+    if (old) {  // evicted or too small: no kernel may still use it
       ACKPT_CUDA_CHECK(cudaDeviceSynchronize());
-      cudaFree(slot->flags);
-      slot->flags = nullptr;
+      cudaFree(old);
     }
-    ACKPT_CUDA_CHECK(cudaMalloc(&slot->flags, size_t(tiles) * sizeof(uint32_t)));
+    uint32_t* p = nullptr;
+    ACKPT_CUDA_CHECK(cudaMalloc(&p, size_t(n) * sizeof(uint32_t)));
     // on the launch stream: a legacy-stream memset is not ordered before work
     // on a non-blocking stream and could land after the first flag publish
-    ACKPT_CUDA_CHECK(cudaMemsetAsync(slot->flags, 0, size_t(tiles) * sizeof(uint32_t), s));
-    slot->stream = s;
-    slot->tiles = tiles;
-    slot->epoch = 0;
-    fresh = true;
-  }
-  // (tile t must cover the same sequences in both launches: equal tile counts)
-  const bool chained = !fresh && slot->last_tiles == tiles && (m == 2 || g_chain_native) && cell->chain_prev &&
-                       cell->chain_prev_stream == static_cast<void*>(s);
-  slot->last_tiles = tiles;
-  Chain ch{slot->flags, chained ? slot->epoch : 0u, slot->epoch + 1};
-  if (++slot->epoch == 0) slot->epoch = 1;  // (flags compare by signed distance)
-  chain_token().cell = c;  // this launch is now the last cell launch
-  chain_token().stream = s;
-  pdl = chained;
-  return ch;
+    ACKPT_CUDA_CHECK(cudaMemsetAsync(p, 0, size_t(n) * sizeof(uint32_t), s));
+    return p;
+  });
+  pdl = st.chained;
+  return Chain{st.flags, st.wait, st.set};
 }
 
 // kernel<<<grid, block, smem, s>>>(args...), as a programmatic dependent

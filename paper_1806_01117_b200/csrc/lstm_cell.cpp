@@ -437,6 +437,64 @@ ACKPT_API int ackpt_set_fused_family(int32_t family) {
 
 ACKPT_API int32_t ackpt_get_fused_family(void) { return ackpt::family(); }
 
+ACKPT_API int ackpt_chain_selftest(void) {
+  // The launch-chain bookkeeping (chain_touch / chain_step, lstm_cell.h) on
+  // host-only cells with a fake flag allocator: no CUDA call is made.
+  return ackpt::guard([&] {
+    using namespace ackpt;
+    static uint32_t fake[4][64];
+    int allocs = 0, frees = 0;
+    auto alloc = [&](uint32_t* old, int64_t) {
+      if (old) ++frees;
+      return fake[allocs++ % 4];
+    };
+    ackpt_lstm A, Bc;
+    void* s1 = reinterpret_cast<void*>(0x10);
+    void* s2 = reinterpret_cast<void*>(0x20);
+    void* s0 = nullptr;  // the legacy default stream is a valid handle
+    auto launch = [&](ackpt_lstm& c, void* s, int64_t tiles, bool marked) {
+      chain_touch(&c);  // every cell API entry
+      std::lock_guard<std::mutex> lk(chain_token().mu);
+      return chain_step(&c, s, tiles, marked, alloc);
+    };
+    auto expect = [&](bool ok, const char* what) {
+      if (!ok) fail(ACKPT_EXECUTION_ERROR, std::string("chain self-test: ") + what);
+    };
+    ChainStep a = launch(A, s1, 16, true);
+    expect(!a.chained && a.wait == 0 && a.set == 1, "first launch on a fresh slot is unchained");
+    ChainStep b = launch(A, s1, 16, true);
+    expect(b.chained && b.wait == a.set && b.set == a.set + 1 && b.flags == a.flags, "back-to-back launch chains");
+    expect(!launch(A, s1, 16, false).chained, "an unmarked launch never chains");
+    launch(A, s1, 16, true);
+    launch(Bc, s1, 16, true);  // another cell in between
+    expect(!launch(A, s1, 16, true).chained, "no chaining across another cell's launch");
+    expect(launch(A, s1, 16, true).chained, "chains again once adjacent");
+    expect(!launch(A, s2, 16, true).chained, "a new stream starts unchained (own slot)");
+    expect(!launch(A, s1, 16, true).chained, "no chaining across a launch on another stream");
+    expect(!launch(A, s1, 32, true).chained, "a larger tiling reallocates: unchained");
+    expect(!launch(A, s1, 16, true).chained, "different tile counts never chain");
+    expect(launch(A, s1, 16, true).chained, "equal tile counts chain again");
+    launch(A, s0, 16, true);
+    expect(launch(A, s0, 16, true).chained, "stream 0 chains with itself");
+    chain_touch(&Bc);  // e.g. a seed kernel of another cell
+    expect(!launch(A, s0, 16, true).chained, "any cell API call in between breaks the chain");
+    void* s3 = reinterpret_cast<void*>(0x30);
+    void* s4 = reinterpret_cast<void*>(0x40);
+    const int frees0 = frees;
+    launch(A, s3, 16, true);
+    launch(A, s4, 16, true);  // fifth stream: evicts a slot
+    expect(frees == frees0 + 1, "the fifth stream evicts one slot");
+    int live = 0;
+    for (auto& sl : A.chain_slots) live += sl.flags != nullptr;
+    expect(live == 4, "four slots at most");
+    {
+      std::lock_guard<std::mutex> lk(chain_token().mu);
+      chain_token().cell = nullptr;  // leave no host-only cell in the token
+      chain_token().stream = nullptr;
+    }
+  });
+}
+
 ACKPT_API int ackpt_lstm_operator(ackpt_lstm* cell, ackpt_operator* out) {
   return ackpt::guard([&] {
     out->ctx = cell;

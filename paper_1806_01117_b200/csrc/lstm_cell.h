@@ -103,6 +103,51 @@ inline void chain_touch(const ackpt_lstm* c) {
 }
 // Frees the cell's flag arrays (after a device synchronization).
 void chain_release(ackpt_lstm* c);
+
+// The chain bookkeeping of one launch, host only (chain.cuh's next() runs it
+// with a CUDA allocator, ackpt_chain_selftest with a fake one).  Caller holds
+// chain_token().mu and called chain_touch(cell) at the API entry.  Picks the
+// stream's flag slot -- (re)allocating it through alloc(old_flags, tiles) when
+// missing or too small, evicting round-robin when all four are taken -- and
+// decides: chained iff the slot is not fresh, the previous launch on it had
+// the same tile count, the launch is marked (executor mark or =force), and the
+// process's last cell launch was this cell's on this stream.
+struct ChainStep {
+  uint32_t* flags;
+  uint32_t wait, set;
+  bool chained;
+};
+template <class Alloc>
+ChainStep chain_step(ackpt_lstm* cell, void* s, int64_t tiles, bool marked, Alloc&& alloc) {
+  ackpt_lstm::ChainSlot* slot = nullptr;
+  for (auto& sl : cell->chain_slots)
+    if (sl.flags && sl.stream == s) slot = &sl;
+  bool fresh = false;
+  if (!slot || slot->tiles < tiles) {
+    if (!slot) {
+      for (auto& sl : cell->chain_slots)
+        if (!sl.flags && !slot) slot = &sl;
+      if (!slot) slot = &cell->chain_slots[cell->chain_victim++ % 4];
+    }
+    uint32_t* old = slot->flags;
+    slot->flags = nullptr;  // (stays empty if the allocation throws)
+    slot->flags = alloc(old, tiles);
+    slot->stream = s;
+    slot->tiles = tiles;
+    slot->last_tiles = 0;
+    slot->epoch = 0;
+    fresh = true;
+  }
+  // (tile t must cover the same sequences in both launches: equal tile counts)
+  const bool chained = !fresh && slot->last_tiles == tiles && marked && cell->chain_prev &&
+                       cell->chain_prev_stream == s;
+  slot->last_tiles = tiles;
+  ChainStep r{slot->flags, chained ? slot->epoch : 0u, slot->epoch + 1, chained};
+  if (++slot->epoch == 0) slot->epoch = 1;  // (flags compare by signed distance)
+  chain_token().cell = cell;  // this launch is now the last cell launch
+  chain_token().stream = s;
+  return r;
+}
 // Tensor-core (tcgen05, 3xTF32) fused kernels, d = 8 (lstm_f32_tc.cu).
 void tc_advance(const ackpt_lstm* c, int64_t from, int count, const float* in, float* out, cudaStream_t s);
 void tc_forward_many(const ackpt_lstm* c, int64_t from, int count, const float* in, float* const* outs,

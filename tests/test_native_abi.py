@@ -112,3 +112,11 @@ def test_best_split_is_smallest_argmin():
         for slots in (2, 3, 5, 12):
             if length > slots + 1:
                 assert MS.best_split(length, slots) == S.best_split(length, slots, table)
+
+
+def test_chain_bookkeeping_selftest():
+    """Launch-chain bookkeeping (csrc/lstm_cell.h chain_step), host only: which
+    launch may chain to which -- same cell and stream, adjacent, equal tile
+    counts, marked; per-stream flag slots with eviction; stream handle 0."""
+    rc = N.lib.ackpt_chain_selftest()
+    assert rc == 0, N.last_error()
